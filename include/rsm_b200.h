@@ -1,0 +1,165 @@
+/*
+ * rsm_b200.h -- C-ABI of the B200-native RSM (arXiv 1411.0814) hot path.
+ *
+ * Plain C types only (pointers, sizes, POD structs); no exceptions cross it.
+ * Every entry point returns an rsm_status (0 = ok) whose values are the
+ * reference's process exit codes (rsm::exit_code, include/rsm/error.hpp:38-46
+ * of the reference); rsm_last_error() gives the message.
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/proj):
+ *   rsm_decompose         <- rsm::decompose            include/rsm/solver.hpp:77, src/solver.cpp:119-146
+ *   rsm_make_trial_params <- rsm::trial_params         include/rsm/solver.hpp:36, src/harvest.cpp:11-35
+ *   rsm_select            <- attempt-order selection in harvest_gram (stage-1 parity hook)
+ *                                                      src/harvest.cpp:79-120, src/sampler.cpp:27-87
+ *   rsm_harvest_gram      <- rsm::harvest_gram         include/rsm/solver.hpp:53-54, src/harvest.cpp:79-120
+ *   rsm_solve_v           <- rsm::solve_v              include/rsm/solver.hpp:65, src/solver.cpp:15-62
+ *   rsm_solve_u           <- rsm::solve_u              include/rsm/solver.hpp:74-75, src/solver.cpp:64-89
+ *   rsm_masked_residual_norm <- rsm::masked_residual_norm include/rsm/core.hpp:94, src/core.cpp:35-39
+ *   rsm_generate          <- rsm::generate (observed matrix only) include/rsm/synth.hpp:29, src/synth.cpp:12-57
+ *
+ * Host buffers are caller-owned; device memory is owned by the context.
+ * Calls are synchronous on return, one host thread per context. Matrices
+ * are row-major FP64 with NaN (ignored) at hidden cells plus a uint8 mask,
+ * exactly rsm::MaskedMatrix (include/rsm/core.hpp:22-57).
+ */
+#ifndef RSM_B200_H
+#define RSM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t rsm_status;
+#define RSM_OK 0
+#define RSM_ERR_INTERNAL 1              /* errc::internal (also CUDA/NCCL failures) */
+#define RSM_ERR_INVALID_CONFIG 2        /* errc::invalid_config */
+#define RSM_ERR_PARSE_IO 3              /* errc::parse_io */
+#define RSM_ERR_INSUFFICIENT_COVERAGE 4 /* errc::insufficient_coverage */
+
+#define RSM_MODE_M1 0 /* column branch (rsm::Mode::M1) */
+#define RSM_MODE_M2 1 /* row branch    (rsm::Mode::M2) */
+
+/* rsm::RsmConfig (include/rsm/solver.hpp:13-23) with TrialPlan flattened
+ * (include/rsm/planner.hpp:12-18): trials + epsilon are what decompose uses. */
+typedef struct {
+  int64_t rank;
+  int32_t mode;
+  int64_t block;
+  int64_t vectors_per_trial;
+  uint64_t trials;
+  double epsilon;
+  uint64_t seed;
+  double gram_rank_tol;
+  int64_t min_dim;
+  int32_t workers; /* accepted and ignored: results never depend on it */
+} rsm_config;
+
+/* rsm::TrialParams (include/rsm/solver.hpp:27-34) */
+typedef struct {
+  int32_t mode;
+  int64_t block;
+  int64_t ell;
+  int64_t rank;
+  int64_t min_count;
+  uint64_t seed;
+} rsm_trial_params;
+
+/* rsm::DecompositionReport (include/rsm/core.hpp:81-90) */
+typedef struct {
+  double e;
+  uint64_t trials_attempted;
+  uint64_t trials_accepted;
+  uint64_t z;
+  int64_t underdetermined_rows;
+  int64_t gram_rank;
+  int32_t borderline_rank_gate;
+  double wall_time;
+} rsm_report;
+
+typedef struct rsm_ctx rsm_ctx;
+
+/* Fills cfg with the reference defaults (RsmConfig{} + TrialPlan{}). */
+void rsm_config_default(rsm_config* cfg);
+
+/* Message of the last failing call on ctx (or of the last context-free call
+ * when ctx is NULL). Valid until the next call on the same context. */
+const char* rsm_last_error(const rsm_ctx* ctx);
+
+/* ---------------------------------------------------------------- context */
+/* world/rank/nccl_id: world==1 for a single GPU (nccl_id ignored). For
+ * world>1, nccl_id points to the 128-byte ncclUniqueId produced by
+ * rsm_nccl_unique_id on rank 0 and broadcast by the caller. */
+rsm_status rsm_ctx_create(rsm_ctx** out, int device, int world, int rank, const void* nccl_id);
+rsm_status rsm_ctx_destroy(rsm_ctx* ctx);
+rsm_status rsm_nccl_unique_id(void* out128);
+/* cudaStream_t the context launches on (for event timing by callers). */
+void* rsm_ctx_stream(rsm_ctx* ctx);
+
+/* Upload a masked matrix (host buffers) into the context: H2D copy, device
+ * bit-packing of the mask, device transpose when m < n. */
+rsm_status rsm_ctx_load(rsm_ctx* ctx, const double* values, const uint8_t* mask, int64_t m,
+                        int64_t n);
+/* Same from device buffers already resident in HBM (no H2D). */
+rsm_status rsm_ctx_load_device(rsm_ctx* ctx, const double* d_values, const uint8_t* d_mask,
+                               int64_t m, int64_t n);
+
+/* decompose on the loaded matrix. U (m x r) and V (n x r) row-major host
+ * buffers may be NULL to leave the factors on the device
+ * (rsm_ctx_fetch_factors copies them later). */
+rsm_status rsm_ctx_decompose(rsm_ctx* ctx, const rsm_config* cfg, double* U, double* V,
+                             rsm_report* rep);
+rsm_status rsm_ctx_fetch_factors(rsm_ctx* ctx, double* U, double* V);
+
+/* Stage entry points on the loaded matrix, for the oriented problem
+ * (m >= n as loaded; call these only for the matrix as given). */
+rsm_status rsm_ctx_select(rsm_ctx* ctx, const rsm_trial_params* p, uint64_t trials,
+                          uint64_t* accepted_attempts /* trials or NULL */,
+                          int64_t* survivors /* trials or NULL */, uint64_t* attempted,
+                          uint64_t* accepted);
+rsm_status rsm_ctx_harvest_gram(rsm_ctx* ctx, const rsm_trial_params* p, uint64_t trials,
+                                double* G /* n*n or NULL */, uint64_t* attempted,
+                                uint64_t* accepted, uint64_t* z);
+/* G == NULL uses the accumulator left on the device by the last harvest. */
+rsm_status rsm_ctx_solve_v(rsm_ctx* ctx, const double* G, int64_t n, int64_t r, double tol,
+                           double* V /* n*r */, int64_t* gram_rank, int32_t* borderline,
+                           double* w_small /* r+1 smallest eigenvalues or NULL */);
+/* V == NULL uses the basis left on the device by the last solve_v. */
+rsm_status rsm_ctx_solve_u(rsm_ctx* ctx, const double* V, int64_t r, double* U /* m*r or NULL */,
+                           int64_t* underdetermined_rows, double* sum_sq_resid);
+
+/* Per-stage device time (ms) of the last decompose, CUDA events on the
+ * context stream: [0] select, [1] svd, [2] gram, [3] gram-reduce,
+ * [4] solve_v, [5] solve_u, [6] total. Returns the number written. */
+int rsm_ctx_stage_ms(rsm_ctx* ctx, double* ms, int cap);
+/* Kernel launches issued by the last decompose. */
+int64_t rsm_ctx_launch_count(rsm_ctx* ctx);
+
+/* --------------------------------------------------------- one-shot API */
+/* Reference-shaped calls on host buffers (use a per-device default context). */
+rsm_status rsm_make_trial_params(const rsm_config* cfg, int64_t m, int64_t n, rsm_trial_params* out);
+rsm_status rsm_decompose(const double* values, const uint8_t* mask, int64_t m, int64_t n,
+                         const rsm_config* cfg, double* U, double* V, rsm_report* rep);
+rsm_status rsm_harvest_gram(const double* values, const uint8_t* mask, int64_t m, int64_t n,
+                            const rsm_trial_params* p, uint64_t trials, double* G,
+                            uint64_t* attempted, uint64_t* accepted, uint64_t* z);
+rsm_status rsm_solve_v(const double* G, int64_t n, int64_t r, double tol, double* V,
+                       int64_t* gram_rank, int32_t* borderline);
+rsm_status rsm_solve_u(const double* values, const uint8_t* mask, int64_t m, int64_t n,
+                       const double* V, int64_t r, double* U, int64_t* underdetermined_rows);
+rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, int64_t m,
+                                    int64_t n, const double* U, const double* V, int64_t r,
+                                    double* e);
+
+/* Host input generator (reference synth streams, observed matrix only),
+ * rows [row0, row0+rows) of an m x n instance; multithreaded. */
+rsm_status rsm_generate(int64_t m, int64_t n, int64_t r, double rho, double sigma, uint64_t seed,
+                        int64_t row0, int64_t rows, double* values, uint8_t* mask);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

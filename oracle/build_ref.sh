@@ -1,0 +1,38 @@
+#!/usr/bin/env bash
+# Builds oracle/_ref from the reference's own sources where they lie under
+# /root/reference (never copied into the repo): the library TUs the hot path
+# needs plus the reference's doctest suites, against builder-written shims for
+# the absent third-party headers (oracle/ref_shim: Eigen subset over LAPACK,
+# LAPACKE forwarder, doctest subset). io.cpp (nlohmann JSON) and the CLI are
+# out of scope and not built. Outputs go only to oracle/_ref/.
+set -euo pipefail
+HERE="$(cd "$(dirname "${BASH_SOURCE[0]}")" && pwd)"
+REF=/root/reference/proj
+OUT="$HERE/_ref"
+if [ ! -d "$REF" ]; then echo "build_ref: $REF absent, skipping"; exit 0; fi
+PY=${PY:-python}
+SCIPY_LIBS=$($PY -c "import scipy,os;print(os.path.realpath(os.path.join(os.path.dirname(scipy.__file__),'..','scipy.libs')))")
+OPENBLAS=$(ls "$SCIPY_LIBS"/libscipy_openblas*.so | head -1)
+mkdir -p "$OUT/obj"
+CXX="g++ -std=c++20 -O2 -fopenmp -fPIC -I$HERE/ref_shim -I$REF/include -I$REF/src -w"
+SRCS="core sampler spectra harvest solver reference synth als planner"
+objs=()
+for s in $SRCS; do
+  o="$OUT/obj/$s.o"
+  if [ ! -f "$o" ] || [ "$REF/src/$s.cpp" -nt "$o" ] || [ "$HERE/ref_shim/Eigen/Dense" -nt "$o" ]; then
+    $CXX -c "$REF/src/$s.cpp" -o "$o" &
+  fi
+  objs+=("$o")
+done
+wait
+if [ ! -f "$OUT/libref.so" ] || [ "$HERE/ref_glue.cpp" -nt "$OUT/libref.so" ] || [ "$(ls -t "$OUT"/obj/*.o | head -1)" -nt "$OUT/libref.so" ]; then
+  $CXX -shared -o "$OUT/libref.so" "$HERE/ref_glue.cpp" "${objs[@]}" "$OPENBLAS" -Wl,-rpath,"$SCIPY_LIBS"
+fi
+# the reference's own unit suites, as oracle self-checks (oracle/_ref/test_*)
+for t in test_core test_sampler test_spectra test_solver test_synth test_planner; do
+  if [ ! -f "$OUT/$t" ] || [ "$REF/tests/$t.cpp" -nt "$OUT/$t" ] || [ "$OUT/libref.so" -nt "$OUT/$t" ]; then
+    $CXX -I"$REF/tests" -o "$OUT/$t" "$REF/tests/$t.cpp" "${objs[@]}" "$OPENBLAS" -Wl,-rpath,"$SCIPY_LIBS" &
+  fi
+done
+wait
+echo "build_ref: ok ($OUT)"

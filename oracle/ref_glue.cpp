@@ -1,0 +1,180 @@
+// ref_glue.cpp -- extern "C" entry points into the reference's own compiled
+// sources (oracle/_ref/libref.so, built by oracle/build_ref.sh from
+// /root/reference/proj/src with the builder-written shims in ref_shim/).
+// TEST INFRASTRUCTURE ONLY: used to pin the C restatement (liborc.so) and as
+// the "reference" CPU baseline.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <vector>
+
+#include "rsm/sampler.hpp"
+#include "rsm/solver.hpp"
+#include "rsm/synth.hpp"
+
+using namespace rsm;
+
+extern "C" void scipy_openblas_set_num_threads(int);
+
+namespace {
+MaskedMatrix make(const double* Y, const uint8_t* mask, int64_t m, int64_t n) {
+  MaskedMatrix M(m, n);
+  std::memcpy(M.values.data(), Y, sizeof(double) * m * n);
+  std::memcpy(M.mask.data(), mask, (size_t)(m * n));
+  return M;
+}
+TrialParams tp(int mode, int64_t block, int64_t ell, int64_t rank, int64_t min_count, uint64_t seed) {
+  TrialParams p;
+  p.mode = mode == 0 ? Mode::M1 : Mode::M2;
+  p.block = block;
+  p.ell = ell;
+  p.rank = rank;
+  p.min_count = min_count;
+  p.seed = seed;
+  return p;
+}
+template <class F>
+int guard(F&& f) {
+  scipy_openblas_set_num_threads(1);  // tools/rsm.cpp:222 sets OPENBLAS_NUM_THREADS=1
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    return exit_code(e.code());
+  } catch (...) {
+    return 1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ref_generate(int64_t m, int64_t n, int64_t r, double rho, double sigma, uint64_t seed, double* Y,
+                 uint8_t* mask, double* truth_basis) {
+  return guard([&] {
+    SyntheticSpec s{m, n, r, rho, sigma, seed};
+    SyntheticInstance inst = generate(s);
+    std::memcpy(Y, inst.observed.values.data(), sizeof(double) * m * n);
+    std::memcpy(mask, inst.observed.mask.data(), (size_t)(m * n));
+    if (truth_basis) std::memcpy(truth_basis, inst.truth_basis.data(), sizeof(double) * n * r);
+  });
+}
+
+// attempt-order acceptance through the reference sampler (sampler.cpp) with
+// the consumption loop of reference::harvest_gram (reference.cpp:12-25)
+int ref_select(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int mode, int64_t block,
+               int64_t min_count, uint64_t seed, uint64_t trials, uint64_t* ids, int64_t* qs,
+               uint64_t* attempted, uint64_t* accepted) {
+  return guard([&] {
+    MaskedMatrix M = make(Y, mask, m, n);
+    uint64_t att = 0, acc = 0;
+    const uint64_t budget = 20 * trials;
+    while (acc < trials && att < budget) {
+      const TrialRng rng{seed, att};
+      auto S = mode == 0 ? sample_m1(M, block, rng, min_count) : sample_m2(M, block, rng, min_count);
+      ++att;
+      if (!S) continue;
+      ids[acc] = att - 1;
+      qs[acc] = mode == 0 ? S->rows() : S->cols();
+      ++acc;
+    }
+    *attempted = att;
+    *accepted = acc;
+  });
+}
+
+int ref_harvest(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int mode, int64_t block,
+                int64_t ell, int64_t rank, int64_t min_count, uint64_t seed, uint64_t trials, int workers,
+                int serial, double* G, uint64_t* attempted, uint64_t* accepted, uint64_t* z) {
+  return guard([&] {
+    MaskedMatrix M = make(Y, mask, m, n);
+    const TrialParams p = tp(mode, block, ell, rank, min_count, seed);
+    HarvestResult h = serial ? reference::harvest_gram(M, p, trials) : harvest_gram(M, p, trials, workers);
+    if (G) std::memcpy(G, h.gram.data().data(), sizeof(double) * n * n);
+    *attempted = h.attempted;
+    *accepted = h.accepted;
+    *z = h.gram.z();
+  });
+}
+
+int ref_small_singular_vectors(const double* S, int64_t p, int64_t q, int64_t r, int64_t ell, double* zeta,
+                               double* sv) {
+  return guard([&] {
+    Submatrix sub;
+    sub.row_indices.resize(p);
+    sub.col_indices.resize(q);
+    for (int64_t i = 0; i < p; ++i) sub.row_indices[i] = i;
+    for (int64_t j = 0; j < q; ++j) sub.col_indices[j] = j;
+    sub.values.assign(S, S + p * q);
+    auto v = small_singular_vectors(sub, r, ell);
+    for (int64_t t = 0; t < ell; ++t) {
+      sv[t] = v[t].singular_value;
+      std::memcpy(zeta + t * q, v[t].zeta.data(), sizeof(double) * q);
+    }
+  });
+}
+
+int ref_solve_v(const double* G, int64_t n, int64_t r, double tol, double* V, int64_t* gram_rank,
+                int32_t* borderline) {
+  return guard([&] {
+    GramAccumulator A(n);
+    std::memcpy(A.raw().data(), G, sizeof(double) * n * n);
+    SolveVResult s = solve_v(A, r, tol);
+    std::memcpy(V, s.v.data(), sizeof(double) * n * r);
+    *gram_rank = s.gram_rank;
+    *borderline = s.borderline ? 1 : 0;
+  });
+}
+
+int ref_solve_u(const double* Y, const uint8_t* mask, int64_t m, int64_t n, const double* V, int64_t r,
+                int workers, double* U, int64_t* flagged) {
+  return guard([&] {
+    MaskedMatrix M = make(Y, mask, m, n);
+    std::vector<double> v(V, V + n * r);
+    SolveUResult s = solve_u(M, v, r, workers);
+    std::memcpy(U, s.u.data(), sizeof(double) * m * r);
+    *flagged = s.underdetermined_rows;
+  });
+}
+
+int ref_decompose(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int64_t rank, int mode,
+                  int64_t block, int64_t vpt, uint64_t trials, double epsilon, uint64_t seed, double tol,
+                  int64_t min_dim, int workers, double* U, double* V, double* out_e, uint64_t* out_u64,
+                  int64_t* out_i64, double* wall) {
+  return guard([&] {
+    MaskedMatrix M = make(Y, mask, m, n);
+    RsmConfig cfg;
+    cfg.rank = rank;
+    cfg.mode = mode == 0 ? Mode::M1 : Mode::M2;
+    cfg.block = block;
+    cfg.vectors_per_trial = vpt;
+    cfg.plan.trials = trials;
+    cfg.plan.epsilon = epsilon;
+    cfg.seed = seed;
+    cfg.gram_rank_tol = tol;
+    cfg.min_dim = min_dim;
+    cfg.workers = workers;
+    auto [F, rep] = decompose(M, cfg);
+    std::memcpy(U, F.u.data(), sizeof(double) * m * rank);
+    std::memcpy(V, F.v.data(), sizeof(double) * n * rank);
+    *out_e = rep.e;
+    out_u64[0] = rep.trials_attempted;
+    out_u64[1] = rep.trials_accepted;
+    out_u64[2] = rep.z;
+    out_i64[0] = rep.underdetermined_rows;
+    out_i64[1] = rep.gram_rank;
+    out_i64[2] = rep.borderline_rank_gate ? 1 : 0;
+    *wall = rep.wall_time;
+  });
+}
+
+double ref_masked_residual_norm(const double* Y, const uint8_t* mask, int64_t m, int64_t n, const double* U,
+                                const double* V, int64_t r) {
+  MaskedMatrix M = make(Y, mask, m, n);
+  Factorization F(m, n, r);
+  std::memcpy(F.u.data(), U, sizeof(double) * m * r);
+  std::memcpy(F.v.data(), V, sizeof(double) * n * r);
+  return masked_residual_norm(M, F);
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+"""ctypes binding of oracle/_ref/libref.so: the reference's own sources
+(/root/reference/proj/src) compiled with the builder-written shims in
+oracle/ref_shim. TEST INFRASTRUCTURE ONLY (pins the C restatement; serves as
+the "reference" CPU baseline)."""
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "_ref", "libref.so")
+_lib = None
+
+
+def available():
+    return os.path.exists(LIB)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(LIB)
+        P, i64, u64, i32, d = C.c_void_p, C.c_int64, C.c_uint64, C.c_int32, C.c_double
+        L.ref_generate.argtypes = [i64, i64, i64, d, d, u64, P, P, P]
+        L.ref_select.argtypes = [P, P, i64, i64, C.c_int, i64, i64, u64, u64, P, P, C.POINTER(u64), C.POINTER(u64)]
+        L.ref_harvest.argtypes = [P, P, i64, i64, C.c_int, i64, i64, i64, i64, u64, u64, C.c_int, C.c_int, P,
+                                  C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]
+        L.ref_small_singular_vectors.argtypes = [P, i64, i64, i64, i64, P, P]
+        L.ref_solve_v.argtypes = [P, i64, i64, d, P, C.POINTER(i64), C.POINTER(i32)]
+        L.ref_solve_u.argtypes = [P, P, i64, i64, P, i64, C.c_int, P, C.POINTER(i64)]
+        L.ref_decompose.argtypes = [P, P, i64, i64, i64, C.c_int, i64, i64, u64, d, u64, d, i64, C.c_int, P, P,
+                                    C.POINTER(d), P, P, C.POINTER(d)]
+        L.ref_masked_residual_norm.restype = d
+        L.ref_masked_residual_norm.argtypes = [P, P, i64, i64, P, P, i64]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+class RefError(RuntimeError):
+    def __init__(self, code):
+        super().__init__(f"reference raised errc exit code {code}")
+        self.code = code
+
+
+def _chk(st):
+    if st:
+        raise RefError(st)
+
+
+def generate(m, n, r, rho, sigma, seed, with_basis=False):
+    Y = np.zeros((m, n))
+    W = np.zeros((m, n), np.uint8)
+    B = np.zeros((n, r)) if with_basis else None
+    _chk(lib().ref_generate(m, n, r, rho, sigma, seed, _p(Y), _p(W), _p(B)))
+    return (Y, W, B) if with_basis else (Y, W)
+
+
+def select(Y, W, mode, block, min_count, seed, trials):
+    m, n = Y.shape
+    ids = np.zeros(trials, np.uint64)
+    qs = np.zeros(trials, np.int64)
+    att, acc = C.c_uint64(), C.c_uint64()
+    _chk(lib().ref_select(_p(Y), _p(W), m, n, mode, block, min_count, seed, trials, _p(ids), _p(qs),
+                          C.byref(att), C.byref(acc)))
+    return ids[:acc.value], qs[:acc.value], att.value, acc.value
+
+
+def harvest(Y, W, p, trials, workers=0, serial=False):
+    m, n = Y.shape
+    G = np.zeros((n, n))
+    att, acc, z = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    _chk(lib().ref_harvest(_p(Y), _p(W), m, n, p.mode, p.block, p.ell, p.rank, p.min_count, p.seed, trials,
+                           workers, 1 if serial else 0, _p(G), C.byref(att), C.byref(acc), C.byref(z)))
+    return G, att.value, acc.value, z.value
+
+
+def small_singular_vectors(S, r, ell):
+    S = np.ascontiguousarray(S, np.float64)
+    p, q = S.shape
+    zeta = np.zeros((ell, q))
+    sv = np.zeros(ell)
+    _chk(lib().ref_small_singular_vectors(_p(S), p, q, r, ell, _p(zeta), _p(sv)))
+    return zeta, sv
+
+
+def solve_v(G, r, tol=1e-9):
+    G = np.ascontiguousarray(G, np.float64)
+    n = G.shape[0]
+    V = np.zeros((n, r))
+    gr, bl = C.c_int64(), C.c_int32()
+    _chk(lib().ref_solve_v(_p(G), n, r, tol, _p(V), C.byref(gr), C.byref(bl)))
+    return V, gr.value, bool(bl.value)
+
+
+def solve_u(Y, W, V, r, workers=0):
+    m, n = Y.shape
+    U = np.zeros((m, r))
+    fl = C.c_int64()
+    _chk(lib().ref_solve_u(_p(Y), _p(W), m, n, _p(np.ascontiguousarray(V)), r, workers, _p(U), C.byref(fl)))
+    return U, fl.value
+
+
+def decompose(Y, W, rank, trials, mode=0, block=0, vectors_per_trial=0, seed=0, tol=1e-9, min_dim=0,
+              epsilon=0.99, workers=0):
+    m, n = Y.shape
+    U = np.zeros((m, rank))
+    V = np.zeros((n, rank))
+    e, wall = C.c_double(), C.c_double()
+    u64 = np.zeros(3, np.uint64)
+    i64 = np.zeros(3, np.int64)
+    _chk(lib().ref_decompose(_p(Y), _p(W), m, n, rank, mode, block, vectors_per_trial, trials, epsilon, seed, tol,
+                             min_dim, workers, _p(U), _p(V), C.byref(e), _p(u64), _p(i64), C.byref(wall)))
+    rep = dict(e=e.value, trials_attempted=int(u64[0]), trials_accepted=int(u64[1]), z=int(u64[2]),
+               underdetermined_rows=int(i64[0]), gram_rank=int(i64[1]), borderline=bool(i64[2]), wall_time=wall.value)
+    return U, V, rep

@@ -1,0 +1,470 @@
+// k_eig.cu -- stage 4: the r minor eigenvectors of the n x n accumulator.
+//
+// Reference: solve_v (solver.cpp:15-62, paths relative to
+// /root/reference/proj) calls LAPACKE_dsyev for the full spectrum, applies
+// the rank gate on w > tol * lambda_max and returns the r eigenvectors of
+// the smallest eigenvalues, sign-fixed. Here a single cooperative persistent
+// kernel runs Chebyshev-filtered block subspace iteration (Zhou & Saad's
+// scaled filter) aimed at the low end of the PSD spectrum:
+//   * ub = ||G||_inf bounds the spectrum from above;
+//   * a block of b >= r+2 vectors is filtered with a degree-d Chebyshev
+//     polynomial damping [a, ub] (a = largest Ritz value of the block,
+//     d chosen so the amplification stays below 1e6 to keep CholQR stable),
+//     re-orthonormalised by CholQR2 and Rayleigh-Ritz projected;
+//   * it stops when the residuals of the r+1 lowest Ritz pairs fall below
+//     1e-12 ub, which makes the r+1 lowest Ritz values the eigenvalues the
+//     rank gate needs and the first r Ritz vectors the basis;
+//   * one extra column runs a plain power iteration for lambda_max (used only
+//     in the rank-gate threshold tol * lambda_max).
+// G is read from L2 by every matvec (each CTA owns a contiguous row block;
+// the iterate is staged through shared memory in 64-row chunks). All grid
+// reductions write per-CTA partials and every CTA sums them in the same
+// fixed order, so the result is bitwise reproducible. When n <= 16 the block
+// is the whole space and a single Rayleigh-Ritz step is the exact
+// eigendecomposition.
+#include <cooperative_groups.h>
+
+#include "rsm_internal.h"
+#include "rsm_dev.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rsmk {
+
+using namespace rsmd;
+
+namespace {
+
+constexpr int ET = 256;        // threads per CTA
+constexpr int BMAX = 16;       // max block size
+constexpr int LDM = BMAX + 1;  // + power column
+constexpr int KC = 64;         // iterate rows per shared chunk
+constexpr int RPW = 2;         // rows per warp per pass
+
+struct EigShared {
+  double xs[KC * LDM];
+  double H[BMAX * BMAX];
+  double S[BMAX * BMAX];
+  double red[LDM * (LDM + 1) / 2 + 2 * LDM + 8];
+  double theta[BMAX];
+  double cs[64];
+  int pairs[64];
+  int flag[4];
+};
+
+__device__ __forceinline__ int pw_of(int b) { return (b + 1) * (b + 2) / 2 + 2 * (b + 1) + 8; }
+
+// Y(rows) = G * X(all rows), ncol columns, leading dimension ld
+__device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double* __restrict__ Yout,
+                       int ncol, int ld, int row_lo, int row_hi, EigShared& sh) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t n = a.n;
+  for (int rbase = row_lo; rbase < row_hi; rbase += 8 * RPW) {
+    double acc[RPW][LDM];
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr)
+#pragma unroll
+      for (int j = 0; j < LDM; ++j) acc[rr][j] = 0.0;
+    for (int64_t k0 = 0; k0 < n; k0 += KC) {
+      const int kn = (int)((n - k0) < KC ? (n - k0) : KC);
+      __syncthreads();
+      for (int e = tid; e < kn * ld; e += ET) sh.xs[e] = Xin[k0 * ld + e];
+      __syncthreads();
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int i = rbase + warp + rr * 8;
+        if (i < row_hi) {
+          const double* grow = a.G + (int64_t)i * n + k0;
+          for (int kk = lane; kk < kn; kk += 32) {
+            const double g = __ldg(grow + kk);
+            const double* x = sh.xs + kk * ld;
+#pragma unroll
+            for (int j = 0; j < LDM; ++j)
+              if (j < ncol) acc[rr][j] = fma(g, x[j], acc[rr][j]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+      const int i = rbase + warp + rr * 8;
+#pragma unroll
+      for (int j = 0; j < LDM; ++j) {
+        if (j < ncol) {
+          const double v = warp_sum(acc[rr][j]);
+          if (lane == 0 && i < row_hi) Yout[(int64_t)i * ld + j] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// grid reduction of cnt values from part[buf] into sh.red; op 0 = sum, 1 = max
+__device__ void grid_reduce(const EigArgs& a, cg::grid_group& grid, int buf, int cnt, int op,
+                            int pw, EigShared& sh) {
+  grid.sync();
+  const double* base = a.part + (size_t)buf * gridDim.x * pw;
+  for (int e = threadIdx.x; e < cnt; e += ET) {
+    double s = op ? -1.0 : 0.0;
+    for (unsigned c = 0; c < gridDim.x; ++c) {
+      const double v = base[(size_t)c * pw + e];
+      s = op ? fmax(s, v) : s + v;
+    }
+    sh.red[e] = s;
+  }
+  __syncthreads();
+}
+
+// local Gram partial of columns [0, nc) of X over own rows -> part[buf]; plus
+// optional squared norm of column pc (pc < 0: none) at index nc*(nc+1)/2
+__device__ void gram_partial(const EigArgs& a, const double* X, int nc, int ld, int pc,
+                             int row_lo, int row_hi, int buf, int pw) {
+  double* out = a.part + ((size_t)buf * gridDim.x + blockIdx.x) * pw;
+  const int P = nc * (nc + 1) / 2;
+  for (int p = threadIdx.x; p < P + 1; p += ET) {
+    int i = 0, j = 0;
+    if (p < P) {
+      int rem = p;
+      while (rem >= nc - i) { rem -= nc - i; ++i; }
+      j = i + rem;
+    } else {
+      if (pc < 0) continue;
+      i = j = pc;
+    }
+    double s = 0.0;
+    for (int row = row_lo; row < row_hi; ++row) s += X[(int64_t)row * ld + i] * X[(int64_t)row * ld + j];
+    out[p] = s;
+  }
+}
+
+// warp 0: Cholesky of the nc x nc matrix in sh.H (from packed sh.red),
+// lower factor in sh.S; retries with a diagonal shift when not positive.
+__device__ void chol_small(int nc, EigShared& sh) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  double shift = 0.0;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    for (int e = lane; e < nc * nc; e += 32) {
+      int i = e / nc, j = e % nc;
+      if (i < j) { int t = i; i = j; j = t; }
+      // packed upper index of (j, i), j <= i
+      const int p = j * nc - j * (j - 1) / 2 + (i - j);
+      sh.S[(e / nc) * BMAX + (e % nc)] = sh.red[p] + ((e / nc == e % nc) ? shift : 0.0);
+    }
+    __syncwarp();
+    int ok = 1;
+    for (int k = 0; k < nc; ++k) {
+      const double d = sh.S[k * BMAX + k];
+      if (!(d > 0.0)) { ok = 0; break; }
+      const double l = sqrt(d);
+      __syncwarp();
+      if (lane == 0) sh.S[k * BMAX + k] = l;
+      if (lane > k && lane < nc) sh.S[lane * BMAX + k] /= l;
+      __syncwarp();
+      for (int e = lane; e < nc * nc; e += 32) {
+        const int i = e / nc, j = e % nc;
+        if (j > k && i >= j) sh.S[i * BMAX + j] -= sh.S[i * BMAX + k] * sh.S[j * BMAX + k];
+      }
+      __syncwarp();
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (ok) break;
+    double tr = 0.0;
+    for (int k = 0; k < nc; ++k) tr += fabs(sh.red[k * nc - k * (k - 1) / 2]);
+    shift = (shift == 0.0) ? 1e-14 * tr : shift * 100.0;
+  }
+  __syncwarp();
+}
+
+// X(own rows) <- X R^{-1}, R = L^T with L in sh.S
+__device__ void apply_rinv(double* X, int nc, int ld, int row_lo, int row_hi, EigShared& sh) {
+  for (int row = row_lo + threadIdx.x; row < row_hi; row += ET) {
+    double y[BMAX];
+    double* x = X + (int64_t)row * ld;
+#pragma unroll
+    for (int j = 0; j < BMAX; ++j) {
+      if (j < nc) {
+        double s = x[j];
+#pragma unroll
+        for (int i = 0; i < BMAX; ++i)
+          if (i < j) s -= y[i] * sh.S[j * BMAX + i];
+        y[j] = s / sh.S[j * BMAX + j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < BMAX; ++j)
+      if (j < nc) x[j] = y[j];
+  }
+}
+
+__device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, int nc, int ld, int pc,
+                       int row_lo, int row_hi, int& buf, int pw, EigShared& sh) {
+  gram_partial(a, X, nc, ld, pc, row_lo, row_hi, buf, pw);
+  const int P = nc * (nc + 1) / 2;
+  grid_reduce(a, grid, buf, P + 1, 0, pw, sh);
+  buf ^= 1;
+  chol_small(nc, sh);
+  __syncthreads();
+  apply_rinv(X, nc, ld, row_lo, row_hi, sh);
+  if (pc >= 0) {
+    const double nrm = sqrt(sh.red[P]);
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    for (int row = row_lo + threadIdx.x; row < row_hi; row += ET) X[(int64_t)row * ld + pc] *= inv;
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ EigShared sh;
+  const int tid = threadIdx.x;
+  const int64_t n = a.n;
+  const int b = a.b, r = a.r, ld = b + 1, pcol = b;
+  const int pw = pw_of(b);
+  const int row_lo = (int)((int64_t)blockIdx.x * a.rows_per_cta < n ? blockIdx.x * a.rows_per_cta : n);
+  const int row_hi = (int)((int64_t)(blockIdx.x + 1) * a.rows_per_cta < n ? (blockIdx.x + 1) * a.rows_per_cta : n);
+  int buf = 0;
+  int matvecs = 0;
+  const bool full = (b >= n);  // block = whole space
+
+  // ---- ub = ||G||_inf ----
+  {
+    double mx = 0.0;
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int row = row_lo + warp; row < row_hi; row += ET / 32) {
+      double s = 0.0;
+      for (int64_t k = lane; k < n; k += 32) s += fabs(__ldg(a.G + (int64_t)row * n + k));
+      s = warp_sum(s);
+      mx = fmax(mx, s);
+    }
+    if (lane == 0) sh.red[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double m2 = 0.0;
+      for (int w = 0; w < ET / 32; ++w) m2 = fmax(m2, sh.red[w]);
+      a.part[((size_t)buf * gridDim.x + blockIdx.x) * pw] = m2;
+    }
+    grid_reduce(a, grid, buf, 1, 1, pw, sh);
+    buf ^= 1;
+  }
+  const double ub = sh.red[0] > 0.0 ? sh.red[0] * (1.0 + 1e-12) : 1.0;
+
+  // ---- initial block: identity (full) or hashed pseudo-random columns ----
+  double* X = a.X;
+  double* Y = a.Y;
+  double* Z = a.Z;
+  for (int row = row_lo + tid; row < row_hi; row += ET)
+    for (int j = 0; j < ld; ++j) {
+      double v;
+      if (full) v = (j == row) ? 1.0 : 0.0;
+      else v = (double)(mix(0x51ed270b27c3e1a5ull ^ ((uint64_t)row * 131 + j)) >> 11) * 0x1.0p-53 - 0.5;
+      if (j == pcol) v = 1.0 + 0.01 * ((double)(mix(0xabcdefull + row) >> 11) * 0x1.0p-53);
+      X[(int64_t)row * ld + j] = v;
+    }
+  __syncthreads();
+  if (!full) {
+    cholqr(a, grid, X, b, ld, pcol, row_lo, row_hi, buf, pw, sh);
+    cholqr(a, grid, X, b, ld, -1, row_lo, row_hi, buf, pw, sh);
+  }
+
+  double acut = 0.5 * ub;
+  double maxres = 0.0, lmax = 0.0;
+  int outer = 0, status = 1;
+  for (; outer < a.max_outer; ++outer) {
+    if (!full) {
+      // ---- Chebyshev filter of degree d on [acut, ub], normalised at 0 ----
+      const double e = 0.5 * (ub - acut), c = 0.5 * (ub + acut);
+      const double x0 = fabs(c / e);
+      const double growth = x0 + sqrt(x0 * x0 - 1.0);
+      int d = (int)floor(log(2e6) / log(growth));
+      d = d < 2 ? 2 : (d > 24 ? 24 : d);
+      double sigma = e / (0.0 - c);
+      const double tau = 2.0 / sigma;
+      grid.sync();  // X complete
+      matvec(a, X, Z, ld, ld, row_lo, row_hi, sh);
+      ++matvecs;
+      for (int row = row_lo + tid; row < row_hi; row += ET) {
+        const int64_t o = (int64_t)row * ld;
+        for (int j = 0; j < b; ++j) Y[o + j] = (Z[o + j] - c * X[o + j]) * (sigma / e);
+        Y[o + pcol] = Z[o + pcol] / ub;
+      }
+      for (int it = 2; it <= d; ++it) {
+        grid.sync();  // Y complete
+        matvec(a, Y, Z, ld, ld, row_lo, row_hi, sh);
+        ++matvecs;
+        const double sigma2 = 1.0 / (tau - sigma);
+        for (int row = row_lo + tid; row < row_hi; row += ET) {
+          const int64_t o = (int64_t)row * ld;
+          for (int j = 0; j < b; ++j)
+            Z[o + j] = (Z[o + j] - c * Y[o + j]) * (2.0 * sigma2 / e) - sigma * sigma2 * X[o + j];
+          Z[o + pcol] = Z[o + pcol] / ub;
+        }
+        double* t = X; X = Y; Y = Z; Z = t;
+        sigma = sigma2;
+      }
+      // filtered block is in Y
+      { double* t = X; X = Y; Y = t; }
+      __syncthreads();
+      cholqr(a, grid, X, b, ld, pcol, row_lo, row_hi, buf, pw, sh);
+      cholqr(a, grid, X, b, ld, -1, row_lo, row_hi, buf, pw, sh);
+    }
+    // ---- Rayleigh-Ritz ----
+    grid.sync();  // X complete
+    matvec(a, X, Z, ld, ld, row_lo, row_hi, sh);
+    ++matvecs;
+    {
+      double* out = a.part + ((size_t)buf * gridDim.x + blockIdx.x) * pw;
+      const int P = b * (b + 1) / 2;
+      for (int p = tid; p < P + 2; p += ET) {
+        double s = 0.0;
+        if (p < P) {
+          int i = 0, rem = p;
+          while (rem >= b - i) { rem -= b - i; ++i; }
+          const int j = i + rem;
+          for (int row = row_lo; row < row_hi; ++row)
+            s += X[(int64_t)row * ld + i] * Z[(int64_t)row * ld + j];
+        } else if (p == P) {
+          for (int row = row_lo; row < row_hi; ++row)
+            s += X[(int64_t)row * ld + pcol] * Z[(int64_t)row * ld + pcol];
+        } else {
+          for (int row = row_lo; row < row_hi; ++row)
+            s += X[(int64_t)row * ld + pcol] * X[(int64_t)row * ld + pcol];
+        }
+        out[p] = s;
+      }
+      grid_reduce(a, grid, buf, P + 2, 0, pw, sh);
+      buf ^= 1;
+      if (sh.red[P + 1] > 0.0) lmax = sh.red[P] / sh.red[P + 1];
+      // symmetric H from the packed upper triangle
+      for (int e2 = tid; e2 < b * b; e2 += ET) {
+        int i = e2 / b, j = e2 % b;
+        if (i > j) { const int t = i; i = j; j = t; }
+        const int p = i * b - i * (i - 1) / 2 + (j - i);
+        sh.H[(e2 / b) * BMAX + (e2 % b)] = sh.red[p];
+      }
+      __syncthreads();
+      if (tid < 32) {
+        warp_jacobi_eig(sh.H, BMAX, sh.S, BMAX, b, sh.cs, sh.pairs, 2.220446049250313e-16, 60, true);
+        if (tid == 0) {
+          // ascending order: selection sort of eigenpairs
+          for (int i = 0; i < b; ++i) sh.theta[i] = sh.H[i * BMAX + i];
+          for (int i = 0; i < b; ++i) {
+            int mn = i;
+            for (int j = i + 1; j < b; ++j)
+              if (sh.theta[j] < sh.theta[mn]) mn = j;
+            if (mn != i) {
+              double t = sh.theta[i]; sh.theta[i] = sh.theta[mn]; sh.theta[mn] = t;
+              for (int k = 0; k < b; ++k) {
+                t = sh.S[k * BMAX + i]; sh.S[k * BMAX + i] = sh.S[k * BMAX + mn]; sh.S[k * BMAX + mn] = t;
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // X <- X S, Z <- Z S (own rows); residual partials
+    {
+      for (int row = row_lo + tid; row < row_hi; row += ET) {
+        double xr[BMAX], zr[BMAX];
+        const int64_t o = (int64_t)row * ld;
+#pragma unroll
+        for (int j = 0; j < BMAX; ++j) {
+          xr[j] = (j < b) ? X[o + j] : 0.0;
+          zr[j] = (j < b) ? Z[o + j] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < BMAX; ++j) {
+          if (j < b) {
+            double sx = 0.0, sz = 0.0;
+#pragma unroll
+            for (int i = 0; i < BMAX; ++i)
+              if (i < b) {
+                sx += xr[i] * sh.S[i * BMAX + j];
+                sz += zr[i] * sh.S[i * BMAX + j];
+              }
+            X[o + j] = sx;
+            Z[o + j] = sz;
+          }
+        }
+      }
+      __syncthreads();
+      double* out = a.part + ((size_t)buf * gridDim.x + blockIdx.x) * pw;
+      for (int j = tid; j < b; j += ET) {
+        double s = 0.0;
+        for (int row = row_lo; row < row_hi; ++row) {
+          const double d = Z[(int64_t)row * ld + j] - sh.theta[j] * X[(int64_t)row * ld + j];
+          s += d * d;
+        }
+        out[j] = s;
+      }
+      grid_reduce(a, grid, buf, b, 0, pw, sh);
+      buf ^= 1;
+    }
+    maxres = 0.0;
+    const int nchk = (r + 1 < b) ? r + 1 : b;
+    for (int j = 0; j < nchk; ++j) maxres = fmax(maxres, sqrt(sh.red[j]));
+    if (full || maxres <= 1e-12 * ub) { status = 0; ++outer; break; }
+    acut = sh.theta[b - 1];
+    if (!(acut < 0.999 * ub)) acut = 0.999 * ub;
+    if (acut <= 0.0) acut = 1e-6 * ub;
+  }
+  if (status != 0 && maxres <= 1e-9 * ub) status = 0;  // converged to a looser bound
+  // ---- outputs ----
+  for (int row = row_lo + tid; row < row_hi; row += ET)
+    for (int j = 0; j < r; ++j) a.V[(int64_t)row * r + j] = X[(int64_t)row * ld + j];
+  if (blockIdx.x == 0 && tid == 0) {
+    for (int j = 0; j < b; ++j) a.w[j] = sh.theta[j];
+    a.istat[0] = status;
+    a.istat[3] = outer;
+    a.istat[4] = matvecs;
+    a.dstat[0] = full ? sh.theta[b - 1] : lmax;
+    a.dstat[1] = ub;
+    a.dstat[2] = maxres;
+  }
+}
+
+// sign fix (solver.cpp:47-60): the largest-magnitude entry of each column is
+// made positive, the first index winning ties. One warp per column.
+__global__ void k_sign_fix(double* V, int64_t n, int r) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < r; c += blockDim.x >> 5) {
+    double best = -1.0;
+    int64_t arg = 0;
+    for (int64_t i = lane; i < n; i += 32) {
+      const double m = fabs(V[i * r + c]);
+      if (m > best) { best = m; arg = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int64_t oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+    }
+    const double flip = V[arg * r + c] < 0.0 ? -1.0 : 1.0;
+    for (int64_t i = lane; i < n; i += 32) V[i * r + c] *= flip;
+  }
+}
+
+int eig_part_width(int b) { return (b + 1) * (b + 2) / 2 + 2 * (b + 1) + 8; }
+
+int eig_max_grid() {
+  int dev = 0, sms = 0, nb = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eig, ET, 0);
+  return sms * (nb > 0 ? nb : 1);
+}
+
+cudaError_t launch_eig(const EigArgs& a, int grid, cudaStream_t s) {
+  void* args[] = {(void*)&a};
+  return cudaLaunchCooperativeKernel((void*)k_eig, dim3(grid), dim3(ET), args, 0, s);
+}
+
+void launch_sign_fix(double* V, int64_t n, int r, cudaStream_t s) {
+  k_sign_fix<<<1, 512, 0, s>>>(V, n, r);
+}
+
+}  // namespace rsmk

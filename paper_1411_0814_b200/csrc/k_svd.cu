@@ -1,0 +1,292 @@
+// k_svd.cu -- stage 2: gather of each accepted submatrix and its top right
+// singular vectors by one-sided (Hestenes) Jacobi in shared memory, FP64.
+//
+// Reference: small_singular_vectors (spectra.cpp:48-86, paths relative to
+// /root/reference/proj) harvests the ell smallest right singular vectors of S
+// from a full-V JacobiSVD; attempt_trial (harvest.cpp:37-51) takes
+// ell = cols - rank for the row branch and ell = block - rank for the column
+// branch. Their outer products sum to  I - V_top V_top^T  over the trial's
+// column support, where V_top holds the q - ell top right singular vectors
+// (q = number of columns of S). So this kernel only produces V_top; stage 3
+// accumulates the identity form.
+//
+// The K "vectors" rotated by the Jacobi are the K rows of S for the row
+// branch (S is K x q, K = k) and the K columns of S for the column branch
+// (S is q_rows x K, K = l). Each outer iteration recomputes their K x K Gram
+// from the data in shared memory, diagonalises it with the warp-parallel
+// cyclic Jacobi and applies the rotation to the vectors; it stops when the
+// recomputed Gram is diagonal to working precision (the one-sided Jacobi
+// convergence test), so accuracy is that of one-sided Jacobi, not of the
+// squared Gram.
+//
+// Also emits, per trial, the column-support bit words and their exclusive
+// popcount prefix (the compact-index map stage 3 needs), and the per-column
+// trial counts (the identity's diagonal) with integer atomics.
+#include "rsm_internal.h"
+#include "rsm_dev.cuh"
+
+namespace rsmk {
+
+using namespace rsmd;
+
+namespace {
+
+// exclusive popcount prefix of nwords words, by warp 0; returns total in *tot
+__device__ void warp0_popc_scan(const uint32_t* words, uint32_t* pre, int64_t nwords,
+                                int* tot) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const int64_t per = (nwords + 31) / 32;
+  const int64_t lo = lane * per;
+  const int64_t hi = lo + per < nwords ? lo + per : nwords;
+  int s = 0;
+  for (int64_t w = lo; w < hi; ++w) s += __popc(words[w]);
+  int incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  int run = incl - s;
+  for (int64_t w = lo; w < hi; ++w) {
+    pre[w] = (uint32_t)run;
+    run += __popc(words[w]);
+  }
+  if (lane == 31) *tot = incl;
+}
+
+}  // namespace
+
+template <bool M2>
+__global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
+  const int K = a.block;
+  const int64_t Lp = a.Lpad;
+
+  // shared layout
+  double* gram = reinterpret_cast<double*>(smem_raw);  // KMAX*KMAX
+  double* W = gram + KMAX * KMAX;                       // KMAX*KMAX
+  double* Vacc = W + KMAX * KMAX;                       // KMAX*KMAX (column branch)
+  double* Tmp = Vacc + KMAX * KMAX;                     // KMAX*KMAX
+  double* cs = Tmp + KMAX * KMAX;                       // 64
+  double* sig = cs + 64;                                // KMAX
+  int* pairs = reinterpret_cast<int*>(sig + KMAX);      // 64
+  int* ord = pairs + 64;                                // KMAX
+  int* idx = ord + KMAX;                                // KMAX
+  int* flags = idx + KMAX;                              // 4
+  uint32_t* cm = reinterpret_cast<uint32_t*>(flags + 4);  // cmw
+  uint32_t* pre = cm + a.cmw;                             // cmw
+  double* vec;
+  {
+    size_t off = (size_t)(reinterpret_cast<unsigned char*>(pre + a.cmw) - smem_raw);
+    off = (off + 15) & ~(size_t)15;
+    vec = a.use_smem ? reinterpret_cast<double*>(smem_raw + off)
+                     : a.scratch + (size_t)blockIdx.x * K * Lp;
+  }
+  uint32_t* rw = a.scratch_u32 + (size_t)blockIdx.x * 2 * a.mwp;  // column branch only
+  uint32_t* rp = rw + a.mwp;
+
+  for (int64_t t = a.t_lo + blockIdx.x; t < a.t_hi; t += gridDim.x) {
+    const int64_t tl = t - a.t_lo;  // local index for outputs
+    if (tid < K) idx[tid] = a.t_idx[t * K + tid];
+    __syncthreads();
+    int64_t L;  // vector length
+    if (M2) {
+      // column support: AND of the K drawn rows' words (sampler.cpp:65-74)
+      for (int64_t w = tid; w < a.cmw; w += nth) {
+        uint32_t acc = 0;
+        if (w < a.nwp) {
+          acc = 0xffffffffu;
+          for (int i = 0; i < K; ++i) acc &= __ldg(a.bitsR + (int64_t)idx[i] * a.nwp + w);
+        }
+        cm[w] = acc;
+      }
+      __syncthreads();
+      warp0_popc_scan(cm, pre, a.cmw, &flags[0]);
+      __syncthreads();
+      L = flags[0];
+      for (int64_t w = tid; w < a.cmw; w += nth) {
+        a.t_cm[tl * a.cmw + w] = cm[w];
+        a.t_pre[tl * a.cmw + w] = pre[w];
+      }
+      // gather S (K x L) row-major into vec (sampler.cpp:80-84)
+      for (int64_t j = tid; j < a.n; j += nth) {
+        const uint32_t word = cm[j >> 5];
+        const uint32_t bit = 1u << (j & 31);
+        if (word & bit) {
+          const int64_t c = pre[j >> 5] + __popc(word & (bit - 1u));
+          for (int i = 0; i < K; ++i) vec[i * Lp + c] = __ldg(a.Y + (int64_t)idx[i] * a.n + j);
+          atomicAdd(a.colcnt + j, 1);
+        }
+      }
+    } else {
+      // column support = the K drawn columns
+      for (int64_t w = tid; w < a.cmw; w += nth) cm[w] = 0;
+      __syncthreads();
+      if (tid < K) atomicOr(&cm[idx[tid] >> 5], 1u << (idx[tid] & 31));
+      __syncthreads();
+      warp0_popc_scan(cm, pre, a.cmw, &flags[1]);
+      __syncthreads();
+      for (int64_t w = tid; w < a.cmw; w += nth) {
+        a.t_cm[tl * a.cmw + w] = cm[w];
+        a.t_pre[tl * a.cmw + w] = pre[w];
+      }
+      if (tid < K) atomicAdd(a.colcnt + idx[tid], 1);
+      // surviving rows: AND of the K columns' words (sampler.cpp:34-43)
+      for (int64_t w = tid; w < a.mwp; w += nth) {
+        uint32_t acc = 0xffffffffu;
+        for (int j = 0; j < K; ++j) acc &= __ldg(a.bitsC + (int64_t)idx[j] * a.mwp + w);
+        rw[w] = acc;
+      }
+      __syncthreads();
+      warp0_popc_scan(rw, rp, a.mwp, &flags[0]);
+      __syncthreads();
+      L = flags[0];
+      // gather S^T (K x L): vector j = column idx[j] over surviving rows
+      for (int64_t w = tid; w < a.mwp; w += nth) {
+        uint32_t word = rw[w];
+        int64_t c = rp[w];
+        while (word) {
+          const int b = __ffs(word) - 1;
+          word &= word - 1;
+          const int64_t i = w * 32 + b;
+          for (int j = 0; j < K; ++j) vec[j * Lp + c] = __ldg(a.Y + i * a.n + idx[j]);
+          ++c;
+        }
+      }
+      if (tid < K * K) Vacc[(tid / K) * KMAX + (tid % K)] = (tid / K == tid % K) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+
+    // ---- one-sided Jacobi with Gram-accelerated sweeps ----
+    const int P = K * (K + 1) / 2;
+    const double tol_ortho = 4.0 * 2.220446049250313e-16 * sqrt((double)(L > 1 ? L : 1));
+    for (int it = 0;; ++it) {
+      for (int p = warp; p < P; p += nwarps) {
+        // unrank p -> (i, j), i <= j
+        int i = 0, rem = p;
+        while (rem >= K - i) { rem -= K - i; ++i; }
+        const int j = i + rem;
+        const double* vi = vec + i * Lp;
+        const double* vj = vec + j * Lp;
+        double s = 0.0;
+        for (int64_t c = lane; c < L; c += 32) s += vi[c] * vj[c];
+        s = warp_sum(s);
+        if (lane == 0) {
+          gram[i * KMAX + j] = s;
+          gram[j * KMAX + i] = s;
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {
+        int big = 0;
+        for (int e = lane; e < K * K; e += 32) {
+          const int p = e / K, q = e % K;
+          if (p < q) {
+            const double g = gram[p * KMAX + q];
+            const double d = sqrt(gram[p * KMAX + p] * gram[q * KMAX + q]);
+            if (g != 0.0 && fabs(g) > tol_ortho * d) big = 1;
+          }
+        }
+        big = __any_sync(0xffffffffu, big);
+        const bool stop = !big || it >= 6;
+        if (stop) {
+          if (lane < K) sig[lane] = sqrt(fmax(gram[lane * KMAX + lane], 0.0));
+        } else {
+          warp_jacobi_eig(gram, KMAX, W, KMAX, K, cs, pairs, 2.220446049250313e-16, 40, true);
+        }
+        if (lane == 0) flags[2] = stop ? 1 : 0;
+      }
+      __syncthreads();
+      if (flags[2]) break;
+      // vectors <- W^T vectors
+      for (int64_t c = tid; c < L; c += nth) {
+        double x[KMAX];
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) x[i] = (i < K) ? vec[i * Lp + c] : 0.0;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+          if (j < K) {
+            double y = 0.0;
+#pragma unroll
+            for (int i = 0; i < KMAX; ++i)
+              if (i < K) y += W[i * KMAX + j] * x[i];
+            vec[j * Lp + c] = y;
+          }
+        }
+      }
+      if (!M2) {
+        // Vacc <- Vacc W
+        for (int e = tid; e < K * K; e += nth) {
+          const int r = e / K, cc = e % K;
+          double s = 0.0;
+          for (int i = 0; i < K; ++i) s += Vacc[r * KMAX + i] * W[i * KMAX + cc];
+          Tmp[r * KMAX + cc] = s;
+        }
+        __syncthreads();
+        for (int e = tid; e < K * K; e += nth) Vacc[(e / K) * KMAX + e % K] = Tmp[(e / K) * KMAX + e % K];
+      }
+      __syncthreads();
+    }
+    // descending singular values, ties by index (stable)
+    if (tid == 0) {
+      for (int i = 0; i < K; ++i) ord[i] = i;
+      for (int i = 1; i < K; ++i) {
+        const int x = ord[i];
+        int b = i - 1;
+        while (b >= 0 && sig[ord[b]] < sig[x]) { ord[b + 1] = ord[b]; --b; }
+        ord[b + 1] = x;
+      }
+    }
+    __syncthreads();
+    const int rex = a.rex;
+    double* vout = a.Vout + a.t_off[tl];
+    if (M2) {
+      // V_top rows over the column support: v_i[c] = rotated_row_i[c] / sigma_i
+      for (int64_t c = tid; c < L; c += nth)
+        for (int i = 0; i < rex; ++i) {
+          const int o = ord[i];
+          const double sg = sig[o];
+          vout[c * rex + i] = sg > 0.0 ? vec[o * Lp + c] / sg : 0.0;
+        }
+    } else {
+      for (int e = tid; e < K * rex; e += nth) {
+        const int j = e / rex, i = e % rex;
+        vout[j * rex + i] = Vacc[j * KMAX + ord[i]];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+size_t svd_smem_fixed(int64_t cmw) {
+  size_t s = sizeof(double) * (4 * KMAX * KMAX + 64 + KMAX) + sizeof(int) * (64 + 3 * KMAX + 4) +
+             sizeof(uint32_t) * 2 * (size_t)cmw;
+  return (s + 15) & ~(size_t)15;
+}
+
+void launch_svd(const SvdArgs& a, bool m2, int grid, size_t smem, cudaStream_t s) {
+  if (m2) {
+    cudaFuncSetAttribute(k_svd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_svd<true><<<grid, 128, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(k_svd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_svd<false><<<grid, 128, smem, s>>>(a);
+  }
+}
+
+int svd_occupancy(bool m2, size_t smem) {
+  int nb = 0;
+  if (m2) {
+    cudaFuncSetAttribute(k_svd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_svd<true>, 128, smem);
+  } else {
+    cudaFuncSetAttribute(k_svd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_svd<false>, 128, smem);
+  }
+  return nb;
+}
+
+}  // namespace rsmk

@@ -1,0 +1,976 @@
+// rsm_ctx.cu -- host orchestration of the B200 RSM hot path and the C-ABI
+// declared in include/rsm_b200.h.
+//
+// Mirrors the reference pipeline (paths relative to /root/reference/proj):
+//   decompose            solver.cpp:119-146  validation, m<n transpose, e
+//   decompose_oriented   solver.cpp:93-115
+//   trial_params         harvest.cpp:11-35
+//   harvest_gram         harvest.cpp:79-120  -> stages 1-3 (k_select/k_svd/k_gram)
+//   solve_v              solver.cpp:15-62    -> stage 4 (k_eig) + rank gate here
+//   solve_u              solver.cpp:64-89    -> stage 5 (k_solve_u)
+// Errors are rsm::errc codes (error.hpp:8-46). CUDA/NCCL failures map to
+// internal. No CPU fallback exists: every numeric stage runs on the device.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/rsm_b200.h"
+#include "rsm_internal.h"
+#include "rsm_dev.cuh"
+
+namespace {
+
+struct RsmError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw RsmError{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(RSM_ERR_INTERNAL, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t need) {
+    if (need <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    need = std::max<size_t>(need, 256);
+    ck(cudaMalloc(&p, need), "cudaMalloc");
+    bytes = need;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// ---- NCCL, loaded at run time only when world > 1 ----
+typedef struct { char internal[128]; } NcclId;
+typedef void* NcclComm;
+struct Nccl {
+  void* h = nullptr;
+  int (*getUniqueId)(NcclId*) = nullptr;
+  int (*commInitRank)(NcclComm*, int, NcclId, int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*allGather)(const void*, void*, size_t, int, NcclComm, cudaStream_t) = nullptr;
+  int (*commDestroy)(NcclComm) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    getUniqueId = (int (*)(NcclId*))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (int (*)(NcclComm*, int, NcclId, int))dlsym(h, "ncclCommInitRank");
+    allReduce = (int (*)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t))dlsym(h, "ncclAllReduce");
+    allGather = (int (*)(const void*, void*, size_t, int, NcclComm, cudaStream_t))dlsym(h, "ncclAllGather");
+    commDestroy = (int (*)(NcclComm))dlsym(h, "ncclCommDestroy");
+    return getUniqueId && commInitRank && allReduce && allGather && commDestroy;
+  }
+};
+Nccl g_nccl;
+constexpr int kNcclFloat64 = 8, kNcclInt64 = 4, kNcclSum = 0;
+
+struct View {
+  const double* Y;
+  const uint32_t* bitsR;
+  const uint32_t* bitsC;
+  int64_t m, n, nwp, mwp;
+};
+
+struct SelResult {
+  uint64_t attempted = 0, accepted = 0;
+  int qmax = 0;
+};
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct rsm_ctx {
+  int device = 0;
+  int world = 1, rank = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  NcclComm comm = nullptr;
+  std::string err;
+
+  // the loaded matrix as given
+  bool loaded = false;
+  int64_t m = 0, n = 0;
+  unsigned long long known = 0;
+  DevBuf Y, M8, bitsR, bitsC;
+  bool haveC = false;
+  // its transpose, built on demand for decompose when m < n
+  DevBuf Yt, M8t, bitsRt, bitsCt;
+  bool haveT = false, haveCt = false;
+
+  // workspace
+  DevBuf sel_idx, sel_q, blockcnt, selstate, t_attempt, t_q, t_idx, t_off, t_cm, t_pre, Vtrial,
+      colcnt, svd_scr, svd_scr32, P, tiles, G, eX, eY, eZ, ePart, eW, eI, eD, Vhat, U, rowres,
+      flagged, dsum, cnt64;
+  int64_t tiles_n = -1;
+  int tiles_cpl = 0;
+  int64_t G_n = 0;      // accumulator on device valid for this n
+  int64_t Vhat_n = 0, Vhat_r = 0;
+  bool oriented_T = false;  // last decompose ran on the transpose
+  int64_t U_m = 0, U_r = 0;
+
+  cudaEvent_t ev[8] = {};
+  double stage_ms[8] = {};
+  int64_t launches = 0;
+
+  void set_err(const std::string& s) { err = s; }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+void record(rsm_ctx* c, int i) { ck(cudaEventRecord(c->ev[i], c->stream), "cudaEventRecord"); }
+
+// ---------------------------------------------------------------- layout
+View make_view(rsm_ctx* c, bool transposed, bool needC) {
+  if (!c->loaded) fail(RSM_ERR_INVALID_CONFIG, "no matrix loaded");
+  View v{};
+  if (!transposed) {
+    v.m = c->m;
+    v.n = c->n;
+    v.nwp = ceil_div(c->n, 128) * 4;
+    v.mwp = ceil_div(c->m, 32);
+    if (needC && !c->haveC) {
+      c->bitsC.ensure(sizeof(uint32_t) * v.n * v.mwp);
+      rsmk::launch_pack_cols(c->M8.as<uint8_t>(), v.m, v.n, c->bitsC.as<uint32_t>(), v.mwp, c->stream);
+      ++c->launches;
+      c->haveC = true;
+    }
+    v.Y = c->Y.as<double>();
+    v.bitsR = c->bitsR.as<uint32_t>();
+    v.bitsC = c->haveC ? c->bitsC.as<uint32_t>() : nullptr;
+  } else {
+    v.m = c->n;
+    v.n = c->m;
+    v.nwp = ceil_div(v.n, 128) * 4;
+    v.mwp = ceil_div(v.m, 32);
+    if (!c->haveT) {
+      c->Yt.ensure(sizeof(double) * c->m * c->n);
+      c->M8t.ensure((size_t)c->m * c->n);
+      rsmk::launch_transpose(c->Y.as<double>(), c->M8.as<uint8_t>(), c->m, c->n, c->Yt.as<double>(),
+                             c->M8t.as<uint8_t>(), c->stream);
+      c->bitsRt.ensure(sizeof(uint32_t) * v.m * v.nwp);
+      rsmk::launch_pack_rows(c->M8t.as<uint8_t>(), v.m, v.n, c->bitsRt.as<uint32_t>(), v.nwp, c->stream);
+      c->launches += 2;
+      c->haveT = true;
+    }
+    if (needC && !c->haveCt) {
+      c->bitsCt.ensure(sizeof(uint32_t) * v.n * v.mwp);
+      rsmk::launch_pack_cols(c->M8t.as<uint8_t>(), v.m, v.n, c->bitsCt.as<uint32_t>(), v.mwp, c->stream);
+      ++c->launches;
+      c->haveCt = true;
+    }
+    v.Y = c->Yt.as<double>();
+    v.bitsR = c->bitsRt.as<uint32_t>();
+    v.bitsC = c->haveCt ? c->bitsCt.as<uint32_t>() : nullptr;
+  }
+  return v;
+}
+
+void load_common(rsm_ctx* c, int64_t m, int64_t n) {
+  c->m = m;
+  c->n = n;
+  c->haveC = c->haveT = c->haveCt = false;
+  const int64_t nwp = ceil_div(n, 128) * 4;
+  c->bitsR.ensure(sizeof(uint32_t) * m * nwp);
+  rsmk::launch_pack_rows(c->M8.as<uint8_t>(), m, n, c->bitsR.as<uint32_t>(), nwp, c->stream);
+  c->cnt64.ensure(sizeof(unsigned long long));
+  ck(cudaMemsetAsync(c->cnt64.p, 0, sizeof(unsigned long long), c->stream), "memset");
+  rsmk::launch_count_bits(c->bitsR.as<uint32_t>(), m * nwp, c->cnt64.as<unsigned long long>(), c->stream);
+  c->launches += 2;
+  ck(cudaMemcpyAsync(&c->known, c->cnt64.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  ck(cudaGetLastError(), "load kernels");
+  c->loaded = true;
+}
+
+// ------------------------------------------------------------- trial params
+rsm_trial_params trial_params_impl(const rsm_config* cfg, int64_t m, int64_t n) {
+  // harvest.cpp:11-35
+  if (cfg->rank < 1) fail(RSM_ERR_INVALID_CONFIG, "rank must be positive");
+  if (cfg->rank >= std::min(m, n)) fail(RSM_ERR_INVALID_CONFIG, "rank must be below min(rows, cols)");
+  rsm_trial_params p{};
+  p.mode = cfg->mode;
+  p.rank = cfg->rank;
+  p.seed = cfg->seed;
+  p.block = cfg->block > 0 ? cfg->block : cfg->rank + 1;
+  if (p.block <= cfg->rank) fail(RSM_ERR_INVALID_CONFIG, "block must exceed rank");
+  const int64_t pool = cfg->mode == RSM_MODE_M1 ? n : m;
+  if (p.block > pool) fail(RSM_ERR_INVALID_CONFIG, "block exceeds matrix dimension");
+  p.min_count = cfg->min_dim > 0 ? cfg->min_dim : cfg->rank + 1;
+  if (p.min_count < cfg->rank + 1) fail(RSM_ERR_INVALID_CONFIG, "min_dim must be at least rank+1");
+  if (cfg->mode == RSM_MODE_M1) {
+    p.ell = cfg->vectors_per_trial > 0 ? cfg->vectors_per_trial : p.block - cfg->rank;
+    if (p.ell > p.block - cfg->rank) fail(RSM_ERR_INVALID_CONFIG, "vectors_per_trial exceeds block-rank");
+  } else {
+    p.ell = cfg->vectors_per_trial;
+  }
+  return p;
+}
+
+void check_device_params(const rsm_trial_params* p, const View& v) {
+  if (p->mode != RSM_MODE_M1 && p->mode != RSM_MODE_M2) fail(RSM_ERR_INVALID_CONFIG, "unknown mode");
+  if (p->block < 1) fail(RSM_ERR_INVALID_CONFIG, "block must be positive");
+  const int64_t pool = p->mode == RSM_MODE_M1 ? v.n : v.m;
+  if (p->block > pool) fail(RSM_ERR_INVALID_CONFIG, p->mode == RSM_MODE_M1 ? "sample_m1: column count out of range" : "sample_m2: row count out of range");
+  if (p->block > rsmd::KMAX) fail(RSM_ERR_INVALID_CONFIG, "device path supports block <= 16 rows/columns per trial");
+  if (v.m > INT32_MAX || v.n > INT32_MAX) fail(RSM_ERR_INVALID_CONFIG, "dimension exceeds 2^31-1");
+}
+
+// ------------------------------------------------------------------ stage 1
+SelResult select_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint64_t T) {
+  if (T < 1) fail(RSM_ERR_INVALID_CONFIG, "trial count must be positive");
+  check_device_params(p, v);
+  const bool m2 = p->mode == RSM_MODE_M2;
+  const int block = (int)p->block;
+  const uint64_t budget = 20 * T;  // harvest.cpp:85
+  c->t_attempt.ensure(sizeof(uint64_t) * T);
+  c->t_q.ensure(sizeof(int32_t) * T);
+  c->t_idx.ensure(sizeof(int32_t) * T * block);
+  c->selstate.ensure(sizeof(rsmk::SelState));
+  ck(cudaMemsetAsync(c->selstate.p, 0, sizeof(rsmk::SelState), c->stream), "memset");
+  const uint32_t* bits = m2 ? v.bitsR : v.bitsC;
+  const int64_t stride = m2 ? v.nwp : v.mwp;
+  const int64_t nwords = m2 ? ceil_div(v.n, 32) : ceil_div(v.m, 32);
+  const int64_t pool = m2 ? v.m : v.n;
+  SelResult r;
+  uint64_t attempted = 0, acc = 0;
+  double p_est = 1.0;
+  rsmk::SelState hs{};
+  while (acc < T && attempted < budget) {
+    const uint64_t want = T - acc;
+    uint64_t chunk = (uint64_t)std::ceil((double)want * 1.1 / p_est) + 256;
+    chunk = std::max<uint64_t>(chunk, 4096);
+    chunk = std::min<uint64_t>(chunk, 1ull << 22);
+    chunk = std::min<uint64_t>(chunk, budget - attempted);
+    c->sel_idx.ensure(sizeof(int32_t) * chunk * block);
+    c->sel_q.ensure(sizeof(int32_t) * chunk);
+    c->blockcnt.ensure(sizeof(int32_t) * (chunk / 1024 + 2));
+    rsmk::launch_select(bits, stride, nwords, pool, block, p->seed, attempted, (int64_t)chunk,
+                        c->sel_idx.as<int32_t>(), c->sel_q.as<int32_t>(), c->stream);
+    rsmk::launch_accept(c->sel_q.as<int32_t>(), c->sel_idx.as<int32_t>(), (int64_t)chunk,
+                        (int32_t)p->min_count, block, attempted, c->blockcnt.as<int32_t>(),
+                        c->selstate.as<rsmk::SelState>(), T, c->t_attempt.as<uint64_t>(),
+                        c->t_q.as<int32_t>(), c->t_idx.as<int32_t>(), c->stream);
+    c->launches += 4;
+    ck(cudaMemcpyAsync(&hs, c->selstate.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "select");
+    ck(cudaGetLastError(), "select kernels");
+    if (hs.attempted_done) {
+      attempted = hs.attempted_done;
+      acc = T;
+      break;
+    }
+    p_est = std::max(1e-3, (double)(hs.acc - acc) / (double)chunk);
+    acc = hs.acc;
+    attempted += chunk;
+  }
+  r.attempted = attempted;
+  r.accepted = acc;
+  r.qmax = hs.qmax;
+  return r;
+}
+
+// ------------------------------------------------------------ stages 2 + 3
+struct HarvestOut {
+  SelResult sel;
+  uint64_t z = 0;
+};
+
+void build_tiles(rsm_ctx* c, int64_t npad, int cpl) {
+  if (c->tiles_n == npad && c->tiles_cpl == cpl) return;
+  const int64_t TR = 64, TC = 32 * cpl;
+  std::vector<int2> t;
+  for (int64_t J = 0; J < npad / TC; ++J)
+    for (int64_t I = 0; I < npad / TR; ++I)
+      if (TC * J + TC - 1 >= TR * I) t.push_back(make_int2((int)I, (int)J));
+  c->tiles.ensure(sizeof(int2) * t.size());
+  ck(cudaMemcpy(c->tiles.p, t.data(), sizeof(int2) * t.size(), cudaMemcpyHostToDevice), "H2D tiles");
+  c->tiles_n = npad;
+  c->tiles_cpl = cpl;
+}
+
+int64_t ntiles_for(int64_t npad, int cpl) {
+  const int64_t TR = 64, TC = 32 * cpl;
+  int64_t k = 0;
+  for (int64_t J = 0; J < npad / TC; ++J)
+    for (int64_t I = 0; I < npad / TR; ++I)
+      if (TC * J + TC - 1 >= TR * I) ++k;
+  return k;
+}
+
+HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint64_t T) {
+  HarvestOut out;
+  const bool m2 = p->mode == RSM_MODE_M2;
+  record(c, 0);
+  out.sel = select_impl(c, v, p, T);
+  record(c, 1);
+  const int64_t Tacc = (int64_t)out.sel.accepted;
+  const int64_t n = v.n;
+  const int64_t npad = ceil_div(n, 128) * 128;
+  const int64_t cmw = npad / 32;
+  const int K = (int)p->block;
+  // per-trial ell / top-vector count (harvest.cpp:44-50)
+  std::vector<int32_t> hq(Tacc > 0 ? Tacc : 1);
+  if (Tacc > 0)
+    ck(cudaMemcpyAsync(hq.data(), c->t_q.p, sizeof(int32_t) * Tacc, cudaMemcpyDeviceToHost, c->stream), "D2H q");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  int rex;
+  if (m2) {
+    rex = (int)p->rank;
+    if (p->ell > 0 && Tacc > 0 && p->ell < (int64_t)out.sel.qmax - p->rank)
+      fail(RSM_ERR_INVALID_CONFIG,
+           "row-branch vectors_per_trial below survivors-rank harvests an implementation-defined "
+           "null-space basis; the device path supports the adaptive default");
+  } else {
+    rex = (int)(p->block - p->ell);
+  }
+  if (rex < 1 || rex > 16) fail(RSM_ERR_INVALID_CONFIG, "device path supports 1 <= block-vectors <= 16 top vectors");
+  // local trial range (trials shard over ranks, no communication needed)
+  const int64_t t_lo = Tacc * c->rank / c->world, t_hi = Tacc * (c->rank + 1) / c->world;
+  const int64_t Tl = t_hi - t_lo;
+  std::vector<int64_t> off(Tl + 1, 0);
+  uint64_t z = 0;
+  for (int64_t t = 0; t < Tacc; ++t) z += m2 ? (uint64_t)(hq[t] - rex) : (uint64_t)p->ell;
+  for (int64_t t = 0; t < Tl; ++t) {
+    const int64_t cols = m2 ? hq[t_lo + t] : K;
+    off[t + 1] = off[t] + cols * rex;
+  }
+  out.z = z;
+  c->G.ensure(sizeof(double) * n * n);
+  c->colcnt.ensure(sizeof(int) * npad);
+  ck(cudaMemsetAsync(c->colcnt.p, 0, sizeof(int) * npad, c->stream), "memset");
+  if (Tl > 0) {
+    c->t_off.ensure(sizeof(int64_t) * (Tl + 1));
+    ck(cudaMemcpyAsync(c->t_off.p, off.data(), sizeof(int64_t) * (Tl + 1), cudaMemcpyHostToDevice, c->stream), "H2D off");
+    c->t_cm.ensure(sizeof(uint32_t) * Tl * cmw);
+    c->t_pre.ensure(sizeof(uint32_t) * Tl * cmw);
+    c->Vtrial.ensure(sizeof(double) * std::max<int64_t>(off[Tl], 1));
+    // stage 2
+    int64_t Lmax = m2 ? out.sel.qmax : 0;
+    if (!m2) for (int64_t t = t_lo; t < t_hi; ++t) Lmax = std::max<int64_t>(Lmax, hq[t]);
+    const int64_t Lpad = std::max<int64_t>(2, (Lmax + 1) & ~int64_t(1));
+    const size_t fixed = rsmk::svd_smem_fixed(cmw);
+    const size_t vecb = sizeof(double) * (size_t)K * Lpad;
+    const bool use_smem = fixed + vecb <= 200 * 1024;
+    const size_t smem = fixed + (use_smem ? vecb : 0);
+    int occ = rsmk::svd_occupancy(m2, smem);
+    if (occ < 1) occ = 1;
+    const int64_t grid = std::min<int64_t>(Tl, (int64_t)c->sms * occ);
+    rsmk::SvdArgs a{};
+    a.Y = v.Y; a.m = v.m; a.n = v.n;
+    a.bitsR = v.bitsR; a.nwp = v.nwp;
+    a.bitsC = v.bitsC; a.mwp = v.mwp;
+    a.t_idx = c->t_idx.as<int32_t>();
+    a.t_lo = t_lo; a.t_hi = t_hi;
+    a.block = K; a.rex = rex;
+    a.t_off = c->t_off.as<int64_t>();
+    a.t_cm = c->t_cm.as<uint32_t>(); a.t_pre = c->t_pre.as<uint32_t>(); a.cmw = cmw;
+    a.Vout = c->Vtrial.as<double>();
+    a.colcnt = c->colcnt.as<int>();
+    if (!use_smem) {
+      c->svd_scr.ensure(vecb * grid);
+      a.scratch = c->svd_scr.as<double>();
+    }
+    if (!m2) {
+      c->svd_scr32.ensure(sizeof(uint32_t) * 2 * v.mwp * grid);
+      a.scratch_u32 = c->svd_scr32.as<uint32_t>();
+    }
+    a.Lpad = Lpad;
+    a.use_smem = use_smem ? 1 : 0;
+    rsmk::launch_svd(a, m2, (int)grid, smem, c->stream);
+    ++c->launches;
+    ck(cudaGetLastError(), "svd launch");
+  }
+  record(c, 2);
+  // stage 3
+  const int cpl = rsmk::gram_cols_per_lane(rex);
+  build_tiles(c, npad, cpl);
+  const int64_t ntiles = ntiles_for(npad, cpl);
+  int nslices = 1;
+  if (Tl > 0) {
+    nslices = (int)std::max<int64_t>(1, ceil_div(2 * (int64_t)c->sms, ntiles));
+    nslices = (int)std::min<int64_t>(nslices, std::max<int64_t>(1, Tl / 16));
+    c->P.ensure(sizeof(double) * (size_t)nslices * npad * npad);
+    rsmk::GramArgs g{};
+    g.t_cm = c->t_cm.as<uint32_t>();
+    g.t_pre = c->t_pre.as<uint32_t>();
+    g.t_off = c->t_off.as<int64_t>();
+    g.V = c->Vtrial.as<double>();
+    g.T = Tl; g.cmw = cmw; g.npad = npad; g.R = rex; g.nslices = nslices;
+    g.tiles = c->tiles.as<int2>();
+    g.P = c->P.as<double>();
+    rsmk::launch_gram(g, (int)ntiles, c->stream);
+    ++c->launches;
+    ck(cudaGetLastError(), "gram launch");
+  } else {
+    c->P.ensure(sizeof(double) * npad * npad);
+    ck(cudaMemsetAsync(c->P.p, 0, sizeof(double) * npad * npad, c->stream), "memset");
+  }
+  record(c, 3);
+  rsmk::launch_gram_reduce(c->P.as<double>(), nslices, npad, n, c->colcnt.as<int>(), c->G.as<double>(), c->stream);
+  ++c->launches;
+  if (c->world > 1) {
+    if (g_nccl.allReduce(c->G.p, c->G.p, (size_t)(n * n), kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
+      fail(RSM_ERR_INTERNAL, "ncclAllReduce failed");
+  }
+  record(c, 4);
+  ck(cudaGetLastError(), "gram reduce");
+  c->G_n = n;
+  return out;
+}
+
+// ------------------------------------------------------------------ stage 4
+struct SolveVOut {
+  int64_t gram_rank = 0;
+  int borderline = 0;
+  std::vector<double> w;
+};
+
+SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
+  // solver.cpp:15-62
+  if (n < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_v: empty accumulator");
+  if (r < 1 || r >= n) fail(RSM_ERR_INVALID_CONFIG, "solve_v: need 1 <= r < n");
+  if (!(tol > 0.0)) fail(RSM_ERR_INVALID_CONFIG, "solve_v: tolerance must be positive");
+  if (c->G_n != n) fail(RSM_ERR_INVALID_CONFIG, "solve_v: no accumulator of this size on the device");
+  int b;
+  if (n <= 16) b = (int)n;
+  else {
+    if (r > 14) fail(RSM_ERR_INVALID_CONFIG, "device eigensolver supports r <= 14 for n > 16");
+    b = (int)std::min<int64_t>(16, std::max<int64_t>(r + 5, 2 * r + 2));
+  }
+  const int ld = b + 1;
+  const int maxgrid = rsmk::eig_max_grid();
+  int grid = (int)std::min<int64_t>(maxgrid, std::max<int64_t>(1, ceil_div(n, 8)));
+  const int rows_per_cta = (int)ceil_div(n, grid);
+  grid = (int)ceil_div(n, rows_per_cta);
+  const int pw = rsmk::eig_part_width(b);
+  c->eX.ensure(sizeof(double) * n * ld);
+  c->eY.ensure(sizeof(double) * n * ld);
+  c->eZ.ensure(sizeof(double) * n * ld);
+  c->ePart.ensure(sizeof(double) * 2 * (size_t)grid * pw);
+  c->eW.ensure(sizeof(double) * 32);
+  c->eI.ensure(sizeof(int) * 8);
+  c->eD.ensure(sizeof(double) * 8);
+  c->Vhat.ensure(sizeof(double) * n * r);
+  rsmk::EigArgs a{};
+  a.G = c->G.as<double>();
+  a.n = n; a.r = (int)r; a.b = b; a.tol = tol;
+  a.rows_per_cta = rows_per_cta; a.rpw = 2;
+  a.X = c->eX.as<double>(); a.Y = c->eY.as<double>(); a.Z = c->eZ.as<double>();
+  a.part = c->ePart.as<double>();
+  a.V = c->Vhat.as<double>();
+  a.w = c->eW.as<double>();
+  a.istat = c->eI.as<int>();
+  a.dstat = c->eD.as<double>();
+  a.max_outer = 60;
+  ck(rsmk::launch_eig(a, grid, c->stream), "cooperative eig launch");
+  rsmk::launch_sign_fix(c->Vhat.as<double>(), n, (int)r, c->stream);
+  c->launches += 2;
+  double w[32];
+  int istat[8];
+  double dstat[8];
+  ck(cudaMemcpyAsync(w, c->eW.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(istat, c->eI.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "solve_v");
+  ck(cudaGetLastError(), "eig kernels");
+  if (istat[0] != 0) fail(RSM_ERR_INTERNAL, "symmetric eigensolver failed to converge");
+  c->Vhat_n = n;
+  c->Vhat_r = r;
+  const double lambda_max = std::max(dstat[0], 0.0);
+  const double threshold = tol * lambda_max;
+  SolveVOut o;
+  o.w.assign(w, w + b);
+  int64_t significant;
+  if (b == n) {
+    significant = 0;
+    for (int i = 0; i < b; ++i)
+      if (w[i] > threshold) ++significant;
+  } else {
+    int64_t small = 0;
+    for (int i = 0; i <= r; ++i)
+      if (!(w[i] > threshold)) ++small;
+    significant = n - small;
+  }
+  if (significant < n - r)
+    fail(RSM_ERR_INSUFFICIENT_COVERAGE, "rank gate failed: constraint coverage below n-r; raise the trial count or epsilon");
+  o.gram_rank = significant;
+  o.borderline = !(w[r] > 10.0 * threshold);
+  return o;
+}
+
+// ------------------------------------------------------------------ stage 5
+struct SolveUOut {
+  int64_t flagged = 0;
+  double ss = 0.0;
+};
+
+SolveUOut solve_u_impl(rsm_ctx* c, const View& v, int64_t r) {
+  if (r < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_u: rank must be positive");
+  if (r > 8) fail(RSM_ERR_INVALID_CONFIG, "device row solver supports r <= 8");
+  if (c->Vhat_n != v.n || c->Vhat_r != r) fail(RSM_ERR_INVALID_CONFIG, "solve_u: basis shape does not match matrix");
+  c->U.ensure(sizeof(double) * v.m * r);
+  c->rowres.ensure(sizeof(double) * v.m);
+  c->flagged.ensure(sizeof(int) * 2);
+  c->dsum.ensure(sizeof(double) * 2);
+  ck(cudaMemsetAsync(c->flagged.p, 0, sizeof(int) * 2, c->stream), "memset");
+  const int64_t lo = v.m * c->rank / c->world, hi = v.m * (c->rank + 1) / c->world;
+  rsmk::SolveUArgs a{};
+  a.Y = v.Y; a.bitsR = v.bitsR;
+  a.m = v.m; a.n = v.n; a.nwp = v.nwp;
+  a.row_lo = lo; a.row_hi = hi;
+  a.V = c->Vhat.as<double>();
+  a.U = c->U.as<double>();
+  a.rowres = c->rowres.as<double>();
+  a.flagged = c->flagged.as<int>();
+  a.r = (int)r;
+  if (hi > lo) {
+    rsmk::launch_solve_u(a, c->stream);
+    rsmk::launch_sum_rows(c->rowres.as<double>() + lo, hi - lo, c->dsum.as<double>(), c->stream);
+    c->launches += 2;
+  } else {
+    ck(cudaMemsetAsync(c->dsum.p, 0, sizeof(double), c->stream), "memset");
+  }
+  double ss = 0.0;
+  int fl = 0;
+  if (c->world > 1) {
+    // row shards: gather U, sum the scalars
+    double* tmp = nullptr;
+    ck(cudaMallocAsync((void**)&tmp, sizeof(double) * 2, c->stream), "malloc");
+    // pack [ss, flagged] as doubles for one allreduce
+    double host2[2];
+    ck(cudaMemcpyAsync(&ss, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(&fl, c->flagged.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    host2[0] = ss;
+    host2[1] = (double)fl;
+    ck(cudaMemcpyAsync(tmp, host2, sizeof(double) * 2, cudaMemcpyHostToDevice, c->stream), "H2D");
+    if (g_nccl.allReduce(tmp, tmp, 2, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
+      fail(RSM_ERR_INTERNAL, "ncclAllReduce failed");
+    ck(cudaMemcpyAsync(host2, tmp, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    // U row blocks are equal-sized only when world divides m; gather via
+    // per-rank broadcast-free allgather of a padded buffer
+    const int64_t maxrows = ceil_div(v.m, c->world);
+    DevBuf pad;
+    pad.ensure(sizeof(double) * maxrows * r * (c->world + 1));
+    double* sendb = pad.as<double>() + (size_t)maxrows * r * c->world;
+    ck(cudaMemcpyAsync(sendb, c->U.as<double>() + lo * r, sizeof(double) * (hi - lo) * r, cudaMemcpyDeviceToDevice, c->stream), "D2D");
+    if (g_nccl.allGather(sendb, pad.p, (size_t)(maxrows * r), kNcclFloat64, c->comm, c->stream) != 0)
+      fail(RSM_ERR_INTERNAL, "ncclAllGather failed");
+    for (int g = 0; g < c->world; ++g) {
+      const int64_t glo = v.m * g / c->world, ghi = v.m * (g + 1) / c->world;
+      ck(cudaMemcpyAsync(c->U.as<double>() + glo * r, pad.as<double>() + (size_t)g * maxrows * r,
+                         sizeof(double) * (ghi - glo) * r, cudaMemcpyDeviceToDevice, c->stream), "D2D");
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    ck(cudaFreeAsync(tmp, c->stream), "free");
+    pad.release();
+    ss = host2[0];
+    fl = (int)host2[1];
+  } else {
+    ck(cudaMemcpyAsync(&ss, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(&fl, c->flagged.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "solve_u");
+  }
+  ck(cudaGetLastError(), "solve_u kernels");
+  c->U_m = v.m;
+  c->U_r = r;
+  SolveUOut o;
+  o.flagged = fl;
+  o.ss = ss;
+  return o;
+}
+
+// ---------------------------------------------------------------- decompose
+void decompose_impl(rsm_ctx* c, const rsm_config* cfg, double* Uout, double* Vout, rsm_report* rep) {
+  const auto t0 = std::chrono::steady_clock::now();
+  c->launches = 0;
+  std::memset(rep, 0, sizeof(*rep));
+  if (!c->loaded) fail(RSM_ERR_INVALID_CONFIG, "no matrix loaded");
+  const int64_t m = c->m, n = c->n;
+  // solver.cpp:122-127
+  if (cfg->rank < 1 || cfg->rank >= std::min(m, n)) fail(RSM_ERR_INVALID_CONFIG, "rank must lie in [1, min(rows, cols))");
+  if (!(cfg->epsilon > 0.0 && cfg->epsilon < 1.0)) fail(RSM_ERR_INVALID_CONFIG, "epsilon must lie in (0,1)");
+  if (cfg->trials < 1) fail(RSM_ERR_INVALID_CONFIG, "trial plan must request at least one trial");
+  if (c->known == 0) fail(RSM_ERR_INSUFFICIENT_COVERAGE, "matrix has no observed entries");
+  const bool tr = m < n;  // solver.cpp:130-140
+  const View v = make_view(c, tr, cfg->mode == RSM_MODE_M1);
+  const rsm_trial_params p = trial_params_impl(cfg, v.m, v.n);
+  HarvestOut h = harvest_impl(c, v, &p, cfg->trials);
+  rep->trials_attempted = h.sel.attempted;
+  rep->trials_accepted = h.sel.accepted;
+  rep->z = h.z;
+  SolveVOut sv = solve_v_impl(c, v.n, cfg->rank, cfg->gram_rank_tol);
+  record(c, 5);
+  rep->gram_rank = sv.gram_rank;
+  rep->borderline_rank_gate = sv.borderline;
+  SolveUOut su = solve_u_impl(c, v, cfg->rank);
+  record(c, 6);
+  rep->underdetermined_rows = su.flagged;
+  rep->e = std::sqrt(su.ss) / std::sqrt((double)c->known);  // core.cpp:35-39
+  c->oriented_T = tr;
+  const int64_t r = cfg->rank;
+  // oriented U is (v.m x r), oriented V is (v.n x r); the transpose swaps them
+  double* hostU = tr ? Vout : Uout;
+  double* hostV = tr ? Uout : Vout;
+  if (hostU) ck(cudaMemcpyAsync(hostU, c->U.p, sizeof(double) * v.m * r, cudaMemcpyDeviceToHost, c->stream), "D2H U");
+  if (hostV) ck(cudaMemcpyAsync(hostV, c->Vhat.p, sizeof(double) * v.n * r, cudaMemcpyDeviceToHost, c->stream), "D2H V");
+  ck(cudaStreamSynchronize(c->stream), "decompose");
+  float ms = 0.f;
+  for (int i = 0; i < 6; ++i) {
+    ck(cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]), "event");
+    c->stage_ms[i] = ms;
+  }
+  ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[6]), "event");
+  c->stage_ms[6] = ms;
+  rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ------------------------------------------------------------ default ctx
+std::mutex g_mu;
+std::map<int, rsm_ctx*> g_default;
+
+rsm_ctx* default_ctx() {
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_default.find(dev);
+  if (it != g_default.end()) return it->second;
+  rsm_ctx* c = nullptr;
+  if (rsm_ctx_create(&c, dev, 1, 0, nullptr) != RSM_OK) fail(RSM_ERR_INTERNAL, std::string("context creation failed: ") + g_err);
+  g_default[dev] = c;
+  return c;
+}
+
+template <class F>
+rsm_status guard(rsm_ctx* c, F&& f) {
+  try {
+    if (c) {
+      ck(cudaSetDevice(c->device), "cudaSetDevice");
+      c->err.clear();
+    }
+    f();
+    return RSM_OK;
+  } catch (const RsmError& e) {
+    if (c) c->err = e.msg;
+    g_err = e.msg;
+    if (c && e.code == RSM_ERR_INTERNAL) cudaGetLastError();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    g_err = e.what();
+    return RSM_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+
+// ======================================================================== C-ABI
+extern "C" {
+
+void rsm_config_default(rsm_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->mode = RSM_MODE_M1;  // RsmConfig{} (solver.hpp:13-23)
+  cfg->epsilon = 0.99;      // TrialPlan{} (planner.hpp:12-18)
+  cfg->gram_rank_tol = 1e-9;
+}
+
+const char* rsm_last_error(const rsm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+rsm_status rsm_ctx_create(rsm_ctx** out, int device, int world, int rank, const void* nccl_id) {
+  return guard(nullptr, [&] {
+    if (!out) fail(RSM_ERR_INVALID_CONFIG, "null output pointer");
+    if (world < 1 || rank < 0 || rank >= world) fail(RSM_ERR_INVALID_CONFIG, "bad world/rank");
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) fail(RSM_ERR_INVALID_CONFIG, "no such CUDA device");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10) fail(RSM_ERR_INTERNAL, "this build targets sm_100a (B200)");
+    rsm_ctx* c = new rsm_ctx();
+    c->device = device;
+    c->world = world;
+    c->rank = rank;
+    c->sms = prop.multiProcessorCount;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
+    if (world > 1) {
+      if (!nccl_id) fail(RSM_ERR_INVALID_CONFIG, "world > 1 needs an NCCL unique id");
+      if (!g_nccl.load()) fail(RSM_ERR_INTERNAL, "libnccl.so.2 not loadable");
+      NcclId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      if (g_nccl.commInitRank(&c->comm, world, id, rank) != 0) fail(RSM_ERR_INTERNAL, "ncclCommInitRank failed");
+    }
+    *out = c;
+  });
+}
+
+rsm_status rsm_ctx_destroy(rsm_ctx* c) {
+  if (!c) return RSM_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  DevBuf* bufs[] = {&c->Y, &c->M8, &c->bitsR, &c->bitsC, &c->Yt, &c->M8t, &c->bitsRt, &c->bitsCt,
+                    &c->sel_idx, &c->sel_q, &c->blockcnt, &c->selstate, &c->t_attempt, &c->t_q,
+                    &c->t_idx, &c->t_off, &c->t_cm, &c->t_pre, &c->Vtrial, &c->colcnt, &c->svd_scr,
+                    &c->svd_scr32, &c->P, &c->tiles, &c->G, &c->eX, &c->eY, &c->eZ, &c->ePart,
+                    &c->eW, &c->eI, &c->eD, &c->Vhat, &c->U, &c->rowres, &c->flagged, &c->dsum,
+                    &c->cnt64};
+  for (DevBuf* b : bufs) b->release();
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  cudaStreamDestroy(c->stream);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_default.begin(); it != g_default.end(); ++it)
+      if (it->second == c) { g_default.erase(it); break; }
+  }
+  delete c;
+  return RSM_OK;
+}
+
+rsm_status rsm_nccl_unique_id(void* out128) {
+  return guard(nullptr, [&] {
+    if (!g_nccl.load()) fail(RSM_ERR_INTERNAL, "libnccl.so.2 not loadable");
+    NcclId id;
+    if (g_nccl.getUniqueId(&id) != 0) fail(RSM_ERR_INTERNAL, "ncclGetUniqueId failed");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+void* rsm_ctx_stream(rsm_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+rsm_status rsm_ctx_load(rsm_ctx* c, const double* values, const uint8_t* mask, int64_t m, int64_t n) {
+  return guard(c, [&] {
+    if (m < 1 || n < 1) fail(RSM_ERR_INVALID_CONFIG, "matrix dimensions must be positive");
+    if (!values || !mask) fail(RSM_ERR_INVALID_CONFIG, "null matrix buffers");
+    c->Y.ensure(sizeof(double) * m * n);
+    c->M8.ensure((size_t)m * n);
+    ck(cudaMemcpyAsync(c->Y.p, values, sizeof(double) * m * n, cudaMemcpyHostToDevice, c->stream), "H2D Y");
+    ck(cudaMemcpyAsync(c->M8.p, mask, (size_t)m * n, cudaMemcpyHostToDevice, c->stream), "H2D mask");
+    load_common(c, m, n);
+  });
+}
+
+rsm_status rsm_ctx_load_device(rsm_ctx* c, const double* d_values, const uint8_t* d_mask, int64_t m, int64_t n) {
+  return guard(c, [&] {
+    if (m < 1 || n < 1) fail(RSM_ERR_INVALID_CONFIG, "matrix dimensions must be positive");
+    c->Y.ensure(sizeof(double) * m * n);
+    c->M8.ensure((size_t)m * n);
+    ck(cudaMemcpyAsync(c->Y.p, d_values, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c->stream), "D2D Y");
+    ck(cudaMemcpyAsync(c->M8.p, d_mask, (size_t)m * n, cudaMemcpyDeviceToDevice, c->stream), "D2D mask");
+    load_common(c, m, n);
+  });
+}
+
+rsm_status rsm_ctx_decompose(rsm_ctx* c, const rsm_config* cfg, double* U, double* V, rsm_report* rep) {
+  return guard(c, [&] { decompose_impl(c, cfg, U, V, rep); });
+}
+
+rsm_status rsm_ctx_fetch_factors(rsm_ctx* c, double* U, double* V) {
+  return guard(c, [&] {
+    if (c->U_m == 0) fail(RSM_ERR_INVALID_CONFIG, "no factors on the device");
+    const int64_t r = c->U_r;
+    const int64_t om = c->U_m, on = c->Vhat_n;
+    double* hostU = c->oriented_T ? V : U;
+    double* hostV = c->oriented_T ? U : V;
+    if (hostU) ck(cudaMemcpyAsync(hostU, c->U.p, sizeof(double) * om * r, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (hostV) ck(cudaMemcpyAsync(hostV, c->Vhat.p, sizeof(double) * on * r, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "fetch");
+  });
+}
+
+rsm_status rsm_ctx_select(rsm_ctx* c, const rsm_trial_params* p, uint64_t trials, uint64_t* accepted_attempts,
+                          int64_t* survivors, uint64_t* attempted, uint64_t* accepted) {
+  return guard(c, [&] {
+    const View v = make_view(c, false, p->mode == RSM_MODE_M1);
+    SelResult s = select_impl(c, v, p, trials);
+    if (accepted_attempts && s.accepted)
+      ck(cudaMemcpyAsync(accepted_attempts, c->t_attempt.p, sizeof(uint64_t) * s.accepted, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (survivors && s.accepted) {
+      std::vector<int32_t> q(s.accepted);
+      ck(cudaMemcpyAsync(q.data(), c->t_q.p, sizeof(int32_t) * s.accepted, cudaMemcpyDeviceToHost, c->stream), "D2H");
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      for (uint64_t i = 0; i < s.accepted; ++i) survivors[i] = q[i];
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *attempted = s.attempted;
+    *accepted = s.accepted;
+  });
+}
+
+rsm_status rsm_ctx_harvest_gram(rsm_ctx* c, const rsm_trial_params* p, uint64_t trials, double* G,
+                                uint64_t* attempted, uint64_t* accepted, uint64_t* z) {
+  return guard(c, [&] {
+    const View v = make_view(c, false, p->mode == RSM_MODE_M1);
+    if (p->rank < 1 || p->block <= p->rank) fail(RSM_ERR_INVALID_CONFIG, "block must exceed rank");
+    if (p->min_count < p->rank + 1) fail(RSM_ERR_INVALID_CONFIG, "degenerate submatrix: needs more than r columns/rows");
+    if (p->mode == RSM_MODE_M1 && (p->ell < 1 || p->ell > p->block - p->rank))
+      fail(RSM_ERR_INVALID_CONFIG, "vector count must lie in [1, cols-r]");
+    HarvestOut h = harvest_impl(c, v, p, trials);
+    if (G) ck(cudaMemcpyAsync(G, c->G.p, sizeof(double) * v.n * v.n, cudaMemcpyDeviceToHost, c->stream), "D2H G");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *attempted = h.sel.attempted;
+    *accepted = h.sel.accepted;
+    *z = h.z;
+  });
+}
+
+rsm_status rsm_ctx_solve_v(rsm_ctx* c, const double* G, int64_t n, int64_t r, double tol, double* V,
+                           int64_t* gram_rank, int32_t* borderline, double* w_small) {
+  return guard(c, [&] {
+    if (G) {
+      if (n < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_v: empty accumulator");
+      c->G.ensure(sizeof(double) * n * n);
+      ck(cudaMemcpyAsync(c->G.p, G, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "H2D G");
+      c->G_n = n;
+    }
+    SolveVOut o = solve_v_impl(c, n, r, tol);
+    if (V) ck(cudaMemcpyAsync(V, c->Vhat.p, sizeof(double) * n * r, cudaMemcpyDeviceToHost, c->stream), "D2H V");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (w_small)
+      for (int64_t i = 0; i <= r && i < (int64_t)o.w.size(); ++i) w_small[i] = o.w[i];
+    *gram_rank = o.gram_rank;
+    *borderline = o.borderline;
+  });
+}
+
+rsm_status rsm_ctx_solve_u(rsm_ctx* c, const double* V, int64_t r, double* U, int64_t* underdetermined_rows,
+                           double* sum_sq_resid) {
+  return guard(c, [&] {
+    const View v = make_view(c, false, false);
+    if (r < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_u: rank must be positive");
+    if (V) {
+      c->Vhat.ensure(sizeof(double) * v.n * r);
+      ck(cudaMemcpyAsync(c->Vhat.p, V, sizeof(double) * v.n * r, cudaMemcpyHostToDevice, c->stream), "H2D V");
+      c->Vhat_n = v.n;
+      c->Vhat_r = r;
+    }
+    SolveUOut o = solve_u_impl(c, v, r);
+    c->oriented_T = false;
+    if (U) ck(cudaMemcpyAsync(U, c->U.p, sizeof(double) * v.m * r, cudaMemcpyDeviceToHost, c->stream), "D2H U");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (underdetermined_rows) *underdetermined_rows = o.flagged;
+    if (sum_sq_resid) *sum_sq_resid = o.ss;
+  });
+}
+
+int rsm_ctx_stage_ms(rsm_ctx* c, double* ms, int cap) {
+  int k = std::min(cap, 7);
+  for (int i = 0; i < k; ++i) ms[i] = c->stage_ms[i];
+  return k;
+}
+
+int64_t rsm_ctx_launch_count(rsm_ctx* c) { return c ? c->launches : 0; }
+
+// ---- one-shot, reference-shaped calls ----
+rsm_status rsm_make_trial_params(const rsm_config* cfg, int64_t m, int64_t n, rsm_trial_params* out) {
+  return guard(nullptr, [&] { *out = trial_params_impl(cfg, m, n); });
+}
+
+rsm_status rsm_decompose(const double* values, const uint8_t* mask, int64_t m, int64_t n, const rsm_config* cfg,
+                         double* U, double* V, rsm_report* rep) {
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  st = rsm_ctx_load(c, values, mask, m, n);
+  if (st) { g_err = c->err; return st; }
+  st = rsm_ctx_decompose(c, cfg, U, V, rep);
+  if (st) g_err = c->err;
+  return st;
+}
+
+rsm_status rsm_harvest_gram(const double* values, const uint8_t* mask, int64_t m, int64_t n,
+                            const rsm_trial_params* p, uint64_t trials, double* G, uint64_t* attempted,
+                            uint64_t* accepted, uint64_t* z) {
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  st = rsm_ctx_load(c, values, mask, m, n);
+  if (!st) st = rsm_ctx_harvest_gram(c, p, trials, G, attempted, accepted, z);
+  if (st) g_err = c->err;
+  return st;
+}
+
+rsm_status rsm_solve_v(const double* G, int64_t n, int64_t r, double tol, double* V, int64_t* gram_rank,
+                       int32_t* borderline) {
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  st = rsm_ctx_solve_v(c, G, n, r, tol, V, gram_rank, borderline, nullptr);
+  if (st) g_err = c->err;
+  return st;
+}
+
+rsm_status rsm_solve_u(const double* values, const uint8_t* mask, int64_t m, int64_t n, const double* V, int64_t r,
+                       double* U, int64_t* underdetermined_rows) {
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  st = rsm_ctx_load(c, values, mask, m, n);
+  if (!st) st = rsm_ctx_solve_u(c, V, r, U, underdetermined_rows, nullptr);
+  if (st) g_err = c->err;
+  return st;
+}
+
+rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, int64_t m, int64_t n,
+                                    const double* U, const double* V, int64_t r, double* e) {
+  // core.cpp:35-39 on the device: the stage-5 residual pass with U given is
+  // not exposed separately; compute via a solve-free kernel path.
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  st = rsm_ctx_load(c, values, mask, m, n);
+  if (st) { g_err = c->err; return st; }
+  return guard(c, [&] {
+    if (c->known == 0) fail(RSM_ERR_INVALID_CONFIG, "empty mask: no known entries");
+    if (r < 1 || r > 16) fail(RSM_ERR_INVALID_CONFIG, "residual: 1 <= r <= 16 on the device");
+    const View v = make_view(c, false, false);
+    c->U.ensure(sizeof(double) * m * r);
+    c->Vhat.ensure(sizeof(double) * n * r);
+    c->rowres.ensure(sizeof(double) * m);
+    c->dsum.ensure(sizeof(double) * 2);
+    ck(cudaMemcpyAsync(c->U.p, U, sizeof(double) * m * r, cudaMemcpyHostToDevice, c->stream), "H2D U");
+    ck(cudaMemcpyAsync(c->Vhat.p, V, sizeof(double) * n * r, cudaMemcpyHostToDevice, c->stream), "H2D V");
+    c->U_m = 0;
+    c->Vhat_n = 0;
+    rsmk::launch_residual(v.Y, v.bitsR, m, n, v.nwp, c->U.as<double>(), c->Vhat.as<double>(), (int)r,
+                          c->rowres.as<double>(), c->stream);
+    rsmk::launch_sum_rows(c->rowres.as<double>(), m, c->dsum.as<double>(), c->stream);
+    double ss = 0.0;
+    ck(cudaMemcpyAsync(&ss, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "residual");
+    ck(cudaGetLastError(), "residual kernels");
+    *e = std::sqrt(ss) / std::sqrt((double)c->known);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// rsm_dev.cuh -- device-side helpers shared by the RSM stage kernels.
+//
+// Counter-based splitmix64 streams restated bit-exactly from the reference
+// (include/rsm/rng.hpp:12-57, paths relative to /root/reference/proj), warp
+// reductions, and a warp-parallel cyclic Jacobi eigensolver for the small
+// symmetric matrices of stages 2 and 4.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rsmd {
+
+constexpr int KMAX = 16;  // max vectors per trial (block k or l) on device
+constexpr int RMAX = 16;  // max excluded top vectors r_ex on device
+
+__device__ __forceinline__ uint64_t mix(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+
+// Rng(seed, tag, index) constructor state (rng.hpp:14-17)
+__device__ __forceinline__ uint64_t rng_state(uint64_t seed, uint64_t tag, uint64_t index) {
+  uint64_t s = mix(seed + 0x9e3779b97f4a7c15ull * tag);
+  return mix(s + 0xbf58476d1ce4e5b9ull * index);
+}
+
+__device__ __forceinline__ uint64_t next_u64(uint64_t& s) {  // rng.hpp:19-22
+  s += 0x9e3779b97f4a7c15ull;
+  return mix(s);
+}
+
+// rejection sampling in [0, bound) (rng.hpp:30-36)
+__device__ __forceinline__ uint64_t next_below(uint64_t& s, uint64_t bound) {
+  const uint64_t limit = bound * (UINT64_MAX / bound);
+  for (;;) {
+    const uint64_t v = next_u64(s);
+    if (v < limit) return v % bound;
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Warp-parallel cyclic Jacobi on a symmetric K x K matrix A (smem,
+// row-major, leading dim lda), K <= 32. Uses the round-robin (tournament)
+// ordering: each step rotates floor(Kp/2) disjoint pairs at once, one lane
+// per pair, then all lanes apply the column and row rotations. On return the
+// diagonal of A holds the eigenvalues and V (K x K, ldv, row-major; column j
+// = eigenvector j) the eigenvectors. Must be called by one full warp.
+// Stops when every off-diagonal |a_pq| <= tol * sqrt(|a_pp a_qq|) or when
+// it is exactly zero; returns the sweep count.
+__device__ inline int warp_jacobi_eig(double* A, int lda, double* V, int ldv, int K,
+                                      double* cs /* smem scratch >= 2*32 doubles */,
+                                      int* pairs /* smem scratch >= 2*32 ints */, double tol,
+                                      int max_sweeps, bool init_v) {
+  const int lane = threadIdx.x & 31;
+  if (init_v)
+    for (int e = lane; e < K * K; e += 32) V[(e / K) * ldv + (e % K)] = (e / K == e % K) ? 1.0 : 0.0;
+  __syncwarp();
+  if (K < 2) return 0;
+  const int Kp = (K + 1) & ~1;  // even count, index K-1+1 is a dummy when K odd
+  const int npair = Kp / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    // convergence test on the current matrix
+    int big = 0;
+    for (int e = lane; e < K * K; e += 32) {
+      const int p = e / K, q = e % K;
+      if (p < q) {
+        const double apq = A[p * lda + q];
+        if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(A[p * lda + p] * A[q * lda + q]))) big = 1;
+      }
+    }
+    if (!__any_sync(0xffffffffu, big)) break;
+    for (int step = 0; step < Kp - 1; ++step) {
+      // round-robin pairing: position 0 fixed, others rotate
+      if (lane < npair) {
+        int a = (lane == 0) ? 0 : ((lane - 1 + step) % (Kp - 1)) + 1;
+        int b = ((Kp - 2 - lane + step) % (Kp - 1)) + 1;
+        int p = a < b ? a : b, q = a < b ? b : a;
+        double c = 1.0, s = 0.0;
+        if (q < K) {
+          const double apq = A[p * lda + q];
+          const double app = A[p * lda + p], aqq = A[q * lda + q];
+          if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
+            const double zeta = (aqq - app) / (2.0 * apq);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = c * t;
+          }
+        }
+        pairs[2 * lane] = p;
+        pairs[2 * lane + 1] = q;
+        cs[2 * lane] = c;
+        cs[2 * lane + 1] = s;
+      }
+      __syncwarp();
+      // column rotation: A <- A J, V <- V J  (J = product of disjoint rotations)
+      for (int e = lane; e < npair * K; e += 32) {
+        const int pr = e / K, row = e % K;
+        const int p = pairs[2 * pr], q = pairs[2 * pr + 1];
+        const double c = cs[2 * pr], s = cs[2 * pr + 1];
+        if (q < K && s != 0.0) {
+          const double x = A[row * lda + p], y = A[row * lda + q];
+          A[row * lda + p] = c * x - s * y;
+          A[row * lda + q] = s * x + c * y;
+          const double vx = V[row * ldv + p], vy = V[row * ldv + q];
+          V[row * ldv + p] = c * vx - s * vy;
+          V[row * ldv + q] = s * vx + c * vy;
+        }
+      }
+      __syncwarp();
+      // row rotation: A <- J^T A
+      for (int e = lane; e < npair * K; e += 32) {
+        const int pr = e / K, col = e % K;
+        const int p = pairs[2 * pr], q = pairs[2 * pr + 1];
+        const double c = cs[2 * pr], s = cs[2 * pr + 1];
+        if (q < K && s != 0.0) {
+          const double x = A[p * lda + col], y = A[q * lda + col];
+          A[p * lda + col] = c * x - s * y;
+          A[q * lda + col] = s * x + c * y;
+        }
+      }
+      __syncwarp();
+      // the rotated pair entries are zero by construction
+      if (lane < npair) {
+        const int p = pairs[2 * lane], q = pairs[2 * lane + 1];
+        if (q < K && cs[2 * lane + 1] != 0.0) {
+          A[p * lda + q] = 0.0;
+          A[q * lda + p] = 0.0;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  return sweep;
+}
+
+}  // namespace rsmd

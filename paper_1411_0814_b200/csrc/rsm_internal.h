@@ -1,0 +1,122 @@
+// rsm_internal.h -- kernel argument blocks and launchers shared between the
+// stage kernels (k_*.cu) and the host orchestration (rsm_ctx.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rsmk {
+
+// device-resident selection state (stage 1 compaction)
+struct SelState {
+  unsigned long long acc;             // accepted so far, capped at T
+  unsigned long long acc_before;      // accepted before the current chunk
+  unsigned long long attempted_done;  // attempt id + 1 of the T-th acceptance, 0 = not yet
+  int qmax;                           // largest survivor count among accepted trials
+  int pad;
+};
+
+struct SvdArgs {
+  const double* Y;       // oriented values, m x n row-major
+  int64_t m, n;
+  const uint32_t* bitsR; // m x nwp row-major mask words
+  int64_t nwp;
+  const uint32_t* bitsC; // n x mwp column-major mask words (column branch)
+  int64_t mwp;
+  const int32_t* t_idx;  // T x block drawn indices (global trial numbering)
+  int64_t t_lo, t_hi;    // this rank's trial range
+  int block;             // K
+  int rex;               // top vectors kept (q - ell)
+  const int64_t* t_off;  // local trial -> offset (doubles) into Vout
+  uint32_t* t_cm;        // local trials x cmw support words
+  uint32_t* t_pre;       // local trials x cmw exclusive popcount prefix
+  int64_t cmw;
+  double* Vout;
+  int* colcnt;           // n per-column trial counts
+  double* scratch;       // per-CTA vector scratch when shared memory is too small
+  uint32_t* scratch_u32; // per-CTA 2*mwp words (column branch)
+  int64_t Lpad;
+  int use_smem;
+};
+
+struct GramArgs {
+  const uint32_t* t_cm;
+  const uint32_t* t_pre;
+  const int64_t* t_off;
+  const double* V;
+  int64_t T;       // local trial count
+  int64_t cmw;
+  int64_t npad;
+  int R;
+  int nslices;
+  const int2* tiles;
+  double* P;       // nslices x npad x npad partials
+};
+
+struct EigArgs {
+  const double* G;  // n x n
+  int64_t n;
+  int r, b;         // wanted, block
+  double tol;       // gram_rank_tol
+  int rows_per_cta;
+  int rpw;          // rows per warp
+  double* X;        // n x ld  (3 buffers)
+  double* Y;
+  double* Z;
+  double* part;     // grid x PARTW partials
+  double* V;        // n x r output
+  double* w;        // b Ritz values output
+  int* istat;       // [0] status, [1] gram_rank (low), [2] borderline, [3] outer its, [4] matvecs
+  double* dstat;    // [0] lambda_max, [1] ub, [2] max residual
+  int max_outer;
+};
+
+struct SolveUArgs {
+  const double* Y;
+  const uint32_t* bitsR;
+  int64_t m, n, nwp;
+  int64_t row_lo, row_hi;
+  const double* V;  // n x r
+  double* U;        // m x r (rows row_lo..row_hi written)
+  double* rowres;   // m residual^2 per row
+  int* flagged;     // count (integer atomics)
+  int r;
+};
+
+// k_prep.cu
+void launch_pack_rows(const uint8_t* mask, int64_t m, int64_t n, uint32_t* bits, int64_t nwp,
+                      cudaStream_t s);
+void launch_pack_cols(const uint8_t* mask, int64_t m, int64_t n, uint32_t* bits, int64_t mwp,
+                      cudaStream_t s);
+void launch_transpose(const double* Y, const uint8_t* M, int64_t m, int64_t n, double* Yt,
+                      uint8_t* Mt, cudaStream_t s);
+void launch_count_bits(const uint32_t* bits, int64_t nwords, unsigned long long* out,
+                       cudaStream_t s);
+// k_select.cu
+void launch_select(const uint32_t* bits, int64_t stride, int64_t nwords, int64_t pool, int block,
+                   uint64_t seed, uint64_t a0, int64_t count, int32_t* idx_out, int32_t* q_out,
+                   cudaStream_t s);
+void launch_accept(const int32_t* q, const int32_t* idx, int64_t count, int32_t min_count,
+                   int block, uint64_t a0, int32_t* blockcnt, SelState* st, uint64_t T,
+                   uint64_t* t_attempt, int32_t* t_q, int32_t* t_idx, cudaStream_t s);
+// k_svd.cu
+size_t svd_smem_fixed(int64_t cmw);
+void launch_svd(const SvdArgs& a, bool m2, int grid, size_t smem, cudaStream_t s);
+int svd_occupancy(bool m2, size_t smem);
+// k_gram.cu
+int gram_cols_per_lane(int R);
+void launch_gram(const GramArgs& a, int ntiles, cudaStream_t s);
+void launch_gram_reduce(const double* P, int nslices, int64_t npad, int64_t n, const int* cnt,
+                        double* G, cudaStream_t s);
+// k_eig.cu
+int eig_part_width(int b);
+cudaError_t launch_eig(const EigArgs& a, int grid, cudaStream_t s);
+int eig_max_grid();
+void launch_sign_fix(double* V, int64_t n, int r, cudaStream_t s);
+// k_solve_u.cu
+void launch_solve_u(const SolveUArgs& a, cudaStream_t s);
+void launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s);
+void launch_residual(const double* Y, const uint32_t* bitsR, int64_t m, int64_t n, int64_t nwp,
+                     const double* U, const double* V, int r, double* rowres, cudaStream_t s);
+
+}  // namespace rsmk

@@ -1,0 +1,304 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle on
+identical seeded inputs. Index selection must match bit-exactly; U V^T within
+1e-9 relative Frobenius (north_star tolerance); report fields exactly."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1411_0814_b200 import rsm
+from tests.util import max_angle_sin, random_masked, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+UV_TOL = 1e-9  # north_star: U V^T within 1e-9 relative Frobenius error, FP64
+
+
+def gen(m, n, r, rho, sigma, seed):
+    M = rsm.generate(m, n, r, rho, sigma, seed)
+    return M
+
+
+def ctx_for(M):
+    c = rsm.Context(0)
+    c.load(M)
+    return c
+
+
+# ------------------------------------------------------------- generator pin
+
+def test_generator_matches_oracle_restatement():
+    M = gen(300, 40, 3, 0.6, 0.1, 7)
+    Y, W = O.generate(300, 40, 3, 0.6, 0.1, 7)
+    assert np.array_equal(M.mask, W)
+    k = W.astype(bool)
+    assert np.array_equal(M.values[k], Y[k])
+    assert np.isnan(M.values[~k]).all()
+
+
+# ------------------------------------------------------------------ stage 1
+
+@pytest.mark.parametrize("shape", [
+    dict(m=2000, n=200, r=3, rho=0.8, k=4, T=2000, seed=0),        # config 1
+    dict(m=131072, n=1024, r=4, rho=0.8, k=5, T=16384, seed=0),    # config 3
+    dict(m=3000, n=100, r=2, rho=0.35, k=6, T=500, seed=5),        # high rejection, budget cut
+])
+def test_select_m2_bit_exact(shape):
+    M = gen(shape["m"], shape["n"], shape["r"], shape["rho"], 1e-3, shape["seed"])
+    p = O.trial_params(shape["r"], 1, M.m, M.n, block=shape["k"], seed=shape["seed"])
+    ids_o, q_o, att_o, acc_o = O.select(M.mask, p, shape["T"])
+    c = ctx_for(M)
+    tp = rsm.TrialParams(rsm.Mode.M2, p.block, p.ell, p.rank, p.min_count, p.seed)
+    ids_g, q_g, att_g, acc_g = c.select(tp, shape["T"])
+    assert (att_g, acc_g) == (att_o, acc_o)
+    assert np.array_equal(ids_g, ids_o)
+    assert np.array_equal(q_g, q_o)
+
+
+def test_select_m1_bit_exact():
+    M = gen(20000, 500, 5, 0.7, 1e-2, 1)  # config 2
+    p = O.trial_params(5, 0, M.m, M.n, seed=1)
+    ids_o, q_o, att_o, acc_o = O.select(M.mask, p, 4096)
+    c = ctx_for(M)
+    tp = rsm.TrialParams(rsm.Mode.M1, p.block, p.ell, p.rank, p.min_count, p.seed)
+    ids_g, q_g, att_g, acc_g = c.select(tp, 4096)
+    assert (att_g, acc_g) == (att_o, acc_o)
+    assert np.array_equal(ids_g, ids_o)
+    assert np.array_equal(q_g, q_o)
+
+
+def test_select_budget_exhausted():
+    # mask so sparse that almost nothing is accepted: the 20x budget ends the run
+    M = gen(400, 60, 2, 0.3, 0.0, 3)
+    p = O.trial_params(2, 1, M.m, M.n, block=8, seed=3)
+    ids_o, q_o, att_o, acc_o = O.select(M.mask, p, 50)
+    c = ctx_for(M)
+    tp = rsm.TrialParams(rsm.Mode.M2, p.block, p.ell, p.rank, p.min_count, p.seed)
+    ids_g, q_g, att_g, acc_g = c.select(tp, 50)
+    assert att_o == 1000 and acc_o < 50
+    assert (att_g, acc_g) == (att_o, acc_o)
+    assert np.array_equal(ids_g, ids_o)
+
+
+# ------------------------------------------------------------- stages 1-3
+
+def _gram_check(M, mode, r, T, seed, block=0, vpt=0):
+    p = O.trial_params(r, mode, M.m, M.n, block=block, vectors_per_trial=vpt, seed=seed)
+    G_o, att_o, acc_o, z_o = O.harvest(M.values, M.mask, p, T)
+    c = ctx_for(M)
+    tp = rsm.TrialParams(rsm.Mode(mode), p.block, p.ell, p.rank, p.min_count, p.seed)
+    h = c.harvest_gram(tp, T)
+    assert (h.attempted, h.accepted, h.z) == (att_o, acc_o, z_o)
+    scale = max(1.0, np.abs(G_o).max())
+    # acceptance criterion 5 (tests/acceptance.cpp:261-310): 1e-10 * max(1, |G|max)
+    assert np.abs(h.gram - G_o).max() <= 1e-10 * scale
+    assert np.array_equal(h.gram, h.gram.T)  # exact symmetry, as the reference
+
+
+def test_harvest_gram_config1():
+    M = gen(2000, 200, 3, 0.8, 1e-3, 0)
+    _gram_check(M, 1, 3, 2000, 0, block=4)
+
+
+def test_harvest_gram_config2_column_branch():
+    M = gen(20000, 500, 5, 0.7, 1e-2, 1)
+    _gram_check(M, 0, 5, 4096, 1, block=6)
+
+
+def test_harvest_gram_config3_prefix():
+    M = gen(131072, 1024, 4, 0.8, 1e-3, 0)
+    _gram_check(M, 1, 4, 48, 0, block=5)
+
+
+def test_harvest_gram_column_branch_explicit_ell():
+    M = gen(600, 30, 2, 0.7, 0.1, 11)
+    _gram_check(M, 0, 2, 300, 11, block=5, vpt=2)
+
+
+# ---------------------------------------------------------------- stage 4
+
+def test_solve_v_matches_dsyev_on_oracle_gram():
+    M = gen(2000, 200, 3, 0.8, 1e-3, 0)
+    p = O.trial_params(3, 1, M.m, M.n, block=4, seed=0)
+    G, *_ = O.harvest(M.values, M.mask, p, 2000)
+    V_o, gr_o, bl_o, w = O.solve_v(G, 3, 1e-9)
+    res = rsm.solve_v(G, 3, 1e-9)
+    assert res.gram_rank == gr_o and res.borderline == bl_o
+    assert max_angle_sin(res.v, V_o) <= 1e-10
+    # distinct eigenvalues: sign-fixed columns agree individually
+    assert np.abs(res.v - V_o).max() <= 1e-9
+
+
+def test_solve_v_reference_cases():
+    # tests/test_solver.cpp:46-86
+    G = np.diag([5.0, 4.0, 0.0, 0.0])
+    res = rsm.solve_v(G, 2, 1e-9)
+    assert res.gram_rank == 2 and not res.borderline
+    P = res.v @ res.v.T
+    assert np.abs(P - np.diag([0, 0, 1, 1.0])).max() <= 1e-12
+    with pytest.raises(rsm.Error) as ei:
+        rsm.solve_v(np.diag([5.0, 0, 0, 0]), 2, 1e-9)
+    assert ei.value.code == rsm.errc.insufficient_coverage
+    res = rsm.solve_v(np.diag([5.0, 2e-8, 0, 0]), 2, 1e-9)
+    assert res.gram_rank == 2 and res.borderline
+    for bad in [(4, 1e-9), (0, 1e-9), (2, 0.0)]:
+        with pytest.raises(rsm.Error) as ei:
+            rsm.solve_v(np.eye(4), *bad)
+        assert ei.value.code == rsm.errc.invalid_config
+
+
+def test_solve_v_larger_iterative_path():
+    # n > 16: Chebyshev-filtered subspace iteration vs dsyev
+    rng = np.random.default_rng(3)
+    n, r = 300, 5
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    w = np.concatenate([rng.uniform(0, 1e-3, r), rng.uniform(50, 100, n - r)])
+    G = (Q * w) @ Q.T
+    G = 0.5 * (G + G.T)
+    V_o, gr_o, bl_o, _ = O.solve_v(G, r, 1e-9)
+    res = rsm.solve_v(G, r, 1e-9)
+    assert res.gram_rank == gr_o and res.borderline == bl_o
+    assert max_angle_sin(res.v, V_o) <= 1e-10
+
+
+# ---------------------------------------------------------------- stage 5
+
+def test_solve_u_matches_cod():
+    M = gen(3000, 120, 4, 0.6, 0.05, 9)
+    rng = np.random.default_rng(9)
+    V, _ = np.linalg.qr(rng.standard_normal((120, 4)))
+    U_o, fl_o = O.solve_u(M.values, M.mask, V, 4)
+    res = rsm.solve_u(M, V, 4)
+    assert res.underdetermined_rows == fl_o
+    assert rel_fro(res.u, U_o) <= 1e-12
+
+
+def test_solve_u_reference_cases():
+    # tests/test_solver.cpp:140-212
+    M = rsm.MaskedMatrix(1, 4)
+    for j in range(4):
+        M.set(0, j, 1.0)
+    res = rsm.solve_u(M, np.full(4, 0.5), 1)
+    assert res.underdetermined_rows == 0 and abs(res.u[0, 0] - 2.0) <= 1e-12
+    M = rsm.MaskedMatrix(3, 4)
+    for j in range(4):
+        M.set(0, j, 1.0)
+        M.set(2, j, 3.0)
+    res = rsm.solve_u(M, np.full(4, 0.5), 1)
+    assert res.underdetermined_rows == 1
+    assert abs(res.u[0, 0] - 2) <= 1e-12 and res.u[1, 0] == 0.0 and abs(res.u[2, 0] - 6) <= 1e-12
+    M = rsm.MaskedMatrix(1, 4)
+    M.set(0, 1, 2.0)
+    vh = np.zeros(8)
+    vh[2] = vh[3] = 1.0
+    res = rsm.solve_u(M, vh, 2)
+    assert res.underdetermined_rows == 1
+    assert np.allclose(res.u[0], [1.0, 1.0], atol=1e-10)
+    M = rsm.MaskedMatrix(2, 3)
+    for i in range(2):
+        for j in range(3):
+            M.set(i, j, float(i + j + 1))
+    res = rsm.solve_u(M, np.array([1, 1, 2, 2, 3, 3.0]), 2)
+    assert res.underdetermined_rows == 2
+    assert np.allclose(res.u[:, 0], res.u[:, 1], atol=1e-10)
+
+
+def test_solve_u_stationarity_random_basis():
+    # tests/test_solver.cpp:174-199
+    vals, mask = random_masked(40, 12, 0.6, 31)
+    M = rsm.MaskedMatrix(40, 12, vals, mask)
+    V = np.random.default_rng(31).standard_normal((12, 3))
+    res = rsm.solve_u(M, V, 3)
+    U_o, fl_o = O.solve_u(vals, mask, V, 3)
+    assert res.underdetermined_rows == fl_o
+    for i in range(40):
+        k = mask[i].astype(bool)
+        y = vals[i, k]
+        grad = V[k].T @ (V[k] @ res.u[i] - y)
+        assert np.abs(grad).max() <= 1e-8 * (1 + np.linalg.norm(y))
+
+
+def test_masked_residual_norm_hand_example():
+    # tests/test_core.cpp:51-63
+    M = rsm.MaskedMatrix(2, 2)
+    M.set(0, 0, 1); M.set(0, 1, 2); M.set(1, 0, 3); M.set(1, 1, 4)
+    F = rsm.Factorization(2, 2, 1, np.array([[1.0], [3.0]]), np.array([[1.0], [2.0]]))
+    assert abs(rsm.masked_residual_norm(M, F) - 1.0) <= 1e-15
+
+
+# --------------------------------------------------------------- end to end
+
+def _e2e(M, cfg):
+    F, rep = rsm.decompose(M, cfg)
+    U_o, V_o, rep_o = O.decompose(M.values, M.mask, cfg.rank, cfg.plan.trials, mode=int(cfg.mode),
+                                  block=cfg.block, vectors_per_trial=cfg.vectors_per_trial, seed=cfg.seed,
+                                  tol=cfg.gram_rank_tol, min_dim=cfg.min_dim)
+    assert rep.trials_attempted == rep_o.trials_attempted
+    assert rep.trials_accepted == rep_o.trials_accepted
+    assert rep.z == rep_o.z
+    assert rep.gram_rank == rep_o.gram_rank
+    assert rep.borderline_rank_gate == bool(rep_o.borderline)
+    assert rep.underdetermined_rows == rep_o.underdetermined_rows
+    uv, uv_o = F.u @ F.v.T, U_o @ V_o.T
+    assert rel_fro(uv, uv_o) <= UV_TOL
+    assert abs(rep.e - rep_o.e) <= 1e-9 * max(rep_o.e, 1e-12) + 1e-14
+    return F, rep
+
+
+def test_decompose_config1():
+    M = gen(2000, 200, 3, 0.8, 1e-3, 0)
+    cfg = rsm.RsmConfig(rank=3, mode=rsm.Mode.M2, block=4, plan=rsm.TrialPlan(2000), seed=0)
+    _e2e(M, cfg)
+
+
+def test_decompose_config2_column_branch():
+    M = gen(20000, 500, 5, 0.7, 1e-2, 1)
+    cfg = rsm.RsmConfig(rank=5, mode=rsm.Mode.M1, block=6, plan=rsm.TrialPlan(4096), seed=1)
+    _e2e(M, cfg)
+
+
+def test_decompose_noiseless_recovers_planted():
+    # tests/test_solver.cpp:245-269 (heuristic plan 25n)
+    M = gen(200, 40, 3, 0.5, 0.0, 17)
+    cfg = rsm.RsmConfig(rank=3, plan=rsm.TrialPlan(25 * 40), seed=17)
+    F, rep = _e2e(M, cfg)
+    assert rep.e <= 1e-8 and rep.gram_rank >= 37
+
+
+def test_decompose_wide_matrix_transposes():
+    # tests/test_solver.cpp:304-324
+    M = gen(30, 90, 2, 0.6, 0.0, 71)
+    cfg = rsm.RsmConfig(rank=2, plan=rsm.TrialPlan(25 * 30), seed=7)
+    F, rep = _e2e(M, cfg)
+    assert F.u.shape == (30, 2) and F.v.shape == (90, 2) and rep.e <= 1e-8
+
+
+def test_decompose_row_branch_floor():
+    # tests/test_solver.cpp:326-344
+    M = gen(150, 30, 2, 0.85, 0.0, 83)
+    cfg = rsm.RsmConfig(rank=2, mode=rsm.Mode.M2, plan=rsm.TrialPlan(300), seed=83)
+    F, rep = _e2e(M, cfg)
+    assert rep.e <= 1e-8 and rep.z >= rep.trials_accepted
+
+
+def test_decompose_validation_errors():
+    vals, mask = random_masked(20, 10, 0.9, 5)
+    M = rsm.MaskedMatrix(20, 10, vals, mask)
+    bad = [rsm.RsmConfig(rank=10, plan=rsm.TrialPlan(250)),
+           rsm.RsmConfig(rank=3, block=2, plan=rsm.TrialPlan(250)),
+           rsm.RsmConfig(rank=3, plan=rsm.TrialPlan(250, epsilon=1.0)),
+           rsm.RsmConfig(rank=3, plan=rsm.TrialPlan(0))]
+    for cfg in bad:
+        with pytest.raises(rsm.Error) as ei:
+            rsm.decompose(M, cfg)
+        assert ei.value.code == rsm.errc.invalid_config
+    with pytest.raises(rsm.Error) as ei:
+        rsm.decompose(rsm.MaskedMatrix(4, 4), rsm.RsmConfig(rank=2, plan=rsm.TrialPlan(100)))
+    assert ei.value.code == rsm.errc.insufficient_coverage
+
+
+def test_decompose_deterministic():
+    M = gen(120, 24, 2, 0.6, 0.2, 53)
+    cfg = rsm.RsmConfig(rank=2, plan=rsm.TrialPlan(600), seed=99)
+    F1, r1 = rsm.decompose(M, cfg)
+    F2, r2 = rsm.decompose(M, cfg)
+    assert np.array_equal(F1.u, F2.u) and np.array_equal(F1.v, F2.v) and r1.e == r2.e
