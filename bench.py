@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RSM hot path (driver contract).
+
+Workload (config.workload): BASELINE.json config 3, "the paper's synthetic
+scale": m=131072, n=1024, r=4, rho=0.8, sigma=1e-3, row branch k=5, 16384
+submatrices, seed 0 (BASELINE.json gives none; 0 documented). A step is one
+full RSM decomposition (selection, SVD, Gram, eigen-extraction, U solve, e).
+The input is synthetic, generated on the host from the reference generator's
+streams (src/synth.cpp:12-57); no public dataset is involved.
+
+  value   submatrices/s of the whole job = T / device time of one decompose,
+          with Y and the mask already resident in HBM; CUDA events on the
+          library's stream; L2 flushed (256 MiB write) between steps, untimed.
+  e2e     the same metric through the public API with host buffers: pinned
+          H2D of Y (FP64) + mask (uint8), decompose, D2H of U and V, per step.
+  roofline for the dominant kernel; stages{} gives every stage's share.
+  cpu_baseline  the reference CPU path (oracle/_ref: the reference's own
+          sources) on a bounded sample of the same workload, extrapolated.
+
+--impl reference runs the reference's CPU implementation alone (rank 0).
+Multi-GPU (torchrun): trials shard over ranks inside one decomposition with a
+single NCCL all-reduce of the n x n accumulator, Y rows shard for the U solve
+(strong scaling: the total work is one decomposition of config 3).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(workload="config3_row_branch_131072x1024_r4", m=131072, n=1024, r=4, rho=0.8, sigma=1e-3, k=5,
+           T=16384, seed=0)
+CONFIGS = {
+    "config3": CFG,
+    "config1": dict(workload="config1_row_branch_2000x200_r3", m=2000, n=200, r=3, rho=0.8, sigma=1e-3, k=4,
+                    T=2000, seed=0),
+    "config4": dict(workload="config4_row_branch_1048576x2048_r8", m=1048576, n=2048, r=8, rho=0.9, sigma=1e-3,
+                    k=9, T=65536, seed=0),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.index), "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        if self.p is None:
+            return out
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if sm:
+            load = [s for s in sm if s > 0.5 * max(sm)] or sm
+            out = {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                   "samples": len(sm)}
+        return out
+
+
+def gen_input(c, rank=0):
+    from paper_1411_0814_b200 import rsm
+    import torch
+    m, n = c["m"], c["n"]
+    # pinned host buffers for the e2e leg (H2D from pinned memory)
+    Yt = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+    Wt = torch.empty((m, n), dtype=torch.uint8, pin_memory=True)
+    Y, W = Yt.numpy(), Wt.numpy()
+    block = 65536
+    for r0 in range(0, m, block):
+        rows = min(block, m - r0)
+        st = rsm.lib().rsm_generate(m, n, c["r"], c["rho"], c["sigma"], c["seed"], r0, rows,
+                                    Y[r0:r0 + rows].ctypes.data_as(rsm.C.c_void_p),
+                                    W[r0:r0 + rows].ctypes.data_as(rsm.C.c_void_p))
+        assert st == 0
+    return Yt, Wt, Y, W
+
+
+def algorithmic(c, qs, nwp_bytes, attempts):
+    """Algorithmic work per stage."""
+    m, n, r, k, T = c["m"], c["n"], c["r"], c["k"], c["T"]
+    q = qs.astype(np.float64)
+    s1_bytes = attempts * k * (n / 32) * 4                           # selection: drawn rows' mask words
+    s2_bytes = T * k * n * 8                                         # gather: full Y rows (SURVEY 8d S1 note)
+    s2_flops = float(np.sum(2 * q * k * (k + 1) / 2 + 2 * r * k * q))
+    s3_flops = float(np.sum(r * q * (q + 1)))                        # symmetric rank-r updates (unique entries)
+    s3_flops_survey = float(np.sum(2 * r * q * q))                   # SURVEY 8d literal-symmetric count
+    s4_bytes = n * n * 8
+    s5_bytes = m * n * 8 + m * nwp_bytes + m * r * 8 + n * r * 8
+    return dict(s1_bytes=s1_bytes, s2_bytes=s2_bytes, s2_flops=s2_flops, s3_flops=s3_flops, s3_flops_survey=s3_flops_survey,
+                s4_bytes=s4_bytes, s5_bytes=s5_bytes)
+
+
+# ------------------------------------------------------------------ CPU arm
+
+def cpu_reference_sample(Y, W, c, G=None, trials_prefix=64, rows_sample=16384):
+    """Time the reference CPU path (oracle/_ref) on a bounded sample and
+    extrapolate a full decomposition: harvest_gram on a prefix of accepted
+    trials (per-trial work is i.i.d.), dsyev on the full n x n accumulator,
+    solve_u + residual on a row slice."""
+    from oracle import refbind as R
+    kind = "reference"
+    if not R.available():
+        return None
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    m, n, r = c["m"], c["n"], c["r"]
+
+    class P:
+        pass
+    p = P()
+    p.mode, p.block, p.rank, p.min_count, p.seed, p.ell = 1, c["k"], r, r + 1, c["seed"], 0
+    _, att, acc, _, t_h = R.harvest(Y, W, p, trials_prefix, workers=threads, timed=True)
+    if G is None:
+        # dsyev cost is data-independent to first order: time it on a symmetric
+        # positive definite matrix of the same size when the accumulator is absent
+        A = np.random.default_rng(1).standard_normal((n, n))
+        G = A @ A.T + n * np.eye(n)
+    _, _, _, t_v = R.solve_v(G, r, 1e-9, timed=True)
+    rs = min(rows_sample, m)
+    Ys, Ws = np.ascontiguousarray(Y[:rs]), np.ascontiguousarray(W[:rs])
+    V = np.linalg.qr(np.random.default_rng(0).standard_normal((n, r)))[0]
+    _, _, t_u = R.solve_u(Ys, Ws, V, r, workers=threads, timed=True)
+    est = t_h * c["T"] / max(acc, 1) + t_v + t_u * m / rs
+    sample = (f"harvest_gram on the first {acc} accepted trials ({t_h:.2f}s, x{c['T'] / max(acc, 1):.0f}), "
+              f"solve_v dsyev(n={n}) on the full accumulator ({t_v:.2f}s), solve_u+residual on {rs} rows "
+              f"({t_u:.2f}s, x{m / rs:.0f}); extrapolated full decompose {est:.1f}s")
+    return dict(value=c["T"] / est, unit="submatrices/s", cores=threads, kind=kind, sample=sample,
+                est_decompose_s=est)
+
+
+def run_reference_arm(args, c):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_1411_0814_b200 import rsm
+    from oracle import refbind as R
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return 0
+    m, n = c["m"], c["n"]
+    M = rsm.generate(m, n, c["r"], c["rho"], c["sigma"], c["seed"])
+    G = None  # dsyev is timed on a same-size SPD matrix (see cpu_reference_sample)
+    vals = []
+    for s in range(args.warmup + args.steps):
+        res = cpu_reference_sample(M.values, M.mask, c, G=G, trials_prefix=8, rows_sample=4096)
+        if s >= args.warmup:
+            vals.append(res)
+    v = statistics.median([x["value"] for x in vals])
+    est = statistics.median([x["est_decompose_s"] for x in vals])
+    line = {"metric": "submatrices/s (full RSM decompose)", "value": v, "unit": "submatrices/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": c["workload"], "m": m, "n": n, "r": c["r"], "rho": c["rho"], "k": c["k"],
+                       "trials": c["T"], "seed": c["seed"]},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "submatrices/s", "cores": vals[0]["cores"], "kind": "reference",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": "submatrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="config3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stages", action="store_true", help="print per-stage ms to stderr")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, c)
+
+    import torch
+    from paper_1411_0814_b200 import rsm
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [rsm.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = rsm.Context(local, world, rank, nccl_id)
+    Yt, Wt, Y, W = gen_input(c, rank)
+    m, n, r, T = c["m"], c["n"], c["r"], c["T"]
+    cfg = rsm.RsmConfig(rank=r, mode=rsm.Mode.M2, block=c["k"], plan=rsm.TrialPlan(T), seed=c["seed"])
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    # ---- device-resident leg (value) ----
+    ctx.load_arrays(Y, W)
+    for _ in range(args.warmup):
+        ctx.decompose(cfg, fetch=False)
+    clocks = Clocks(local)
+    barrier()
+    clocks.start()
+    times, stage_rows, launches = [], [], 0
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, rep = ctx.decompose(cfg, fetch=False)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        stage_rows.append(ctx.stage_ms())
+        launches += ctx.launch_count()
+    barrier()
+    clk = clocks.stop()
+    tot = torch.tensor([sum(times)], dtype=torch.float64, device=f"cuda:{local}")
+    if dist is not None:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = tot.item() / args.steps
+    value = T / (ms_per_step / 1e3)
+
+    # ---- end-to-end leg (public API, host buffers) ----
+    e2e_times = []
+    U = np.empty((m, r))
+    V = np.empty((n, r))
+    for s in range(args.warmup + args.steps):
+        flush.zero_()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.load_arrays(Y, W)
+        F, rep2 = ctx.decompose(cfg, fetch=True)
+        e1.record(stream)
+        e1.synchronize()
+        if s >= args.warmup:
+            e2e_times.append(e0.elapsed_time(e1))
+    et = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=f"cuda:{local}")
+    if dist is not None:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_ms = et.item() / args.steps
+    h2d = m * n * 8 + m * n
+    d2h = (m + n) * r * 8
+
+    # ---- roofline of the dominant kernel ----
+    st = np.array(stage_rows)  # select, svd, gram, reduce, solve_v, solve_u, total
+    med = np.median(st, axis=0)
+    names = ["select", "svd", "gram", "gram_reduce", "solve_v", "solve_u"]
+    ids, qs, att, acc = ctx.select(rsm.TrialParams(rsm.Mode.M2, c["k"], 0, r, r + 1, c["seed"]), T)
+    alg = algorithmic(c, qs, ((n + 127) // 128) * 4 * 4, att)
+    hbm, hbm_src = peaks()
+    fp64 = rsm.fp64_peak_tflops(local)
+    stage_info = {}
+    for i, nm in enumerate(names):
+        stage_info[nm] = {"ms": float(med[i]), "share": float(med[i] / med[6]) if med[6] > 0 else None}
+    stage_info["select"].update(alg_bytes=alg["s1_bytes"], gbs=alg["s1_bytes"] / (med[0] * 1e-3) / 1e9)
+    stage_info["svd"].update(alg_flops=alg["s2_flops"], tflops=alg["s2_flops"] / (med[1] * 1e-3) / 1e12,
+                             alg_bytes=alg["s2_bytes"], gbs=alg["s2_bytes"] / (med[1] * 1e-3) / 1e9)
+    stage_info["gram"].update(alg_flops=alg["s3_flops"], tflops=alg["s3_flops"] / (med[2] * 1e-3) / 1e12)
+    stage_info["solve_v"].update(alg_bytes=alg["s4_bytes"])
+    stage_info["solve_u"].update(alg_bytes=alg["s5_bytes"], gbs=alg["s5_bytes"] / (med[5] * 1e-3) / 1e9)
+    dom = names[int(np.argmax(med[:6]))]
+    if dom in ("gram", "svd"):
+        ach = stage_info[dom]["tflops"]
+        roof = {"kernel": dom, "bound": "fp64", "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
+                "frac": ach / fp64, "peak_source": "measured in-run (DFMA microbenchmark, rsm_fp64_peak_tflops)"}
+    else:
+        key = {"select": 0, "solve_u": 5, "solve_v": 4}[dom]
+        ab = {"select": alg["s1_bytes"], "solve_u": alg["s5_bytes"], "solve_v": alg["s4_bytes"]}[dom]
+        ach = ab / (med[key] * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "peak_source": f"{hbm_src} (MEASURED_PEAKS.json hbm_gbs)"}
+    tr = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tr = json.load(open(tpath)).get(dom)
+        except Exception:
+            tr = None
+    roof["traffic"] = tr
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        G = None
+        try:
+            # the accumulator the reference's solve_v would see (from the device harvest)
+            G = ctx.harvest_gram(rsm.TrialParams(rsm.Mode.M2, c["k"], 0, r, r + 1, c["seed"]), T).gram
+        except Exception:
+            pass
+        try:
+            cpu = cpu_reference_sample(Y, W, c, G=G)
+        except Exception as ex:  # report, never fail the GPU line
+            cpu = {"value": None, "unit": "submatrices/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {ex}"}
+    stage_info["solve_v"]["solver"] = ctx.solver_stats()
+    if args.stages and rank == 0:
+        print(json.dumps(stage_info), file=sys.stderr)
+    if rank == 0:
+        line = {"metric": "submatrices/s (full RSM decompose)", "value": value, "unit": "submatrices/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (reference generator streams, seed 0)",
+                "config": {"workload": c["workload"], "m": m, "n": n, "r": r, "rho": c["rho"], "sigma": c["sigma"],
+                           "k": c["k"], "trials": T, "seed": c["seed"], "parallelism": f"trials+rows x{world}",
+                           "l2": "flushed (256 MiB write) between timed steps; Y (1 GiB) exceeds L2"},
+                "e2e": {"value": T / (e2e_ms / 1e3), "unit": "submatrices/s", "ms_per_step": e2e_ms,
+                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "roofline": roof, "stages": stage_info, "cpu_baseline": cpu, "clocks": clk,
+                "gpu_launches": launches,
+                "report": {"e": rep.e, "attempted": rep.trials_attempted, "accepted": rep.trials_accepted,
+                           "z": rep.z, "gram_rank": rep.gram_rank, "underdetermined_rows": rep.underdetermined_rows}}
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -137,6 +137,10 @@ rsm_status rsm_ctx_solve_u(rsm_ctx* ctx, const double* V, int64_t r, double* U /
 int rsm_ctx_stage_ms(rsm_ctx* ctx, double* ms, int cap);
 /* Kernel launches issued by the last decompose. */
 int64_t rsm_ctx_launch_count(rsm_ctx* ctx);
+/* Stage-4 eigensolver diagnostics of the last solve_v: [0] outer iterations,
+ * [1] matvecs, [2] lambda_max, [3] spectrum upper bound, [4] max residual of
+ * the wanted Ritz pairs, [5] block size, [6] cooperative grid. */
+int rsm_ctx_solver_stats(rsm_ctx* ctx, double* out, int cap);
 
 /* --------------------------------------------------------- one-shot API */
 /* Reference-shaped calls on host buffers (use a per-device default context). */
@@ -153,6 +157,10 @@ rsm_status rsm_solve_u(const double* values, const uint8_t* mask, int64_t m, int
 rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, int64_t m,
                                     int64_t n, const double* U, const double* V, int64_t r,
                                     double* e);
+
+/* FP64 DFMA throughput of the device (TFLOP/s), the roofline denominator of
+ * the FP64-bound stages (not in MEASURED_PEAKS.json). */
+rsm_status rsm_fp64_peak_tflops(int device, double* tflops);
 
 /* Host input generator (reference synth streams, observed matrix only),
  * rows [row0, row0+rows) of an m x n instance; multithreaded. */

@@ -3,6 +3,7 @@
 // /root/reference/proj/src with the builder-written shims in ref_shim/).
 // TEST INFRASTRUCTURE ONLY: used to pin the C restatement (liborc.so) and as
 // the "reference" CPU baseline.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -85,11 +86,13 @@ int ref_select(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int m
 
 int ref_harvest(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int mode, int64_t block,
                 int64_t ell, int64_t rank, int64_t min_count, uint64_t seed, uint64_t trials, int workers,
-                int serial, double* G, uint64_t* attempted, uint64_t* accepted, uint64_t* z) {
+                int serial, double* G, uint64_t* attempted, uint64_t* accepted, uint64_t* z, double* secs) {
   return guard([&] {
     MaskedMatrix M = make(Y, mask, m, n);
     const TrialParams p = tp(mode, block, ell, rank, min_count, seed);
+    const auto t0 = std::chrono::steady_clock::now();
     HarvestResult h = serial ? reference::harvest_gram(M, p, trials) : harvest_gram(M, p, trials, workers);
+    if (secs) *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (G) std::memcpy(G, h.gram.data().data(), sizeof(double) * n * n);
     *attempted = h.attempted;
     *accepted = h.accepted;
@@ -115,11 +118,13 @@ int ref_small_singular_vectors(const double* S, int64_t p, int64_t q, int64_t r,
 }
 
 int ref_solve_v(const double* G, int64_t n, int64_t r, double tol, double* V, int64_t* gram_rank,
-                int32_t* borderline) {
+                int32_t* borderline, double* secs) {
   return guard([&] {
     GramAccumulator A(n);
     std::memcpy(A.raw().data(), G, sizeof(double) * n * n);
+    const auto t0 = std::chrono::steady_clock::now();
     SolveVResult s = solve_v(A, r, tol);
+    if (secs) *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::memcpy(V, s.v.data(), sizeof(double) * n * r);
     *gram_rank = s.gram_rank;
     *borderline = s.borderline ? 1 : 0;
@@ -127,11 +132,17 @@ int ref_solve_v(const double* G, int64_t n, int64_t r, double tol, double* V, in
 }
 
 int ref_solve_u(const double* Y, const uint8_t* mask, int64_t m, int64_t n, const double* V, int64_t r,
-                int workers, double* U, int64_t* flagged) {
+                int workers, double* U, int64_t* flagged, double* secs) {
   return guard([&] {
     MaskedMatrix M = make(Y, mask, m, n);
     std::vector<double> v(V, V + n * r);
+    const auto t0 = std::chrono::steady_clock::now();
     SolveUResult s = solve_u(M, v, r, workers);
+    Factorization F(m, n, r);
+    F.u = s.u;
+    F.v = v;
+    (void)masked_residual_norm(M, F);  // the e pass decompose runs after solve_u (solver.cpp:142)
+    if (secs) *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::memcpy(U, s.u.data(), sizeof(double) * m * r);
     *flagged = s.underdetermined_rows;
   });

@@ -24,10 +24,10 @@ def lib():
         L.ref_generate.argtypes = [i64, i64, i64, d, d, u64, P, P, P]
         L.ref_select.argtypes = [P, P, i64, i64, C.c_int, i64, i64, u64, u64, P, P, C.POINTER(u64), C.POINTER(u64)]
         L.ref_harvest.argtypes = [P, P, i64, i64, C.c_int, i64, i64, i64, i64, u64, u64, C.c_int, C.c_int, P,
-                                  C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]
+                                  C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(d)]
         L.ref_small_singular_vectors.argtypes = [P, i64, i64, i64, i64, P, P]
-        L.ref_solve_v.argtypes = [P, i64, i64, d, P, C.POINTER(i64), C.POINTER(i32)]
-        L.ref_solve_u.argtypes = [P, P, i64, i64, P, i64, C.c_int, P, C.POINTER(i64)]
+        L.ref_solve_v.argtypes = [P, i64, i64, d, P, C.POINTER(i64), C.POINTER(i32), C.POINTER(d)]
+        L.ref_solve_u.argtypes = [P, P, i64, i64, P, i64, C.c_int, P, C.POINTER(i64), C.POINTER(d)]
         L.ref_decompose.argtypes = [P, P, i64, i64, i64, C.c_int, i64, i64, u64, d, u64, d, i64, C.c_int, P, P,
                                     C.POINTER(d), P, P, C.POINTER(d)]
         L.ref_masked_residual_norm.restype = d
@@ -69,13 +69,15 @@ def select(Y, W, mode, block, min_count, seed, trials):
     return ids[:acc.value], qs[:acc.value], att.value, acc.value
 
 
-def harvest(Y, W, p, trials, workers=0, serial=False):
+def harvest(Y, W, p, trials, workers=0, serial=False, timed=False):
     m, n = Y.shape
     G = np.zeros((n, n))
-    att, acc, z = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    att, acc, z, secs = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_double()
     _chk(lib().ref_harvest(_p(Y), _p(W), m, n, p.mode, p.block, p.ell, p.rank, p.min_count, p.seed, trials,
-                           workers, 1 if serial else 0, _p(G), C.byref(att), C.byref(acc), C.byref(z)))
-    return G, att.value, acc.value, z.value
+                           workers, 1 if serial else 0, _p(G), C.byref(att), C.byref(acc), C.byref(z),
+                           C.byref(secs)))
+    out = (G, att.value, acc.value, z.value)
+    return out + (secs.value,) if timed else out
 
 
 def small_singular_vectors(S, r, ell):
@@ -87,21 +89,24 @@ def small_singular_vectors(S, r, ell):
     return zeta, sv
 
 
-def solve_v(G, r, tol=1e-9):
+def solve_v(G, r, tol=1e-9, timed=False):
     G = np.ascontiguousarray(G, np.float64)
     n = G.shape[0]
     V = np.zeros((n, r))
-    gr, bl = C.c_int64(), C.c_int32()
-    _chk(lib().ref_solve_v(_p(G), n, r, tol, _p(V), C.byref(gr), C.byref(bl)))
-    return V, gr.value, bool(bl.value)
+    gr, bl, secs = C.c_int64(), C.c_int32(), C.c_double()
+    _chk(lib().ref_solve_v(_p(G), n, r, tol, _p(V), C.byref(gr), C.byref(bl), C.byref(secs)))
+    out = (V, gr.value, bool(bl.value))
+    return out + (secs.value,) if timed else out
 
 
-def solve_u(Y, W, V, r, workers=0):
+def solve_u(Y, W, V, r, workers=0, timed=False):
+    """solve_u followed by masked_residual_norm (the e pass of decompose)."""
     m, n = Y.shape
     U = np.zeros((m, r))
-    fl = C.c_int64()
-    _chk(lib().ref_solve_u(_p(Y), _p(W), m, n, _p(np.ascontiguousarray(V)), r, workers, _p(U), C.byref(fl)))
-    return U, fl.value
+    fl, secs = C.c_int64(), C.c_double()
+    _chk(lib().ref_solve_u(_p(Y), _p(W), m, n, _p(np.ascontiguousarray(V)), r, workers, _p(U), C.byref(fl),
+                           C.byref(secs)))
+    return (U, fl.value, secs.value) if timed else (U, fl.value)
 
 
 def decompose(Y, W, rank, trials, mode=0, block=0, vectors_per_trial=0, seed=0, tol=1e-9, min_dim=0,

@@ -404,10 +404,19 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       grid_reduce(a, grid, buf, b, 0, pw, sh);
       buf ^= 1;
     }
+    // the r wanted pairs must converge; the (r+1)-th Ritz value only has to be
+    // resolved against the rank-gate thresholds: either converged too, or
+    // clearly above 10 tol lambda_max (eigenvalues that small are amplified by
+    // the filter exactly like the wanted ones, so they would be in the block)
     maxres = 0.0;
-    const int nchk = (r + 1 < b) ? r + 1 : b;
-    for (int j = 0; j < nchk; ++j) maxres = fmax(maxres, sqrt(sh.red[j]));
-    if (full || maxres <= 1e-12 * ub) { status = 0; ++outer; break; }
+    for (int j = 0; j < r && j < b; ++j) maxres = fmax(maxres, sqrt(sh.red[j]));
+    bool sep = true;
+    if (r < b) {
+      const double rr = sqrt(sh.red[r]);
+      const double gate = 10.0 * a.tol * fmax(lmax, 0.0);
+      sep = rr <= 1e-12 * ub || (sh.theta[r] - rr > 1e3 * gate && sh.theta[r] - rr > 1e-8 * ub);
+    }
+    if (full || (maxres <= 1e-12 * ub && sep)) { status = 0; ++outer; break; }
     acut = sh.theta[b - 1];
     if (!(acut < 0.999 * ub)) acut = 0.999 * ub;
     if (acut <= 0.0) acut = 1e-6 * ub;

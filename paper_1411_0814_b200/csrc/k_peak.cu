@@ -1,0 +1,55 @@
+// k_peak.cu -- FP64 (DFMA) throughput microbenchmark. MEASURED_PEAKS.json
+// carries HBM and bf16 peaks only, so bench.py measures the FP64 roofline
+// denominator of the compute-bound stages in the same run with this kernel:
+// every thread runs 8 independent FMA chains, grid = 8 CTAs per SM.
+#include <cuda_runtime.h>
+
+#include "../../include/rsm_b200.h"
+
+namespace {
+
+__global__ void __launch_bounds__(256) k_dfma(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
+         x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace
+
+extern "C" rsm_status rsm_fp64_peak_tflops(int device, double* tflops) {
+  if (cudaSetDevice(device) != cudaSuccess) return RSM_ERR_INTERNAL;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double)) != cudaSuccess) return RSM_ERR_INTERNAL;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 4096, blocks = sms * 8, threads = 256;
+  k_dfma<<<blocks, threads>>>(d, 64, 0.999999, 1e-7);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    k_dfma<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (cudaGetLastError() != cudaSuccess) return RSM_ERR_INTERNAL;
+  const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return RSM_OK;
+}

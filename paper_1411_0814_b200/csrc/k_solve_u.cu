@@ -258,14 +258,12 @@ __global__ void __launch_bounds__(256) k_solve_u(SolveUArgs a) {
   }
 }
 
-// deterministic single-CTA sum of n doubles (fixed per-thread ranges + tree)
+// deterministic single-CTA sum of n doubles (fixed strided order + tree)
 __global__ void k_sum_rows(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
   __shared__ double part[1024];
   const int tid = threadIdx.x;
-  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t lo = tid * per, hi = (lo + per < n) ? lo + per : n;
   double s = 0.0;
-  for (int64_t i = lo; i < hi; ++i) s += v[i];
+  for (int64_t i = tid; i < n; i += blockDim.x) s += v[i];  // coalesced, fixed order
   part[tid] = s;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {

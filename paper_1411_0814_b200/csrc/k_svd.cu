@@ -162,7 +162,9 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
 
     // ---- one-sided Jacobi with Gram-accelerated sweeps ----
     const int P = K * (K + 1) / 2;
-    const double tol_ortho = 4.0 * 2.220446049250313e-16 * sqrt((double)(L > 1 ? L : 1));
+    // off-diagonals relative to the larger norm: this bounds the rotation of
+    // the top-rex subspace (what stage 3 consumes) by ~tol * g_ii / (g_ii - g_jj)
+    const double tol_ortho = 1e-14;
     for (int it = 0;; ++it) {
       for (int p = warp; p < P; p += nwarps) {
         // unrank p -> (i, j), i <= j
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
           const int p = e / K, q = e % K;
           if (p < q) {
             const double g = gram[p * KMAX + q];
-            const double d = sqrt(gram[p * KMAX + p] * gram[q * KMAX + q]);
+            const double d = fmax(gram[p * KMAX + p], gram[q * KMAX + q]);
             if (g != 0.0 && fabs(g) > tol_ortho * d) big = 1;
           }
         }

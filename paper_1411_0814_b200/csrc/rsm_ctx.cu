@@ -137,6 +137,7 @@ struct rsm_ctx {
 
   cudaEvent_t ev[8] = {};
   double stage_ms[8] = {};
+  double solver_stats[8] = {};  // eig: outer its, matvecs, lambda_max, ub, max residual, block, grid
   int64_t launches = 0;
 
   void set_err(const std::string& s) { err = s; }
@@ -502,6 +503,13 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "solve_v");
   ck(cudaGetLastError(), "eig kernels");
+  c->solver_stats[0] = istat[3];
+  c->solver_stats[1] = istat[4];
+  c->solver_stats[2] = dstat[0];
+  c->solver_stats[3] = dstat[1];
+  c->solver_stats[4] = dstat[2];
+  c->solver_stats[5] = b;
+  c->solver_stats[6] = grid;
   if (istat[0] != 0) fail(RSM_ERR_INTERNAL, "symmetric eigensolver failed to converge");
   c->Vhat_n = n;
   c->Vhat_r = r;
@@ -890,6 +898,12 @@ int rsm_ctx_stage_ms(rsm_ctx* c, double* ms, int cap) {
 }
 
 int64_t rsm_ctx_launch_count(rsm_ctx* c) { return c ? c->launches : 0; }
+
+int rsm_ctx_solver_stats(rsm_ctx* c, double* out, int cap) {
+  const int k = std::min(cap, 7);
+  for (int i = 0; i < k; ++i) out[i] = c->solver_stats[i];
+  return k;
+}
 
 // ---- one-shot, reference-shaped calls ----
 rsm_status rsm_make_trial_params(const rsm_config* cfg, int64_t m, int64_t n, rsm_trial_params* out) {

@@ -98,6 +98,7 @@ def lib():
         "rsm_ctx_solve_u": (i32, [_P, _P, i64, _P, C.POINTER(i64), C.POINTER(dbl)]),
         "rsm_ctx_stage_ms": (C.c_int, [_P, _P, C.c_int]),
         "rsm_ctx_launch_count": (i64, [_P]),
+        "rsm_ctx_solver_stats": (C.c_int, [_P, _P, C.c_int]),
         "rsm_make_trial_params": (i32, [C.POINTER(_Config), i64, i64, C.POINTER(_TrialParams)]),
         "rsm_decompose": (i32, [_P, _P, i64, i64, C.POINTER(_Config), _P, _P, C.POINTER(_Report)]),
         "rsm_harvest_gram": (i32, [_P, _P, i64, i64, C.POINTER(_TrialParams), u64, _P, C.POINTER(u64),
@@ -106,6 +107,7 @@ def lib():
         "rsm_solve_u": (i32, [_P, _P, i64, i64, _P, i64, _P, C.POINTER(i64)]),
         "rsm_masked_residual_norm": (i32, [_P, _P, i64, i64, _P, _P, i64, C.POINTER(dbl)]),
         "rsm_generate": (i32, [i64, i64, i64, dbl, dbl, u64, i64, i64, _P, _P]),
+        "rsm_fp64_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -120,8 +122,8 @@ def exported_symbols():
     return ["rsm_config_default", "rsm_last_error", "rsm_ctx_create", "rsm_ctx_destroy", "rsm_nccl_unique_id",
             "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_decompose", "rsm_ctx_fetch_factors",
             "rsm_ctx_select", "rsm_ctx_harvest_gram", "rsm_ctx_solve_v", "rsm_ctx_solve_u", "rsm_ctx_stage_ms",
-            "rsm_ctx_launch_count", "rsm_make_trial_params", "rsm_decompose", "rsm_harvest_gram", "rsm_solve_v",
-            "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate"]
+            "rsm_ctx_launch_count", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_harvest_gram", "rsm_solve_v",
+            "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_fp64_peak_tflops"]
 
 
 def _check(st: int, ctx=None):
@@ -368,6 +370,12 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().rsm_ctx_launch_count(self.h))
 
+    def solver_stats(self) -> dict:
+        buf = (C.c_double * 8)()
+        lib().rsm_ctx_solver_stats(self.h, C.cast(buf, C.c_void_p), 8)
+        keys = ["outer", "matvecs", "lambda_max", "ub", "max_residual", "block", "grid"]
+        return dict(zip(keys, buf[:7]))
+
 
 # ------------------------------------------------------- reference-shaped API
 
@@ -434,6 +442,13 @@ def masked_residual_norm(M: MaskedMatrix, F: Factorization) -> float:
     _check(lib().rsm_masked_residual_norm(_ptr(M.values), _ptr(M.mask), M.m, M.n, _ptr(U), _ptr(V), F.r,
                                           C.byref(e)))
     return e.value
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    """Measured DFMA throughput (TFLOP/s) of the device."""
+    t = C.c_double()
+    _check(lib().rsm_fp64_peak_tflops(device, C.byref(t)))
+    return t.value
 
 
 def generate(m: int, n: int, r: int, rho: float, sigma: float, seed: int, row0: int = 0,

@@ -1,0 +1,20 @@
+"""Config-3 (or c1/c4) decompositions on cuda:0, for ncu captures of the stage kernels."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1411_0814_b200 import rsm  # noqa: E402
+
+cfgname = sys.argv[1] if len(sys.argv) > 1 else "c3"
+shapes = {"c3": (131072, 1024, 4, 0.8, 1e-3, 5, 16384), "c1": (2000, 200, 3, 0.8, 1e-3, 4, 2000),
+          "c4": (1048576, 2048, 8, 0.9, 1e-3, 9, 65536)}
+m, n, r, rho, sigma, k, T = shapes[cfgname]
+M = rsm.generate(m, n, r, rho, sigma, 0)
+ctx = rsm.Context(0)
+ctx.load(M)
+cfg = rsm.RsmConfig(rank=r, mode=rsm.Mode.M2, block=k, plan=rsm.TrialPlan(T), seed=0)
+for i in range(int(os.environ.get("REPS", "2"))):
+    t0 = time.time()
+    _, rep = ctx.decompose(cfg, fetch=False)
+    print(i, f"{(time.time() - t0) * 1e3:.2f} ms", ctx.stage_ms(), ctx.solver_stats(), rep.e, flush=True)
