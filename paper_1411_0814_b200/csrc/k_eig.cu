@@ -38,11 +38,11 @@ namespace {
 constexpr int ET = 256;        // threads per CTA
 constexpr int BMAX = 16;       // max block size
 constexpr int LDM = BMAX + 1;  // + power column
-constexpr int KC = 64;         // iterate rows per shared chunk
+constexpr int XS_BYTES = 96 * 1024;  // dynamic shared memory for the staged iterate
 constexpr int RPW = 2;         // rows per warp per pass
 
 struct EigShared {
-  double xs[KC * LDM];
+  double pad0;
   double H[BMAX * BMAX];
   double S[BMAX * BMAX];
   double red[LDM * (LDM + 1) / 2 + 2 * LDM + 8];
@@ -54,9 +54,11 @@ struct EigShared {
 
 __device__ __forceinline__ int pw_of(int b) { return (b + 1) * (b + 2) / 2 + 2 * (b + 1) + 8; }
 
-// Y(rows) = G * X(all rows), ncol columns, leading dimension ld
+// Y(rows) = G * X(all rows), ncol columns, leading dimension ld. The iterate
+// is staged into shared memory (xs, kc rows at a time; the whole of it when
+// it fits) with 16-byte loads, all in flight at once.
 __device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double* __restrict__ Yout,
-                       int ncol, int ld, int row_lo, int row_hi, EigShared& sh) {
+                       int ncol, int ld, int row_lo, int row_hi, double* xs, int kc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t n = a.n;
   for (int rbase = row_lo; rbase < row_hi; rbase += 8 * RPW) {
@@ -65,19 +67,31 @@ __device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double*
     for (int rr = 0; rr < RPW; ++rr)
 #pragma unroll
       for (int j = 0; j < LDM; ++j) acc[rr][j] = 0.0;
-    for (int64_t k0 = 0; k0 < n; k0 += KC) {
-      const int kn = (int)((n - k0) < KC ? (n - k0) : KC);
+    for (int64_t k0 = 0; k0 < n; k0 += kc) {
+      const int kn = (int)((n - k0) < kc ? (n - k0) : kc);
       __syncthreads();
-      for (int e = tid; e < kn * ld; e += ET) sh.xs[e] = Xin[k0 * ld + e];
+      {
+        const int tot = kn * ld;  // doubles; chunk start k0*ld is even when ld is even or k0 even
+        const double* src = Xin + k0 * ld;
+        if ((((uintptr_t)src) & 15) == 0) {
+          const double2* s2 = reinterpret_cast<const double2*>(src);
+          double2* d2 = reinterpret_cast<double2*>(xs);
+          for (int e = tid; e < tot / 2; e += ET) d2[e] = s2[e];
+          if ((tot & 1) && tid == 0) xs[tot - 1] = src[tot - 1];
+        } else {
+          for (int e = tid; e < tot; e += ET) xs[e] = src[e];
+        }
+      }
       __syncthreads();
 #pragma unroll
       for (int rr = 0; rr < RPW; ++rr) {
         const int i = rbase + warp + rr * 8;
         if (i < row_hi) {
           const double* grow = a.G + (int64_t)i * n + k0;
+#pragma unroll 4
           for (int kk = lane; kk < kn; kk += 32) {
             const double g = __ldg(grow + kk);
-            const double* x = sh.xs + kk * ld;
+            const double* x = xs + kk * ld;
 #pragma unroll
             for (int j = 0; j < LDM; ++j)
               if (j < ncol) acc[rr][j] = fma(g, x[j], acc[rr][j]);
@@ -220,6 +234,8 @@ __device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, int nc
 __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ EigShared sh;
+  extern __shared__ __align__(16) double xs_dyn[];
+  const int kc_rows = (int)((XS_BYTES / 8) / (a.b + 1));
   const int tid = threadIdx.x;
   const int64_t n = a.n;
   const int b = a.b, r = a.r, ld = b + 1, pcol = b;
@@ -250,7 +266,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     grid_reduce(a, grid, buf, 1, 1, pw, sh);
     buf ^= 1;
   }
-  const double ub = sh.red[0] > 0.0 ? sh.red[0] * (1.0 + 1e-12) : 1.0;
+  double ub = sh.red[0] > 0.0 ? sh.red[0] * (1.0 + 1e-12) : 1.0;  // ||G||_inf (rigorous)
 
   // ---- initial block: identity (full) or hashed pseudo-random columns ----
   double* X = a.X;
@@ -284,7 +300,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       double sigma = e / (0.0 - c);
       const double tau = 2.0 / sigma;
       grid.sync();  // X complete
-      matvec(a, X, Z, ld, ld, row_lo, row_hi, sh);
+      matvec(a, X, Z, ld, ld, row_lo, row_hi, xs_dyn, kc_rows);
       ++matvecs;
       for (int row = row_lo + tid; row < row_hi; row += ET) {
         const int64_t o = (int64_t)row * ld;
@@ -293,7 +309,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       }
       for (int it = 2; it <= d; ++it) {
         grid.sync();  // Y complete
-        matvec(a, Y, Z, ld, ld, row_lo, row_hi, sh);
+        matvec(a, Y, Z, ld, ld, row_lo, row_hi, xs_dyn, kc_rows);
         ++matvecs;
         const double sigma2 = 1.0 / (tau - sigma);
         for (int row = row_lo + tid; row < row_hi; row += ET) {
@@ -313,7 +329,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     }
     // ---- Rayleigh-Ritz ----
     grid.sync();  // X complete
-    matvec(a, X, Z, ld, ld, row_lo, row_hi, sh);
+    matvec(a, X, Z, ld, ld, row_lo, row_hi, xs_dyn, kc_rows);
     ++matvecs;
     {
       double* out = a.part + ((size_t)buf * gridDim.x + blockIdx.x) * pw;
@@ -416,7 +432,15 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       const double gate = 10.0 * a.tol * fmax(lmax, 0.0);
       sep = rr <= 1e-12 * ub || (sh.theta[r] - rr > 1e3 * gate && sh.theta[r] - rr > 1e-8 * ub);
     }
-    if (full || (maxres <= 1e-12 * ub && sep)) { status = 0; ++outer; break; }
+    // 1e-13 ub: one filter pass gains ~6 digits, so this rarely costs an extra
+    // pass, and it keeps the basis (and a noiseless e) at dsyev's accuracy
+    if (full || (maxres <= 1e-13 * ub && sep)) { status = 0; ++outer; break; }
+    // tighten the damping interval's top: ||G||_inf can exceed lambda_max
+    // several-fold; the power column's Rayleigh quotient (a lower bound after
+    // >= 8 matvecs) with a 10% margin is used instead. A mild underestimate
+    // only amplifies the top eigenvalues by T_d(1+eps), negligible next to the
+    // wanted end's T_d(|x0|).
+    if (outer == 0 && lmax > 0.0) ub = fmin(ub, fmax(1.1 * lmax, 1.1 * sh.theta[b - 1]));
     acut = sh.theta[b - 1];
     if (!(acut < 0.999 * ub)) acut = 0.999 * ub;
     if (acut <= 0.0) acut = 1e-6 * ub;
@@ -463,13 +487,15 @@ int eig_max_grid() {
   int dev = 0, sms = 0, nb = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eig, ET, 0);
+  cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, XS_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eig, ET, XS_BYTES);
   return sms * (nb > 0 ? nb : 1);
 }
 
 cudaError_t launch_eig(const EigArgs& a, int grid, cudaStream_t s) {
   void* args[] = {(void*)&a};
-  return cudaLaunchCooperativeKernel((void*)k_eig, dim3(grid), dim3(ET), args, 0, s);
+  cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, XS_BYTES);
+  return cudaLaunchCooperativeKernel((void*)k_eig, dim3(grid), dim3(ET), args, XS_BYTES, s);
 }
 
 void launch_sign_fix(double* V, int64_t n, int r, cudaStream_t s) {

@@ -5,44 +5,134 @@
 // attempt order (harvest.cpp:110-117). Per trial the harvested vectors sum to
 // I - V V^T on the trial's column support (see k_svd.cu), so
 //     G = diag(count) - sum_t  E_t V_t V_t^T E_t^T
-// with count[c] = number of trials whose support holds column c. This kernel
-// forms the second term with register-resident output tiles: a CTA owns a
-// 64 x (32*CPL) tile of G (8 warps x 8 rows, lane = column) and a slice of
-// the trial list; every trial's compact V rows that fall into the tile are
-// staged in shared memory (zero rows where the trial does not touch the
-// tile), and each warp applies the rank-R update to its 8 x 32*CPL block,
-// skipping rows outside the support. No atomics: each tile x slice partial
-// is written once and stage 3b sums the slices in a fixed order, so G is
-// bitwise reproducible. Only tiles touching the upper triangle are computed;
-// stage 3b mirrors them (the reference G is exactly symmetric).
+// with count[c] = number of trials whose support holds column c.
+//
+// This kernel forms the second term with register-resident output tiles: a
+// CTA owns a 64 x (32*CPL) tile of G (8 warps x 8 rows, lane = column) and a
+// slice of the trial list. For every trial the compact V rows that fall into
+// the tile's row block and column block are two contiguous segments of the
+// trial's V array (k_svd writes the rows in support order with an even
+// stride RP), so they are streamed into shared memory with 16-byte
+// cp.async copies through an NS-stage ring of CH-trial groups: the copies of
+// group g+NS-1 are in flight while group g is computed. The per-trial
+// metadata (segment offsets, support words) is loaded one 64-trial batch
+// ahead into registers and published to shared memory. Each warp applies
+// the rank-R update to its 8 x 32*CPL register block, skipping rows outside
+// the support (warp-uniform) and reading zeros for columns outside it.
+//
+// No atomics: each tile x slice partial is written once and stage 3b sums
+// the slices in a fixed order, so G is bitwise reproducible. Only tiles
+// touching the upper triangle are computed; stage 3b mirrors them (the
+// reference G is exactly symmetric).
 #include "rsm_internal.h"
 #include "rsm_dev.cuh"
 
 namespace rsmk {
 
-template <int R, int CPL>
-struct GramCfg {
-  static constexpr int TR = 64;
-  static constexpr int TC = 32 * CPL;
-  static constexpr int CH = (R <= 4) ? 8 : (R <= 8 ? 4 : 2);  // trials per staged chunk
-};
+namespace {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
 template <int R, int CPL>
-__global__ void __launch_bounds__(256) k_gram(GramArgs a) {
+struct GramCfg {
+  static constexpr int RP = (R + 1) & ~1;  // padded row stride (doubles)
+  static constexpr int TR = 64;
+  static constexpr int TC = 32 * CPL;
+  static constexpr int CH = (R <= 4) ? 4 : 2;  // trials per pipeline group
+  static constexpr int NS = 3;                 // pipeline depth (groups)
+  static constexpr int MB = 64;                // metadata batch (trials)
+  static constexpr int SLOT = (TR + TC) * RP;  // doubles per trial slot
+};
+
+struct TrialMeta {
+  long long srcI, srcJ;  // segment starts in V (doubles)
+  unsigned wI[2];
+  unsigned wJ[4];
+  int nI, nJ;
+};
+
+}  // namespace
+
+template <int R, int CPL>
+__global__ void __launch_bounds__(256, 2) k_gram(GramArgs a) {
   using C = GramCfg<R, CPL>;
-  constexpr int TR = C::TR, TC = C::TC, CH = C::CH, SPAN = TR + TC;
+  constexpr int RP = C::RP, TR = C::TR, TC = C::TC, CH = C::CH, NS = C::NS, MB = C::MB, SLOT = C::SLOT;
   extern __shared__ __align__(16) double sm[];
-  double* VI = sm;                       // [CH][TR][R]
-  double* VJ = VI + CH * TR * R;         // [CH][TC][R]
-  uint32_t* rbits = reinterpret_cast<uint32_t*>(VJ + CH * TC * R);  // [CH][2]
+  double* ring = sm;                                              // [NS][CH][SLOT]
+  TrialMeta* meta = reinterpret_cast<TrialMeta*>(ring + NS * CH * SLOT);  // [2][MB]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int2 tile = a.tiles[blockIdx.x];
   const int64_t row0 = (int64_t)tile.x * TR, col0 = (int64_t)tile.y * TC;
+  const int64_t wrow = row0 >> 5, wcol = col0 >> 5;
   const int slice = blockIdx.y;
   const int64_t per = (a.T + a.nslices - 1) / a.nslices;
-  const int64_t t_begin = slice * per;
-  const int64_t t_end = (t_begin + per < a.T) ? t_begin + per : a.T;
+  const int64_t tb = slice * per;
+  const int64_t te = (tb + per < a.T) ? tb + per : a.T;
+  const int64_t ntr = te > tb ? te - tb : 0;
+  const int64_t ngroups = (ntr + CH - 1) / CH;
+
+  // ---- metadata of one batch: thread u < MB loads trial tb + b*MB + u ----
+  long long m_off = 0;
+  unsigned m_pI = 0, m_pJ = 0, m_w[2 + CPL];
+  auto meta_load = [&](int64_t b) {
+    const int64_t t = tb + b * MB + tid;
+    if (tid < MB && b * MB + tid < ntr) {
+      m_off = __ldg(a.t_off + t);
+      m_pI = __ldg(a.t_pre + t * a.cmw + wrow);
+      m_pJ = __ldg(a.t_pre + t * a.cmw + wcol);
+      m_w[0] = __ldg(a.t_cm + t * a.cmw + wrow);
+      m_w[1] = __ldg(a.t_cm + t * a.cmw + wrow + 1);
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) m_w[2 + s] = __ldg(a.t_cm + t * a.cmw + wcol + s);
+    }
+  };
+  auto meta_store = [&](int64_t b) {
+    if (tid < MB && b * MB + tid < ntr) {
+      TrialMeta& m = meta[(b & 1) * MB + tid];
+      m.srcI = m_off + (long long)m_pI * RP;
+      m.srcJ = m_off + (long long)m_pJ * RP;
+      m.wI[0] = m_w[0];
+      m.wI[1] = m_w[1];
+      int nJ = 0;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const unsigned w = s < CPL ? m_w[2 + s] : 0u;
+        m.wJ[s] = w;
+        nJ += __popc(w);
+      }
+      m.nI = __popc(m_w[0]) + __popc(m_w[1]);
+      m.nJ = nJ;
+    }
+  };
+  // issue the copies of group g into ring stage g % NS
+  auto issue = [&](int64_t g) {
+    if (g < ngroups) {
+      double* st = ring + (g % NS) * CH * SLOT;
+#pragma unroll 1
+      for (int u = 0; u < CH; ++u) {
+        const int64_t i = g * CH + u;
+        if (i >= ntr) break;
+        const TrialMeta& m = meta[((i / MB) & 1) * MB + (i % MB)];
+        double* dI = st + u * SLOT;
+        double* dJ = dI + TR * RP;
+        const int cI = m.nI * RP / 2, cJ = m.nJ * RP / 2;
+        for (int c = tid; c < cI + cJ; c += 256) {
+          if (c < cI) cp_async16(dI + 2 * c, a.V + m.srcI + 2 * c);
+          else cp_async16(dJ + 2 * (c - cI), a.V + m.srcJ + 2 * (c - cI));
+        }
+      }
+    }
+    cp_async_commit();  // (possibly empty) group keeps the wait count uniform
+  };
 
   double acc[8][CPL];
 #pragma unroll
@@ -50,66 +140,73 @@ __global__ void __launch_bounds__(256) k_gram(GramArgs a) {
 #pragma unroll
     for (int s = 0; s < CPL; ++s) acc[i][s] = 0.0;
 
-  for (int64_t t0 = t_begin; t0 < t_end; t0 += CH) {
-    // ---- stage the chunk's V rows for the tile's row and column ranges ----
-    for (int p = tid; p < CH * SPAN; p += 256) {
-      const int u = p / SPAN, pos = p % SPAN;
-      const int64_t t = t0 + u;
-      double* dst = (pos < TR) ? VI + ((int64_t)u * TR + pos) * R
-                               : VJ + ((int64_t)u * TC + (pos - TR)) * R;
-      bool have = false;
-      if (t < t_end) {
-        const int64_t c = (pos < TR) ? row0 + pos : col0 + (pos - TR);
-        const uint32_t word = __ldg(a.t_cm + t * a.cmw + (c >> 5));
-        const uint32_t bit = 1u << (c & 31);
-        if (word & bit) {
-          const int64_t ci = __ldg(a.t_pre + t * a.cmw + (c >> 5)) + __popc(word & (bit - 1u));
-          const double* src = a.V + __ldg(a.t_off + t) + ci * R;
-#pragma unroll
-          for (int k = 0; k < R; ++k) dst[k] = __ldg(src + k);
-          have = true;
-        }
-      }
-      if (!have) {
-#pragma unroll
-        for (int k = 0; k < R; ++k) dst[k] = 0.0;
-      }
-    }
-    if (tid < CH * 2) {
-      const int u = tid >> 1, h = tid & 1;
-      const int64_t t = t0 + u;
-      rbits[tid] = (t < t_end) ? __ldg(a.t_cm + t * a.cmw + (row0 >> 5) + h) : 0u;
-    }
+  if (ngroups > 0) {
+    meta_load(0);
+    meta_store(0);
+    meta_load(1);  // batch 1 in registers, published after the first group
     __syncthreads();
-    // ---- rank-R updates of the register tile ----
+#pragma unroll
+    for (int g = 0; g < NS - 1; ++g) issue(g);
+  }
+  const int shI = (warp & 3) * 8;
+  for (int64_t g = 0; g < ngroups; ++g) {
+    // publish the next metadata batch early enough for the copies that need it
+    // (batch b+1 is published one group after batch b starts, long before
+    // issue() reaches it; buffer (b+1)&1 last served batch b-1, which is done)
+    if (g >= 1 && ((g - 1) * CH) % MB == 0) {
+      const int64_t b = ((g - 1) * CH) / MB;
+      meta_store(b + 1);
+      meta_load(b + 2);
+    }
+    __syncthreads();  // meta visible; previous compute done with the stage we refill
+    issue(g + NS - 1);
+    cp_async_wait<NS - 1>();
+    __syncthreads();  // group g landed for every thread
+    const double* st = ring + (g % NS) * CH * SLOT;
 #pragma unroll 1
     for (int u = 0; u < CH; ++u) {
-      const uint32_t rb = (rbits[u * 2 + (warp >> 2)] >> ((warp & 3) * 8)) & 0xffu;
+      const int64_t i = g * CH + u;
+      if (i >= ntr) break;
+      const TrialMeta& m = meta[((i / MB) & 1) * MB + (i % MB)];
+      const unsigned wI0 = m.wI[0], wI1 = m.wI[1];
+      const unsigned rb = ((warp < 4 ? wI0 : wI1) >> shI) & 0xffu;
       if (rb == 0) continue;  // warp-uniform
+      const double* VI = st + u * SLOT;
+      const double* VJ = VI + TR * RP;
+      // this lane's columns: compact index = support bits below it
       double vj[CPL][R];
+      int pref = 0;
 #pragma unroll
-      for (int s = 0; s < CPL; ++s)
+      for (int s = 0; s < CPL; ++s) {
+        const unsigned w = m.wJ[s];
+        const bool sel = (w >> lane) & 1u;
+        const int ci = pref + __popc(w & ((1u << lane) - 1u));
 #pragma unroll
-        for (int k = 0; k < R; ++k) vj[s][k] = VJ[((int64_t)u * TC + lane + 32 * s) * R + k];
-      const double* vib = VI + ((int64_t)u * TR + warp * 8) * R;
+        for (int k = 0; k < R; ++k) vj[s][k] = sel ? VJ[ci * RP + k] : 0.0;
+        pref += __popc(w);
+      }
+      int base = (warp < 4) ? __popc(wI0 & ((1u << shI) - 1u))
+                            : __popc(wI0) + __popc(wI1 & ((1u << shI) - 1u));
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (rb & (1u << i)) {
-          double vi[R];
+      for (int r8 = 0; r8 < 8; ++r8) {
+        if (rb & (1u << r8)) {
+          const double* vi = VI + base * RP;
+          ++base;
+          double x[R];
 #pragma unroll
-          for (int k = 0; k < R; ++k) vi[k] = vib[i * R + k];
+          for (int k = 0; k < R; ++k) x[k] = vi[k];
 #pragma unroll
           for (int s = 0; s < CPL; ++s) {
             double d = 0.0;
 #pragma unroll
-            for (int k = 0; k < R; ++k) d = fma(vi[k], vj[s][k], d);
-            acc[i][s] -= d;
+            for (int k = 0; k < R; ++k) d = fma(x[k], vj[s][k], d);
+            acc[r8][s] -= d;
           }
         }
       }
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
   // ---- write the slice partial ----
   double* out = a.P + (int64_t)slice * a.npad * a.npad;
 #pragma unroll
@@ -146,10 +243,14 @@ __global__ void k_gram_reduce(const double* __restrict__ P, int nslices, int64_t
 }
 
 template <int R, int CPL>
-static void launch_gram_t(const GramArgs& a, int ntiles, cudaStream_t s) {
+static size_t gram_smem() {
   using C = GramCfg<R, CPL>;
-  const size_t smem = sizeof(double) * (size_t)C::CH * (C::TR + C::TC) * R +
-                      sizeof(uint32_t) * C::CH * 2;
+  return sizeof(double) * (size_t)C::NS * C::CH * C::SLOT + sizeof(TrialMeta) * 2 * C::MB;
+}
+
+template <int R, int CPL>
+static void launch_gram_t(const GramArgs& a, int ntiles, cudaStream_t s) {
+  const size_t smem = gram_smem<R, CPL>();
   cudaFuncSetAttribute(k_gram<R, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)ntiles, (unsigned)a.nslices);
   k_gram<R, CPL><<<grid, 256, smem, s>>>(a);

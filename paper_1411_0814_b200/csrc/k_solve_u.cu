@@ -6,16 +6,22 @@
 // per row: gather V rows at the observed columns, complete orthogonal
 // decomposition, minimum-norm solution; the row is counted as
 // underdetermined when it has fewer than r observations or the basis
-// restricted to them is rank deficient; an empty row gets zeros. Here one
-// warp owns a row: it streams the row of Y once with 128-bit loads, selects
-// through the bit-packed mask (hidden cells hold NaN and are never read into
+// restricted to them is rank deficient; an empty row gets zeros.
+//
+// Here one warp owns a row at a time. Each warp double-buffers its rows in
+// shared memory: while row i is solved, the 16-byte cp.async copies of its
+// next row (values and mask words) are in flight, so Y is streamed from HBM
+// exactly once with all of a row's loads outstanding. The warp selects
+// through the bit-packed mask (hidden cells hold NaN and never enter
 // arithmetic), accumulates the r x r normal matrix V_O^T V_O and V_O^T y,
-// reduces them across the warp and solves by Cholesky in registers. Rows
-// whose normal matrix is singular or ill-conditioned fall back to an
-// eigendecomposition pseudo-inverse (the minimum-norm solution, as the COD
-// gives). The residual of e (masked_residual_norm, core.cpp:15-39) is formed
-// directly as sum (y - u.v)^2 in a second pass over the (L1/L2-resident)
-// row, never by the cancelling ||y||^2 - u^T b shortcut.
+// reduces them across the warp and solves by Cholesky in registers. Rows whose
+// normal matrix is singular or ill-conditioned take an eigendecomposition
+// pseudo-inverse (the minimum-norm solution, as the COD gives). The residual
+// of e (masked_residual_norm, core.cpp:15-39) is formed directly as
+// sum (y - u.v)^2 from the row still in shared memory, never by the
+// cancelling ||y||^2 - u^T b shortcut.
+#include <algorithm>
+
 #include "rsm_internal.h"
 #include "rsm_dev.cuh"
 
@@ -24,6 +30,8 @@ namespace rsmk {
 using namespace rsmd;
 
 namespace {
+
+constexpr int SU_WARPS = 4;
 
 template <int R>
 struct RowAcc {
@@ -109,45 +117,80 @@ __device__ int pinv_solve(const double* Ap, const double* b, double* u) {
   return rank;
 }
 
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes16) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+
+// issue the copies of one row (values + mask words) into a warp buffer
+__device__ __forceinline__ void issue_row(const SolveUArgs& a, int64_t row, double* ybuf, uint32_t* wbuf,
+                                          bool vec16) {
+  const int lane = threadIdx.x & 31;
+  const double* y = a.Y + row * a.n;
+  if (vec16) {
+    for (int64_t c = lane; c < a.n / 2; c += 32) cp_async(ybuf + 2 * c, y + 2 * c, 1);
+  } else {
+    for (int64_t c = lane; c < a.n; c += 32) cp_async(ybuf + c, y + c, 0);
+  }
+  const uint32_t* w = a.bitsR + row * a.nwp;  // nwp is a multiple of 4 words
+  for (int64_t c = lane; c < a.nwp / 4; c += 32) cp_async(wbuf + 4 * c, w + 4 * c, 1);
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
 }  // namespace
 
-template <int R, bool VSMEM, bool VEC2>
-__global__ void __launch_bounds__(256) k_solve_u(SolveUArgs a) {
-  extern __shared__ __align__(16) double Vs[];
-  const int lane = threadIdx.x & 31;
+template <int R, bool VSMEM>
+__global__ void __launch_bounds__(SU_WARPS * 32) k_solve_u(SolveUArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
-  const double* Vp = a.V;
+  const int64_t npd = (n + 1) & ~int64_t(1);
+  double* Vs = sm;
+  double* wb = sm + (VSMEM ? ((n * R + 1) & ~int64_t(1)) : 0);
+  const int64_t bufd = npd + a.nwp / 2;  // doubles per row buffer (values + words)
+  double* yb0 = wb + (2 * warp) * bufd;
+  double* yb1 = wb + (2 * warp + 1) * bufd;
+  // V in shared memory is stored component-major (Vs[k*n + c]) so the 32
+  // lanes of a warp, which own 32 consecutive columns, read consecutive words
   if (VSMEM) {
-    for (int64_t e = threadIdx.x; e < n * R; e += blockDim.x) Vs[e] = a.V[e];
+    for (int64_t e = threadIdx.x; e < n * R; e += blockDim.x) Vs[(e % R) * n + e / R] = a.V[e];
     __syncthreads();
-    Vp = Vs;
   }
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t row = a.row_lo + gw; row < a.row_hi; row += nw) {
-    const double* y = a.Y + row * n;
-    const uint32_t* mb = a.bitsR + row * a.nwp;
+  auto vrow = [&](int64_t c, double* v) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) v[k] = VSMEM ? Vs[k * n + c] : __ldg(a.V + c * R + k);
+  };
+  const bool vec16 = (n % 2) == 0;
+  const int64_t gw = (int64_t)blockIdx.x * SU_WARPS + warp;
+  const int64_t nw = (int64_t)gridDim.x * SU_WARPS;
+  int cur = 0;
+  int64_t row = a.row_lo + gw;
+  if (row < a.row_hi) issue_row(a, row, yb0, reinterpret_cast<uint32_t*>(yb0 + npd), vec16);
+  for (; row < a.row_hi; row += nw) {
+    double* ycur = cur ? yb1 : yb0;
+    double* ynxt = cur ? yb0 : yb1;
+    const int64_t nxt = row + nw;
+    if (nxt < a.row_hi) {
+      issue_row(a, nxt, ynxt, reinterpret_cast<uint32_t*>(ynxt + npd), vec16);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncwarp();
+    const double* y = ycur;
+    const uint32_t* wd = reinterpret_cast<const uint32_t*>(ycur + npd);
     RowAcc<R> s;
 #pragma unroll
     for (int p = 0; p < RowAcc<R>::NP; ++p) s.A[p] = 0.0;
 #pragma unroll
     for (int i = 0; i < R; ++i) s.b[i] = 0.0;
     s.nj = 0;
-    if (VEC2) {
-      for (int64_t c0 = 2 * lane; c0 < n; c0 += 64) {
-        const uint32_t w = __ldg(mb + (c0 >> 5));
-        const uint32_t sh = (uint32_t)(c0 & 31);
-        const bool k0 = (w >> sh) & 1u, k1 = (w >> (sh + 1)) & 1u;
-        if (k0 | k1) {
-          const double2 yy = __ldg(reinterpret_cast<const double2*>(y + c0));
-          if (k0) acc_add<R>(s, Vp + c0 * R, yy.x);
-          if (k1) acc_add<R>(s, Vp + (c0 + 1) * R, yy.y);
-        }
-      }
-    } else {
-      for (int64_t c = lane; c < n; c += 32) {
-        const uint32_t w = __ldg(mb + (c >> 5));
-        if ((w >> (c & 31)) & 1u) acc_add<R>(s, Vp + c * R, __ldg(y + c));
+    for (int64_t c = lane, w = 0; c < n; c += 32, ++w) {
+      if ((wd[w] >> lane) & 1u) {
+        double v[R];
+        vrow(c, v);
+        acc_add<R>(s, v, y[c]);
       }
     }
     // butterfly reduction: every lane ends with the row totals
@@ -171,7 +214,6 @@ __global__ void __launch_bounds__(256) k_solve_u(SolveUArgs a) {
       for (int i = 0; i < R; ++i) {
 #pragma unroll
         for (int j = 0; j <= i; ++j) {
-          // A(i,j) with i >= j from the upper packing (j, i)
           double v = s.A[j * R - j * (j - 1) / 2 + (i - j)];
 #pragma unroll
           for (int k = 0; k < j; ++k) v -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
@@ -206,41 +248,17 @@ __global__ void __launch_bounds__(256) k_solve_u(SolveUArgs a) {
       const int rank = pinv_solve<R>(s.A, s.b, u);
       flagged = (nj < R) || (rank < R);
     }
-    // second pass: direct residual over the known cells
+    // second pass over the row still in shared memory: direct residual
     double ss = 0.0;
-    if (VEC2) {
-      for (int64_t c0 = 2 * lane; c0 < n; c0 += 64) {
-        const uint32_t w = __ldg(mb + (c0 >> 5));
-        const uint32_t sh = (uint32_t)(c0 & 31);
-        const bool k0 = (w >> sh) & 1u, k1 = (w >> (sh + 1)) & 1u;
-        if (k0 | k1) {
-          const double2 yy = __ldg(reinterpret_cast<const double2*>(y + c0));
-          if (k0) {
-            double p = 0.0;
+    for (int64_t c = lane, w = 0; c < n; c += 32, ++w) {
+      if ((wd[w] >> lane) & 1u) {
+        double v[R];
+        vrow(c, v);
+        double p = 0.0;
 #pragma unroll
-            for (int k = 0; k < R; ++k) p = fma(u[k], Vp[c0 * R + k], p);
-            const double d = yy.x - p;
-            ss = fma(d, d, ss);
-          }
-          if (k1) {
-            double p = 0.0;
-#pragma unroll
-            for (int k = 0; k < R; ++k) p = fma(u[k], Vp[(c0 + 1) * R + k], p);
-            const double d = yy.y - p;
-            ss = fma(d, d, ss);
-          }
-        }
-      }
-    } else {
-      for (int64_t c = lane; c < n; c += 32) {
-        const uint32_t w = __ldg(mb + (c >> 5));
-        if ((w >> (c & 31)) & 1u) {
-          double p = 0.0;
-#pragma unroll
-          for (int k = 0; k < R; ++k) p = fma(u[k], Vp[c * R + k], p);
-          const double d = __ldg(y + c) - p;
-          ss = fma(d, d, ss);
-        }
+        for (int k = 0; k < R; ++k) p = fma(u[k], v[k], p);
+        const double d = y[c] - p;
+        ss = fma(d, d, ss);
       }
     }
     ss = warp_sum(ss);
@@ -255,6 +273,8 @@ __global__ void __launch_bounds__(256) k_solve_u(SolveUArgs a) {
       a.rowres[row] = ss;
       if (flagged) atomicAdd(a.flagged, 1);
     }
+    __syncwarp();  // this buffer is refilled by the next iteration's prefetch
+    cur ^= 1;
   }
 }
 
@@ -307,26 +327,25 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t vbytes = (size_t)a.n * R * sizeof(double);
-  const bool vsm = vbytes <= 96 * 1024;
-  const bool vec2 = (a.n % 2) == 0;
+  const size_t vbytes = sizeof(double) * (size_t)(((a.n * R) + 1) & ~int64_t(1));
+  const size_t bufb = sizeof(double) * (size_t)(((a.n + 1) & ~int64_t(1)) + a.nwp / 2);
+  const size_t rows_b = (size_t)SU_WARPS * 2 * bufb;
+  const bool vsm = vbytes + rows_b <= 112 * 1024;
+  const size_t smem = rows_b + (vsm ? vbytes : 0);
   const int64_t rows = a.row_hi - a.row_lo;
-  int64_t blocks = (rows + 7) / 8;
-  const int64_t cap = (int64_t)sms * 8;
-  if (blocks > cap) blocks = cap;
+  int occ = 0;
+  if (vsm) {
+    cudaFuncSetAttribute(k_solve_u<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_solve_u<R, true>, SU_WARPS * 32, smem);
+  } else {
+    cudaFuncSetAttribute(k_solve_u<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_solve_u<R, false>, SU_WARPS * 32, smem);
+  }
+  if (occ < 1) occ = 1;
+  int64_t blocks = std::min<int64_t>((rows + SU_WARPS - 1) / SU_WARPS, (int64_t)sms * occ);
   if (blocks < 1) blocks = 1;
-  const size_t smem = vsm ? vbytes : 0;
-#define RSM_SU(VS, V2)                                                                          \
-  do {                                                                                          \
-    cudaFuncSetAttribute(k_solve_u<R, VS, V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                         (int)smem);                                                            \
-    k_solve_u<R, VS, V2><<<(unsigned)blocks, 256, smem, s>>>(a);                                \
-  } while (0)
-  if (vsm && vec2) RSM_SU(true, true);
-  else if (vsm) RSM_SU(true, false);
-  else if (vec2) RSM_SU(false, true);
-  else RSM_SU(false, false);
-#undef RSM_SU
+  if (vsm) k_solve_u<R, true><<<(unsigned)blocks, SU_WARPS * 32, smem, s>>>(a);
+  else k_solve_u<R, false><<<(unsigned)blocks, SU_WARPS * 32, smem, s>>>(a);
 }
 
 void launch_solve_u(const SolveUArgs& a, cudaStream_t s) {

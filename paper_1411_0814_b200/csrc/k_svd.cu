@@ -22,6 +22,8 @@
 // Also emits, per trial, the column-support bit words and their exclusive
 // popcount prefix (the compact-index map stage 3 needs), and the per-column
 // trial counts (the identity's diagonal) with integer atomics.
+#include <algorithm>
+
 #include "rsm_internal.h"
 #include "rsm_dev.cuh"
 
@@ -243,24 +245,230 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
       }
     }
     __syncthreads();
-    const int rex = a.rex;
+    // rows are stored with an even stride rp >= rex (zero padded) so every
+    // trial's per-block segment is 16-byte aligned for stage 3's cp.async
+    const int rex = a.rex, rp = (a.rex + 1) & ~1;
     double* vout = a.Vout + a.t_off[tl];
     if (M2) {
       // V_top rows over the column support: v_i[c] = rotated_row_i[c] / sigma_i
       for (int64_t c = tid; c < L; c += nth)
-        for (int i = 0; i < rex; ++i) {
-          const int o = ord[i];
-          const double sg = sig[o];
-          vout[c * rex + i] = sg > 0.0 ? vec[o * Lp + c] / sg : 0.0;
+        for (int i = 0; i < rp; ++i) {
+          double v = 0.0;
+          if (i < rex) {
+            const int o = ord[i];
+            const double sg = sig[o];
+            v = sg > 0.0 ? vec[o * Lp + c] / sg : 0.0;
+          }
+          vout[c * rp + i] = v;
         }
     } else {
-      for (int e = tid; e < K * rex; e += nth) {
-        const int j = e / rex, i = e % rex;
-        vout[j * rex + i] = Vacc[j * KMAX + ord[i]];
+      for (int e = tid; e < K * rp; e += nth) {
+        const int j = e / rp, i = e % rp;
+        vout[j * rp + i] = i < rex ? Vacc[j * KMAX + ord[i]] : 0.0;
       }
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Row branch, warp per trial (K = k <= 9): no CTA barriers, 4 independent
+// trials per CTA. The warp ANDs the k mask rows' words, scans the popcounts
+// (shuffle scan), gathers the k x q submatrix into its shared-memory slice
+// (lane = column, coalesced row reads), then runs the same Gram-accelerated
+// one-sided Jacobi: every lane accumulates all K(K+1)/2 partial dot products
+// of its columns in registers (one pass over the data), a butterfly reduction
+// leaves the full Gram in every lane, the convergence test is evaluated
+// redundantly (warp-uniform), and only the K x K eigensolve goes through
+// shared memory.
+constexpr int SVDW_WARPS = 4;
+
+template <int K>
+__global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
+  constexpr int P = K * (K + 1) / 2;
+  extern __shared__ __align__(16) double smw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t Lp = a.Lpad;
+  const int64_t per_warp = K * Lp + 2 * K * K + 64 + 32 + a.cmw;  // doubles
+  double* S = smw + warp * per_warp;
+  double* Gs = S + K * Lp;
+  double* Ws = Gs + K * K;
+  double* cs = Ws + K * K;
+  int* pairs = reinterpret_cast<int*>(cs + 64);
+  uint32_t* cm = reinterpret_cast<uint32_t*>(cs + 96);
+  uint32_t* pre = cm + a.cmw;
+  const int rex = a.rex, rp = (a.rex + 1) & ~1;
+  const int64_t nwarps = (int64_t)gridDim.x * SVDW_WARPS;
+
+  for (int64_t t = a.t_lo + (int64_t)blockIdx.x * SVDW_WARPS + warp; t < a.t_hi; t += nwarps) {
+    const int64_t tl = t - a.t_lo;
+    const int myidx = lane < K ? a.t_idx[t * K + lane] : 0;
+    int rows[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) rows[i] = __shfl_sync(0xffffffffu, myidx, i);
+    // support words + exclusive popcount prefix (warp scan over lanes, words
+    // w = s*32 + lane)
+    int run = 0;
+    for (int64_t w0 = 0; w0 < a.cmw; w0 += 32) {
+      const int64_t w = w0 + lane;
+      uint32_t acc = 0;
+      if (w < a.nwp && w < a.cmw) {
+        acc = 0xffffffffu;
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc &= __ldg(a.bitsR + (int64_t)rows[i] * a.nwp + w);
+      }
+      const int c = __popc(acc);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (w < a.cmw) {
+        cm[w] = acc;
+        pre[w] = (uint32_t)(run + incl - c);
+        a.t_cm[tl * a.cmw + w] = acc;
+        a.t_pre[tl * a.cmw + w] = (uint32_t)(run + incl - c);
+      }
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const int L = run;
+    __syncwarp();
+    // gather S (K x L): lane = column within each 32-column word
+    for (int64_t j0 = 0; j0 < a.n; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const uint32_t word = cm[j0 >> 5];
+      const uint32_t bit = 1u << lane;
+      if (j < a.n && (word & bit)) {
+        const int c = (int)pre[j0 >> 5] + __popc(word & (bit - 1u));
+#pragma unroll
+        for (int i = 0; i < K; ++i) S[i * Lp + c] = __ldg(a.Y + (int64_t)rows[i] * a.n + j);
+        atomicAdd(a.colcnt + j, 1);
+      }
+    }
+    __syncwarp();
+    // one-sided Jacobi, Gram-accelerated
+    double g[P];
+    for (int it = 0;; ++it) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) g[p] = 0.0;
+      for (int c = lane; c < L; c += 32) {
+        double x[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
+        int p = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int j = i; j < K; ++j) {
+            g[p] = fma(x[i], x[j], g[p]);
+            ++p;
+          }
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) g[p] = warp_sum(g[p]);
+      bool big = false;
+      {
+        int p = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int j = i; j < K; ++j) {
+            if (j > i) {
+              const double dii = g[i * K - i * (i - 1) / 2];
+              const double djj = g[j * K - j * (j - 1) / 2];
+              if (g[p] != 0.0 && fabs(g[p]) > 1e-14 * fmax(dii, djj)) big = true;
+            }
+            ++p;
+          }
+      }
+      if (!big || it >= 6) break;  // warp-uniform
+      {
+        int p = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int j = i; j < K; ++j) {
+            if (lane == 0) {
+              Gs[i * K + j] = g[p];
+              Gs[j * K + i] = g[p];
+            }
+            ++p;
+          }
+      }
+      __syncwarp();
+      warp_jacobi_eig(Gs, K, Ws, K, K, cs, pairs, 2.220446049250313e-16, 40, true);
+      __syncwarp();
+      for (int c = lane; c < L; c += 32) {
+        double x[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          double y = 0.0;
+#pragma unroll
+          for (int i = 0; i < K; ++i) y = fma(Ws[i * K + j], x[i], y);
+          S[j * Lp + c] = y;
+        }
+      }
+      __syncwarp();
+    }
+    // descending norms (stable), then the top rows, normalised
+    double sig[K];
+    int ord[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      sig[i] = sqrt(fmax(g[i * K - i * (i - 1) / 2], 0.0));
+      ord[i] = i;
+    }
+    // stable bubble sort on K <= 9 entries (ties keep the lower index first)
+    for (int pass = 0; pass < K - 1; ++pass)
+      for (int j = 0; j < K - 1 - pass; ++j)
+        if (sig[ord[j]] < sig[ord[j + 1]]) {
+          const int tmp = ord[j];
+          ord[j] = ord[j + 1];
+          ord[j + 1] = tmp;
+        }
+    double inv[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) inv[i] = sig[ord[i]] > 0.0 ? 1.0 / sig[ord[i]] : 0.0;
+    double* vout = a.Vout + a.t_off[tl];
+    for (int c = lane; c < L; c += 32) {
+      for (int i = 0; i < rp; ++i) {
+        // same rounding as the CTA kernel: rotated row / sigma
+        const double v = (i < rex && i < K && inv[i] > 0.0) ? S[ord[i] * Lp + c] / sig[ord[i]] : 0.0;
+        vout[c * rp + i] = v;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+size_t svd_warp_smem(int K, int64_t Lpad, int64_t cmw) {
+  return sizeof(double) * (size_t)SVDW_WARPS * (K * Lpad + 2 * K * K + 64 + 32 + cmw);
+}
+
+bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s) {
+  const int K = a.block;
+  if (K < 2 || K > 9) return false;
+  const size_t smem = svd_warp_smem(K, a.Lpad, a.cmw);
+  if (smem > 200 * 1024) return false;
+  const int64_t Tl = a.t_hi - a.t_lo;
+#define RSM_SVDW(KK)                                                                                \
+  case KK: {                                                                                        \
+    cudaFuncSetAttribute(k_svd_warp<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+    int occ = 0;                                                                                    \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_svd_warp<KK>, SVDW_WARPS * 32, smem);     \
+    if (occ < 1) occ = 1;                                                                           \
+    const int64_t grid = std::min<int64_t>((Tl + SVDW_WARPS - 1) / SVDW_WARPS, (int64_t)sms * occ); \
+    k_svd_warp<KK><<<(unsigned)std::max<int64_t>(grid, 1), SVDW_WARPS * 32, smem, s>>>(a);          \
+    return true;                                                                                    \
+  }
+  switch (K) {
+    RSM_SVDW(2) RSM_SVDW(3) RSM_SVDW(4) RSM_SVDW(5) RSM_SVDW(6) RSM_SVDW(7) RSM_SVDW(8) RSM_SVDW(9)
+    default: return false;
+  }
+#undef RSM_SVDW
 }
 
 size_t svd_smem_fixed(int64_t cmw) {

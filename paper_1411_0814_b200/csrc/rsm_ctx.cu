@@ -362,7 +362,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   for (int64_t t = 0; t < Tacc; ++t) z += m2 ? (uint64_t)(hq[t] - rex) : (uint64_t)p->ell;
   for (int64_t t = 0; t < Tl; ++t) {
     const int64_t cols = m2 ? hq[t_lo + t] : K;
-    off[t + 1] = off[t] + cols * rex;
+    off[t + 1] = off[t] + cols * ((rex + 1) & ~1);  // even row stride (k_svd.cu)
   }
   out.z = z;
   c->G.ensure(sizeof(double) * n * n);
@@ -406,7 +406,8 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     }
     a.Lpad = Lpad;
     a.use_smem = use_smem ? 1 : 0;
-    rsmk::launch_svd(a, m2, (int)grid, smem, c->stream);
+    // row branch with k <= 9: warp-per-trial kernel; otherwise CTA per trial
+    if (!(m2 && rsmk::launch_svd_warp(a, c->sms, c->stream))) rsmk::launch_svd(a, m2, (int)grid, smem, c->stream);
     ++c->launches;
     ck(cudaGetLastError(), "svd launch");
   }
@@ -417,7 +418,8 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   const int64_t ntiles = ntiles_for(npad, cpl);
   int nslices = 1;
   if (Tl > 0) {
-    nslices = (int)std::max<int64_t>(1, ceil_div(2 * (int64_t)c->sms, ntiles));
+    // at most one wave of the 2-CTA/SM kernel: floor(2*SMs / tiles) slices
+    nslices = (int)std::max<int64_t>(1, (2 * (int64_t)c->sms) / ntiles);
     nslices = (int)std::min<int64_t>(nslices, std::max<int64_t>(1, Tl / 16));
     c->P.ensure(sizeof(double) * (size_t)nslices * npad * npad);
     rsmk::GramArgs g{};

@@ -103,6 +103,7 @@ void launch_accept(const int32_t* q, const int32_t* idx, int64_t count, int32_t 
 size_t svd_smem_fixed(int64_t cmw);
 void launch_svd(const SvdArgs& a, bool m2, int grid, size_t smem, cudaStream_t s);
 int svd_occupancy(bool m2, size_t smem);
+bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s);  // row branch, k <= 9
 // k_gram.cu
 int gram_cols_per_lane(int R);
 void launch_gram(const GramArgs& a, int ntiles, cudaStream_t s);

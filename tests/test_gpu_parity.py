@@ -240,7 +240,8 @@ def _e2e(M, cfg):
     assert rep.underdetermined_rows == rep_o.underdetermined_rows
     uv, uv_o = F.u @ F.v.T, U_o @ V_o.T
     assert rel_fro(uv, uv_o) <= UV_TOL
-    assert abs(rep.e - rep_o.e) <= 1e-9 * max(rep_o.e, 1e-12) + 1e-14
+    # e relative to the reference's, with an absolute floor at the rounding level of unit-scale data
+    assert abs(rep.e - rep_o.e) <= 1e-9 * rep_o.e + 1e-12
     return F, rep
 
 
