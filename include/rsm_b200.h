@@ -161,6 +161,8 @@ rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, i
 /* FP64 DFMA throughput of the device (TFLOP/s), the roofline denominator of
  * the FP64-bound stages (not in MEASURED_PEAKS.json). */
 rsm_status rsm_fp64_peak_tflops(int device, double* tflops);
+/* FP64 tensor-core (DMMA m8n8k4) throughput of the device (TFLOP/s). */
+rsm_status rsm_dmma_peak_tflops(int device, double* tflops);
 
 /* Host input generator (reference synth streams, observed matrix only),
  * rows [row0, row0+rows) of an m x n instance; multithreaded. */

@@ -246,15 +246,24 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   int matvecs = 0;
   const bool full = (b >= n);  // block = whole space
 
-  // ---- ub = ||G||_inf ----
+  // ---- ub: an upper bound of the spectrum ----
+  // With the accumulator's structure G = diag(count) - sum E V V^T E^T (a PSD
+  // matrix subtracted from a diagonal), lambda_max(G) <= max count: a tight,
+  // rigorous bound (a.cnt, up to rounding of the PSD part). Otherwise (a G
+  // supplied by the caller) ||G||_inf.
   {
     double mx = 0.0;
     const int warp = tid >> 5, lane = tid & 31;
-    for (int row = row_lo + warp; row < row_hi; row += ET / 32) {
-      double s = 0.0;
-      for (int64_t k = lane; k < n; k += 32) s += fabs(__ldg(a.G + (int64_t)row * n + k));
-      s = warp_sum(s);
-      mx = fmax(mx, s);
+    if (a.cnt) {
+      for (int row = row_lo + tid; row < row_hi; row += ET) mx = fmax(mx, (double)a.cnt[row]);
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    } else {
+      for (int row = row_lo + warp; row < row_hi; row += ET / 32) {
+        double s = 0.0;
+        for (int64_t k = lane; k < n; k += 32) s += fabs(__ldg(a.G + (int64_t)row * n + k));
+        s = warp_sum(s);
+        mx = fmax(mx, s);
+      }
     }
     if (lane == 0) sh.red[warp] = mx;
     __syncthreads();
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     grid_reduce(a, grid, buf, 1, 1, pw, sh);
     buf ^= 1;
   }
-  double ub = sh.red[0] > 0.0 ? sh.red[0] * (1.0 + 1e-12) : 1.0;  // ||G||_inf (rigorous)
+  double ub = sh.red[0] > 0.0 ? sh.red[0] * (1.0 + 1e-10) : 1.0;  // rigorous
 
   // ---- initial block: identity (full) or hashed pseudo-random columns ----
   double* X = a.X;
@@ -440,7 +449,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     // >= 8 matvecs) with a 10% margin is used instead. A mild underestimate
     // only amplifies the top eigenvalues by T_d(1+eps), negligible next to the
     // wanted end's T_d(|x0|).
-    if (outer == 0 && lmax > 0.0) ub = fmin(ub, fmax(1.1 * lmax, 1.1 * sh.theta[b - 1]));
+    if (outer == 0 && lmax > 0.0 && !a.cnt) ub = fmin(ub, fmax(1.1 * lmax, 1.1 * sh.theta[b - 1]));
     acut = sh.theta[b - 1];
     if (!(acut < 0.999 * ub)) acut = 0.999 * ub;
     if (acut <= 0.0) acut = 1e-6 * ub;

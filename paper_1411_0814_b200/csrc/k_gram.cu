@@ -56,7 +56,8 @@ struct TrialMeta {
   long long srcI, srcJ;  // segment starts in V (doubles)
   unsigned wI[2];
   unsigned wJ[4];
-  int nI, nJ;
+  int preI[2];  // support bits before each row-block word
+  int preJ[4];  // support bits before each column-block word
 };
 
 }  // namespace
@@ -102,32 +103,36 @@ __global__ void __launch_bounds__(256, 2) k_gram(GramArgs a) {
       m.srcJ = m_off + (long long)m_pJ * RP;
       m.wI[0] = m_w[0];
       m.wI[1] = m_w[1];
-      int nJ = 0;
+      m.preI[0] = 0;
+      m.preI[1] = __popc(m_w[0]);
+      int run = 0;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const unsigned w = s < CPL ? m_w[2 + s] : 0u;
         m.wJ[s] = w;
-        nJ += __popc(w);
+        m.preJ[s] = run;
+        run += __popc(w);
       }
-      m.nI = __popc(m_w[0]) + __popc(m_w[1]);
-      m.nJ = nJ;
     }
   };
-  // issue the copies of group g into ring stage g % NS
+  // Issue the copies of group g into ring stage g % NS: per trial the two
+  // compact segments (support rows of the tile's row block, support columns
+  // of its column block), contiguous in V, as 16-byte cp.async chunks.
   auto issue = [&](int64_t g) {
     if (g < ngroups) {
       double* st = ring + (g % NS) * CH * SLOT;
+      const int64_t i0 = g * CH;
+      const int nt = (int)((ntr - i0) < CH ? (ntr - i0) : CH);
 #pragma unroll 1
-      for (int u = 0; u < CH; ++u) {
-        const int64_t i = g * CH + u;
-        if (i >= ntr) break;
+      for (int u = 0; u < nt; ++u) {
+        const int64_t i = i0 + u;
         const TrialMeta& m = meta[((i / MB) & 1) * MB + (i % MB)];
-        double* dI = st + u * SLOT;
-        double* dJ = dI + TR * RP;
-        const int cI = m.nI * RP / 2, cJ = m.nJ * RP / 2;
+        double* slot = st + u * SLOT;
+        const int cI = (m.preI[1] + __popc(m.wI[1])) * (RP / 2);
+        const int cJ = (m.preJ[3] + __popc(m.wJ[3])) * (RP / 2);
         for (int c = tid; c < cI + cJ; c += 256) {
-          if (c < cI) cp_async16(dI + 2 * c, a.V + m.srcI + 2 * c);
-          else cp_async16(dJ + 2 * (c - cI), a.V + m.srcJ + 2 * (c - cI));
+          if (c < cI) cp_async16(slot + 2 * c, a.V + m.srcI + 2 * c);
+          else cp_async16(slot + TR * RP + 2 * (c - cI), a.V + m.srcJ + 2 * (c - cI));
         }
       }
     }
@@ -173,35 +178,36 @@ __global__ void __launch_bounds__(256, 2) k_gram(GramArgs a) {
       if (rb == 0) continue;  // warp-uniform
       const double* VI = st + u * SLOT;
       const double* VJ = VI + TR * RP;
-      // this lane's columns: compact index = support bits below it
-      double vj[CPL][R];
-      int pref = 0;
+      // this lane's columns: compact index = support bits below it (zeros outside)
+      double vj[CPL][RP];
 #pragma unroll
       for (int s = 0; s < CPL; ++s) {
         const unsigned w = m.wJ[s];
         const bool sel = (w >> lane) & 1u;
-        const int ci = pref + __popc(w & ((1u << lane) - 1u));
+        const int cj = m.preJ[s] + __popc(w & ((1u << lane) - 1u));
 #pragma unroll
-        for (int k = 0; k < R; ++k) vj[s][k] = sel ? VJ[ci * RP + k] : 0.0;
-        pref += __popc(w);
+        for (int h = 0; h < RP / 2; ++h) {
+          const double2 t = sel ? reinterpret_cast<const double2*>(VJ + cj * RP)[h] : make_double2(0.0, 0.0);
+          vj[s][2 * h] = t.x;
+          vj[s][2 * h + 1] = t.y;
+        }
       }
-      int base = (warp < 4) ? __popc(wI0 & ((1u << shI) - 1u))
-                            : __popc(wI0) + __popc(wI1 & ((1u << shI) - 1u));
+      int ci = (warp < 4) ? __popc(wI0 & ((1u << shI) - 1u)) : m.preI[1] + __popc(wI1 & ((1u << shI) - 1u));
 #pragma unroll
       for (int r8 = 0; r8 < 8; ++r8) {
-        if (rb & (1u << r8)) {
-          const double* vi = VI + base * RP;
-          ++base;
-          double x[R];
+        if (rb & (1u << r8)) {  // warp-uniform
+          double x[RP];
 #pragma unroll
-          for (int k = 0; k < R; ++k) x[k] = vi[k];
-#pragma unroll
-          for (int s = 0; s < CPL; ++s) {
-            double d = 0.0;
-#pragma unroll
-            for (int k = 0; k < R; ++k) d = fma(x[k], vj[s][k], d);
-            acc[r8][s] -= d;
+          for (int h = 0; h < RP / 2; ++h) {
+            const double2 t = reinterpret_cast<const double2*>(VI + ci * RP)[h];
+            x[2 * h] = t.x;
+            x[2 * h + 1] = t.y;
           }
+          ++ci;
+#pragma unroll
+          for (int s = 0; s < CPL; ++s)
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc[r8][s] = fma(-x[k], vj[s][k], acc[r8][s]);
         }
       }
     }
@@ -257,6 +263,8 @@ static void launch_gram_t(const GramArgs& a, int ntiles, cudaStream_t s) {
 }
 
 int gram_cols_per_lane(int R) { return R <= 4 ? 4 : (R <= 8 ? 2 : 1); }
+
+int gram_ctas_per_sm(int) { return 2; }
 
 void launch_gram(const GramArgs& a, int ntiles, cudaStream_t s) {
   switch (a.R) {

@@ -22,7 +22,53 @@ __global__ void __launch_bounds__(256) k_dfma(double* out, int iters, double a, 
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) throughput: 4 independent
+// accumulator fragments per warp
+__global__ void __launch_bounds__(256) k_dmma(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 0.999;
+  double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[u][0]), "+d"(c[u][1])
+                   : "d"(a), "d"(b));
+  }
+  const double s = c[0][0] + c[1][1] + c[2][0] + c[3][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace
+
+extern "C" rsm_status rsm_dmma_peak_tflops(int device, double* tflops) {
+  if (cudaSetDevice(device) != cudaSuccess) return RSM_ERR_INTERNAL;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double)) != cudaSuccess) return RSM_ERR_INTERNAL;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 8192, blocks = sms * 4, threads = 256;
+  k_dmma<<<blocks, threads>>>(d, 64);
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    k_dmma<<<blocks, threads>>>(d, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (cudaGetLastError() != cudaSuccess) return RSM_ERR_INTERNAL;
+  const double flops = 2.0 * 8 * 8 * 4 * 4.0 * (double)iters * blocks * (threads / 32);
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return RSM_OK;
+}
 
 extern "C" rsm_status rsm_fp64_peak_tflops(int device, double* tflops) {
   if (cudaSetDevice(device) != cudaSuccess) return RSM_ERR_INTERNAL;

@@ -186,12 +186,24 @@ __global__ void __launch_bounds__(SU_WARPS * 32) k_solve_u(SolveUArgs a) {
 #pragma unroll
     for (int i = 0; i < R; ++i) s.b[i] = 0.0;
     s.nj = 0;
-    for (int64_t c = lane, w = 0; c < n; c += 32, ++w) {
-      if ((wd[w] >> lane) & 1u) {
-        double v[R];
-        vrow(c, v);
-        acc_add<R>(s, v, y[c]);
-      }
+    // branchless: unknown cells contribute zero vectors (selected, never
+    // multiplied, so the NaN at hidden cells never enters arithmetic)
+    const int nfull = (int)(n >> 5);
+    for (int w = 0; w < nfull; ++w) {
+      const int c = w * 32 + lane;
+      const bool k = (wd[w] >> lane) & 1u;
+      double v[R];
+      vrow(c, v);
+#pragma unroll
+      for (int q = 0; q < R; ++q) v[q] = k ? v[q] : 0.0;
+      acc_add<R>(s, v, k ? y[c] : 0.0);
+      s.nj += k ? 0 : -1;  // acc_add counted one
+    }
+    if ((int64_t)nfull * 32 + lane < n && ((wd[nfull] >> lane) & 1u)) {
+      const int c = nfull * 32 + lane;
+      double v[R];
+      vrow(c, v);
+      acc_add<R>(s, v, y[c]);
     }
     // butterfly reduction: every lane ends with the row totals
 #pragma unroll
@@ -250,16 +262,26 @@ __global__ void __launch_bounds__(SU_WARPS * 32) k_solve_u(SolveUArgs a) {
     }
     // second pass over the row still in shared memory: direct residual
     double ss = 0.0;
-    for (int64_t c = lane, w = 0; c < n; c += 32, ++w) {
-      if ((wd[w] >> lane) & 1u) {
-        double v[R];
-        vrow(c, v);
-        double p = 0.0;
+    for (int w = 0; w < nfull; ++w) {
+      const int c = w * 32 + lane;
+      const bool k = (wd[w] >> lane) & 1u;
+      double v[R];
+      vrow(c, v);
+      double p = 0.0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) p = fma(u[k], v[k], p);
-        const double d = y[c] - p;
-        ss = fma(d, d, ss);
-      }
+      for (int q = 0; q < R; ++q) p = fma(u[q], v[q], p);
+      const double d = k ? y[c] - p : 0.0;
+      ss = fma(d, d, ss);
+    }
+    if ((int64_t)nfull * 32 + lane < n && ((wd[nfull] >> lane) & 1u)) {
+      const int c = nfull * 32 + lane;
+      double v[R];
+      vrow(c, v);
+      double p = 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) p = fma(u[q], v[q], p);
+      const double d = y[c] - p;
+      ss = fma(d, d, ss);
     }
     ss = warp_sum(ss);
     if (lane < R) {

@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
     // rows are stored with an even stride rp >= rex (zero padded) so every
     // trial's per-block segment is 16-byte aligned for stage 3's cp.async
     const int rex = a.rex, rp = (a.rex + 1) & ~1;
+    // compact layout: support column c (ascending) -> row c, stride rp
     double* vout = a.Vout + a.t_off[tl];
     if (M2) {
       // V_top rows over the column support: v_i[c] = rotated_row_i[c] / sigma_i
@@ -432,6 +433,7 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     double inv[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) inv[i] = sig[ord[i]] > 0.0 ? 1.0 / sig[ord[i]] : 0.0;
+    // compact layout: support column c (in ascending order) -> row c, stride rp
     double* vout = a.Vout + a.t_off[tl];
     for (int c = lane; c < L; c += 32) {
       for (int i = 0; i < rp; ++i) {

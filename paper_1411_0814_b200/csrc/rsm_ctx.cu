@@ -131,6 +131,7 @@ struct rsm_ctx {
   int64_t tiles_n = -1;
   int tiles_cpl = 0;
   int64_t G_n = 0;      // accumulator on device valid for this n
+  bool G_harvest = false;  // G = diag(colcnt) - PSD (from our harvest, single rank)
   int64_t Vhat_n = 0, Vhat_r = 0;
   bool oriented_T = false;  // last decompose ran on the transpose
   int64_t U_m = 0, U_r = 0;
@@ -360,9 +361,12 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   std::vector<int64_t> off(Tl + 1, 0);
   uint64_t z = 0;
   for (int64_t t = 0; t < Tacc; ++t) z += m2 ? (uint64_t)(hq[t] - rex) : (uint64_t)p->ell;
+  // stage 2 writes each trial's top vectors compactly (support columns in
+  // ascending order) with an even row stride, so every per-block segment is
+  // 16-byte aligned for stage 3's cp.async
   for (int64_t t = 0; t < Tl; ++t) {
     const int64_t cols = m2 ? hq[t_lo + t] : K;
-    off[t + 1] = off[t] + cols * ((rex + 1) & ~1);  // even row stride (k_svd.cu)
+    off[t + 1] = off[t] + cols * ((rex + 1) & ~1);
   }
   out.z = z;
   c->G.ensure(sizeof(double) * n * n);
@@ -419,7 +423,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   int nslices = 1;
   if (Tl > 0) {
     // at most one wave of the 2-CTA/SM kernel: floor(2*SMs / tiles) slices
-    nslices = (int)std::max<int64_t>(1, (2 * (int64_t)c->sms) / ntiles);
+    nslices = (int)std::max<int64_t>(1, ((int64_t)rsmk::gram_ctas_per_sm(rex) * c->sms) / ntiles);
     nslices = (int)std::min<int64_t>(nslices, std::max<int64_t>(1, Tl / 16));
     c->P.ensure(sizeof(double) * (size_t)nslices * npad * npad);
     rsmk::GramArgs g{};
@@ -447,6 +451,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   record(c, 4);
   ck(cudaGetLastError(), "gram reduce");
   c->G_n = n;
+  c->G_harvest = (c->world == 1);
   return out;
 }
 
@@ -494,6 +499,7 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   a.istat = c->eI.as<int>();
   a.dstat = c->eD.as<double>();
   a.max_outer = 60;
+  a.cnt = c->G_harvest ? c->colcnt.as<int>() : nullptr;
   ck(rsmk::launch_eig(a, grid, c->stream), "cooperative eig launch");
   rsmk::launch_sign_fix(c->Vhat.as<double>(), n, (int)r, c->stream);
   c->launches += 2;
@@ -862,6 +868,7 @@ rsm_status rsm_ctx_solve_v(rsm_ctx* c, const double* G, int64_t n, int64_t r, do
       c->G.ensure(sizeof(double) * n * n);
       ck(cudaMemcpyAsync(c->G.p, G, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "H2D G");
       c->G_n = n;
+      c->G_harvest = false;
     }
     SolveVOut o = solve_v_impl(c, n, r, tol);
     if (V) ck(cudaMemcpyAsync(V, c->Vhat.p, sizeof(double) * n * r, cudaMemcpyDeviceToHost, c->stream), "D2H V");

@@ -69,6 +69,7 @@ struct EigArgs {
   int* istat;       // [0] status, [1] gram_rank (low), [2] borderline, [3] outer its, [4] matvecs
   double* dstat;    // [0] lambda_max, [1] ub, [2] max residual
   int max_outer;
+  const int* cnt;   // per-column trial counts when G = diag(cnt) - PSD (else null)
 };
 
 struct SolveUArgs {
@@ -106,6 +107,7 @@ int svd_occupancy(bool m2, size_t smem);
 bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s);  // row branch, k <= 9
 // k_gram.cu
 int gram_cols_per_lane(int R);
+int gram_ctas_per_sm(int R);
 void launch_gram(const GramArgs& a, int ntiles, cudaStream_t s);
 void launch_gram_reduce(const double* P, int nslices, int64_t npad, int64_t n, const int* cnt,
                         double* G, cudaStream_t s);

@@ -108,6 +108,7 @@ def lib():
         "rsm_masked_residual_norm": (i32, [_P, _P, i64, i64, _P, _P, i64, C.POINTER(dbl)]),
         "rsm_generate": (i32, [i64, i64, i64, dbl, dbl, u64, i64, i64, _P, _P]),
         "rsm_fp64_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
+        "rsm_dmma_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -123,7 +124,8 @@ def exported_symbols():
             "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_decompose", "rsm_ctx_fetch_factors",
             "rsm_ctx_select", "rsm_ctx_harvest_gram", "rsm_ctx_solve_v", "rsm_ctx_solve_u", "rsm_ctx_stage_ms",
             "rsm_ctx_launch_count", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_harvest_gram", "rsm_solve_v",
-            "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_fp64_peak_tflops"]
+            "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_fp64_peak_tflops",
+            "rsm_dmma_peak_tflops"]
 
 
 def _check(st: int, ctx=None):
@@ -448,6 +450,13 @@ def fp64_peak_tflops(device: int = 0) -> float:
     """Measured DFMA throughput (TFLOP/s) of the device."""
     t = C.c_double()
     _check(lib().rsm_fp64_peak_tflops(device, C.byref(t)))
+    return t.value
+
+
+def dmma_peak_tflops(device: int = 0) -> float:
+    """Measured FP64 tensor-core (DMMA) throughput (TFLOP/s) of the device."""
+    t = C.c_double()
+    _check(lib().rsm_dmma_peak_tflops(device, C.byref(t)))
     return t.value
 
 
