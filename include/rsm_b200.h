@@ -96,6 +96,9 @@ const char* rsm_last_error(const rsm_ctx* ctx);
 rsm_status rsm_ctx_create(rsm_ctx** out, int device, int world, int rank, const void* nccl_id);
 rsm_status rsm_ctx_destroy(rsm_ctx* ctx);
 rsm_status rsm_nccl_unique_id(void* out128);
+/* Work split across ranks (host-only, no device): rank owns [lo, hi) of
+ * total units -- accepted trials in stage 2-3, rows in stage 5. */
+void rsm_shard_range(int64_t total, int world, int rank, int64_t* lo, int64_t* hi);
 /* cudaStream_t the context launches on (for event timing by callers). */
 void* rsm_ctx_stream(rsm_ctx* ctx);
 

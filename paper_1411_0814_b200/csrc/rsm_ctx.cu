@@ -356,7 +356,8 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   }
   if (rex < 1 || rex > 16) fail(RSM_ERR_INVALID_CONFIG, "device path supports 1 <= block-vectors <= 16 top vectors");
   // local trial range (trials shard over ranks, no communication needed)
-  const int64_t t_lo = Tacc * c->rank / c->world, t_hi = Tacc * (c->rank + 1) / c->world;
+  int64_t t_lo, t_hi;
+  rsm_shard_range(Tacc, c->world, c->rank, &t_lo, &t_hi);
   const int64_t Tl = t_hi - t_lo;
   std::vector<int64_t> off(Tl + 1, 0);
   uint64_t z = 0;
@@ -558,7 +559,8 @@ SolveUOut solve_u_impl(rsm_ctx* c, const View& v, int64_t r) {
   c->flagged.ensure(sizeof(int) * 2);
   c->dsum.ensure(sizeof(double) * 2);
   ck(cudaMemsetAsync(c->flagged.p, 0, sizeof(int) * 2, c->stream), "memset");
-  const int64_t lo = v.m * c->rank / c->world, hi = v.m * (c->rank + 1) / c->world;
+  int64_t lo, hi;
+  rsm_shard_range(v.m, c->world, c->rank, &lo, &hi);
   rsmk::SolveUArgs a{};
   a.Y = v.Y; a.bitsR = v.bitsR;
   a.m = v.m; a.n = v.n; a.nwp = v.nwp;
@@ -602,7 +604,8 @@ SolveUOut solve_u_impl(rsm_ctx* c, const View& v, int64_t r) {
     if (g_nccl.allGather(sendb, pad.p, (size_t)(maxrows * r), kNcclFloat64, c->comm, c->stream) != 0)
       fail(RSM_ERR_INTERNAL, "ncclAllGather failed");
     for (int g = 0; g < c->world; ++g) {
-      const int64_t glo = v.m * g / c->world, ghi = v.m * (g + 1) / c->world;
+      int64_t glo, ghi;
+      rsm_shard_range(v.m, c->world, g, &glo, &ghi);
       ck(cudaMemcpyAsync(c->U.as<double>() + glo * r, pad.as<double>() + (size_t)g * maxrows * r,
                          sizeof(double) * (ghi - glo) * r, cudaMemcpyDeviceToDevice, c->stream), "D2D");
     }
@@ -711,6 +714,12 @@ rsm_status guard(rsm_ctx* c, F&& f) {
 
 // ======================================================================== C-ABI
 extern "C" {
+
+void rsm_shard_range(int64_t total, int world, int rank, int64_t* lo, int64_t* hi) {
+  // contiguous, balanced, deterministic: rank g owns [total*g/world, total*(g+1)/world)
+  *lo = total * rank / world;
+  *hi = total * (rank + 1) / world;
+}
 
 void rsm_config_default(rsm_config* cfg) {
   std::memset(cfg, 0, sizeof(*cfg));

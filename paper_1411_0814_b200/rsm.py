@@ -109,6 +109,7 @@ def lib():
         "rsm_generate": (i32, [i64, i64, i64, dbl, dbl, u64, i64, i64, _P, _P]),
         "rsm_fp64_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
         "rsm_dmma_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
+        "rsm_shard_range": (None, [i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -125,7 +126,7 @@ def exported_symbols():
             "rsm_ctx_select", "rsm_ctx_harvest_gram", "rsm_ctx_solve_v", "rsm_ctx_solve_u", "rsm_ctx_stage_ms",
             "rsm_ctx_launch_count", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_harvest_gram", "rsm_solve_v",
             "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_fp64_peak_tflops",
-            "rsm_dmma_peak_tflops"]
+            "rsm_dmma_peak_tflops", "rsm_shard_range"]
 
 
 def _check(st: int, ctx=None):
@@ -451,6 +452,13 @@ def fp64_peak_tflops(device: int = 0) -> float:
     t = C.c_double()
     _check(lib().rsm_fp64_peak_tflops(device, C.byref(t)))
     return t.value
+
+
+def shard_range(total: int, world: int, rank: int):
+    """The library's work split: rank owns [lo, hi) of total units."""
+    lo, hi = C.c_int64(), C.c_int64()
+    lib().rsm_shard_range(total, world, rank, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
 
 
 def dmma_peak_tflops(device: int = 0) -> float:
