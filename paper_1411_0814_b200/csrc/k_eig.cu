@@ -114,18 +114,34 @@ __device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double*
   __syncthreads();
 }
 
-// grid reduction of cnt values from part[buf] into sh.red; op 0 = sum, 1 = max
+// partial of value e of this CTA for reduction buffer buf; layout [buf][e][cta]
+// so one warp reads the grid's partials of a value with coalesced loads
+__device__ __forceinline__ double* pslot(const EigArgs& a, int buf, int pw, int e) {
+  return a.part + ((size_t)buf * pw + e) * gridDim.x + blockIdx.x;
+}
+
+// grid reduction of cnt values from part[buf] into sh.red; op 0 = sum, 1 = max.
+// One warp per value: lanes sum a strided subset of the CTAs' partials, then a
+// butterfly; the order is fixed, so every CTA gets bitwise identical results.
 __device__ void grid_reduce(const EigArgs& a, cg::grid_group& grid, int buf, int cnt, int op,
                             int pw, EigShared& sh) {
   grid.sync();
-  const double* base = a.part + (size_t)buf * gridDim.x * pw;
-  for (int e = threadIdx.x; e < cnt; e += ET) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nc = (int)gridDim.x;
+  for (int e = warp; e < cnt; e += ET / 32) {
+    const double* base = a.part + ((size_t)buf * pw + e) * nc;
     double s = op ? -1.0 : 0.0;
-    for (unsigned c = 0; c < gridDim.x; ++c) {
-      const double v = base[(size_t)c * pw + e];
+#pragma unroll 4
+    for (int c = lane; c < nc; c += 32) {
+      const double v = base[c];
       s = op ? fmax(s, v) : s + v;
     }
-    sh.red[e] = s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t = __shfl_xor_sync(0xffffffffu, s, o);
+      s = op ? fmax(s, t) : s + t;
+    }
+    if (lane == 0) sh.red[e] = s;
   }
   __syncthreads();
 }
@@ -134,7 +150,6 @@ __device__ void grid_reduce(const EigArgs& a, cg::grid_group& grid, int buf, int
 // optional squared norm of column pc (pc < 0: none) at index nc*(nc+1)/2
 __device__ void gram_partial(const EigArgs& a, const double* X, int nc, int ld, int pc,
                              int row_lo, int row_hi, int buf, int pw) {
-  double* out = a.part + ((size_t)buf * gridDim.x + blockIdx.x) * pw;
   const int P = nc * (nc + 1) / 2;
   for (int p = threadIdx.x; p < P + 1; p += ET) {
     int i = 0, j = 0;
@@ -148,7 +163,7 @@ __device__ void gram_partial(const EigArgs& a, const double* X, int nc, int ld, 
     }
     double s = 0.0;
     for (int row = row_lo; row < row_hi; ++row) s += X[(int64_t)row * ld + i] * X[(int64_t)row * ld + j];
-    out[p] = s;
+    *pslot(a, buf, pw, p) = s;
   }
 }
 
@@ -270,7 +285,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     if (tid == 0) {
       double m2 = 0.0;
       for (int w = 0; w < ET / 32; ++w) m2 = fmax(m2, sh.red[w]);
-      a.part[((size_t)buf * gridDim.x + blockIdx.x) * pw] = m2;
+      *pslot(a, buf, pw, 0) = m2;
     }
     grid_reduce(a, grid, buf, 1, 1, pw, sh);
     buf ^= 1;
@@ -298,6 +313,20 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   double acut = 0.5 * ub;
   double maxres = 0.0, lmax = 0.0;
   int outer = 0, status = 1;
+  // phase clocks (CTA 0, thread 0): [0] filter, [1] CholQR2, [2] RR matvec+reduce,
+  // [3] small eigensolve, [4] rotate+residual, [5] setup before the loop
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+  const bool tme = blockIdx.x == 0 && tid == 0;
+#define EIG_T(i)                          \
+  do {                                    \
+    if (tme) {                            \
+      const long long t_ = clock64();     \
+      tacc[i] += t_ - tlast;              \
+      tlast = t_;                         \
+    }                                     \
+  } while (0)
+  EIG_T(5);
   for (; outer < a.max_outer; ++outer) {
     if (!full) {
       // ---- Chebyshev filter of degree d on [acut, ub], normalised at 0 ----
@@ -333,15 +362,16 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       // filtered block is in Y
       { double* t = X; X = Y; Y = t; }
       __syncthreads();
+      EIG_T(0);
       cholqr(a, grid, X, b, ld, pcol, row_lo, row_hi, buf, pw, sh);
       cholqr(a, grid, X, b, ld, -1, row_lo, row_hi, buf, pw, sh);
+      EIG_T(1);
     }
     // ---- Rayleigh-Ritz ----
     grid.sync();  // X complete
     matvec(a, X, Z, ld, ld, row_lo, row_hi, xs_dyn, kc_rows);
     ++matvecs;
     {
-      double* out = a.part + ((size_t)buf * gridDim.x + blockIdx.x) * pw;
       const int P = b * (b + 1) / 2;
       for (int p = tid; p < P + 2; p += ET) {
         double s = 0.0;
@@ -358,7 +388,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
           for (int row = row_lo; row < row_hi; ++row)
             s += X[(int64_t)row * ld + pcol] * X[(int64_t)row * ld + pcol];
         }
-        out[p] = s;
+        *pslot(a, buf, pw, p) = s;
       }
       grid_reduce(a, grid, buf, P + 2, 0, pw, sh);
       buf ^= 1;
@@ -371,8 +401,9 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
         sh.H[(e2 / b) * BMAX + (e2 % b)] = sh.red[p];
       }
       __syncthreads();
+      EIG_T(2);
       if (tid < 32) {
-        warp_jacobi_eig(sh.H, BMAX, sh.S, BMAX, b, sh.cs, sh.pairs, 2.220446049250313e-16, 60, true);
+        warp_jacobi_eig_abs(sh.H, BMAX, sh.S, BMAX, b, sh.cs, sh.pairs, 60);
         if (tid == 0) {
           // ascending order: selection sort of eigenpairs
           for (int i = 0; i < b; ++i) sh.theta[i] = sh.H[i * BMAX + i];
@@ -391,6 +422,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       }
       __syncthreads();
     }
+    EIG_T(3);
     // X <- X S, Z <- Z S (own rows); residual partials
     {
       for (int row = row_lo + tid; row < row_hi; row += ET) {
@@ -417,18 +449,18 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
         }
       }
       __syncthreads();
-      double* out = a.part + ((size_t)buf * gridDim.x + blockIdx.x) * pw;
       for (int j = tid; j < b; j += ET) {
         double s = 0.0;
         for (int row = row_lo; row < row_hi; ++row) {
           const double d = Z[(int64_t)row * ld + j] - sh.theta[j] * X[(int64_t)row * ld + j];
           s += d * d;
         }
-        out[j] = s;
+        *pslot(a, buf, pw, j) = s;
       }
       grid_reduce(a, grid, buf, b, 0, pw, sh);
       buf ^= 1;
     }
+    EIG_T(4);
     // the r wanted pairs must converge; the (r+1)-th Ritz value only has to be
     // resolved against the rank-gate thresholds: either converged too, or
     // clearly above 10 tol lambda_max (eigenvalues that small are amplified by
@@ -466,7 +498,9 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     a.dstat[0] = full ? sh.theta[b - 1] : lmax;
     a.dstat[1] = ub;
     a.dstat[2] = maxres;
+    for (int i = 0; i < 6; ++i) a.dstat[3 + i] = (double)tacc[i];
   }
+#undef EIG_T
 }
 
 // sign fix (solver.cpp:47-60): the largest-magnitude entry of each column is

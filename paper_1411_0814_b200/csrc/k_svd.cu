@@ -335,16 +335,31 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     }
     const int L = run;
     __syncwarp();
-    // gather S (K x L): lane = column within each 32-column word
-    for (int64_t j0 = 0; j0 < a.n; j0 += 32) {
-      const int64_t j = j0 + lane;
-      const uint32_t word = cm[j0 >> 5];
-      const uint32_t bit = 1u << lane;
-      if (j < a.n && (word & bit)) {
-        const int c = (int)pre[j0 >> 5] + __popc(word & (bit - 1u));
+    // gather S (K x L): lane = column within each 32-column word. The K rows
+    // are read whole and unconditionally, UW words at a time, so K*UW loads
+    // per lane are in flight (hidden cells are loaded but never used)
+    constexpr int UW = 4;
+    for (int64_t j0 = 0; j0 < a.n; j0 += 32 * UW) {
+      double yv[UW][K];
 #pragma unroll
-        for (int i = 0; i < K; ++i) S[i * Lp + c] = __ldg(a.Y + (int64_t)rows[i] * a.n + j);
-        atomicAdd(a.colcnt + j, 1);
+      for (int u = 0; u < UW; ++u) {
+        const int64_t j = j0 + 32 * u + lane;
+#pragma unroll
+        for (int i = 0; i < K; ++i) yv[u][i] = j < a.n ? __ldg(a.Y + (int64_t)rows[i] * a.n + j) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UW; ++u) {
+        const int64_t j = j0 + 32 * u + lane;
+        if (j0 + 32 * u < a.n) {
+          const uint32_t word = cm[(j0 >> 5) + u];
+          const uint32_t bit = 1u << lane;
+          if (j < a.n && (word & bit)) {
+            const int c = (int)pre[(j0 >> 5) + u] + __popc(word & (bit - 1u));
+#pragma unroll
+            for (int i = 0; i < K; ++i) S[i * Lp + c] = yv[u][i];
+            atomicAdd(a.colcnt + j, 1);
+          }
+        }
       }
     }
     __syncwarp();

@@ -138,7 +138,7 @@ struct rsm_ctx {
 
   cudaEvent_t ev[8] = {};
   double stage_ms[8] = {};
-  double solver_stats[8] = {};  // eig: outer its, matvecs, lambda_max, ub, max residual, block, grid
+  double solver_stats[16] = {};  // eig: outer its, matvecs, lambda_max, ub, max residual, block, grid
   int64_t launches = 0;
 
   void set_err(const std::string& s) { err = s; }
@@ -487,7 +487,7 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   c->ePart.ensure(sizeof(double) * 2 * (size_t)grid * pw);
   c->eW.ensure(sizeof(double) * 32);
   c->eI.ensure(sizeof(int) * 8);
-  c->eD.ensure(sizeof(double) * 8);
+  c->eD.ensure(sizeof(double) * 16);
   c->Vhat.ensure(sizeof(double) * n * r);
   rsmk::EigArgs a{};
   a.G = c->G.as<double>();
@@ -506,10 +506,10 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   c->launches += 2;
   double w[32];
   int istat[8];
-  double dstat[8];
+  double dstat[16];
   ck(cudaMemcpyAsync(w, c->eW.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaMemcpyAsync(istat, c->eI.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
-  ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 9, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "solve_v");
   ck(cudaGetLastError(), "eig kernels");
   c->solver_stats[0] = istat[3];
@@ -519,6 +519,7 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   c->solver_stats[4] = dstat[2];
   c->solver_stats[5] = b;
   c->solver_stats[6] = grid;
+  for (int i = 0; i < 6; ++i) c->solver_stats[7 + i] = dstat[3 + i];  // phase clocks (cycles)
   if (istat[0] != 0) fail(RSM_ERR_INTERNAL, "symmetric eigensolver failed to converge");
   c->Vhat_n = n;
   c->Vhat_r = r;
@@ -918,7 +919,7 @@ int rsm_ctx_stage_ms(rsm_ctx* c, double* ms, int cap) {
 int64_t rsm_ctx_launch_count(rsm_ctx* c) { return c ? c->launches : 0; }
 
 int rsm_ctx_solver_stats(rsm_ctx* c, double* out, int cap) {
-  const int k = std::min(cap, 7);
+  const int k = std::min(cap, 13);
   for (int i = 0; i < k; ++i) out[i] = c->solver_stats[i];
   return k;
 }

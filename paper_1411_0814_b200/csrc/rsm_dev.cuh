@@ -66,8 +66,13 @@ __device__ __forceinline__ int warp_sum_int(int v) {
 __device__ inline int warp_jacobi_eig(double* A, int lda, double* V, int ldv, int K,
                                       double* cs /* smem scratch >= 2*32 doubles */,
                                       int* pairs /* smem scratch >= 2*32 ints */, double tol,
-                                      int max_sweeps, bool init_v) {
+                                      int max_sweeps, bool init_v, double abs_thr = 0.0) {
   const int lane = threadIdx.x & 31;
+  // abs_thr > 0: absolute test |a_pq| <= abs_thr (eigenvalues to abs_thr, as
+  // dsyev delivers them); otherwise the relative test against sqrt(|a_pp a_qq|)
+  auto big_off = [&](double apq, double app, double aqq) {
+    return abs_thr > 0.0 ? fabs(apq) > abs_thr : (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq)));
+  };
   if (init_v)
     for (int e = lane; e < K * K; e += 32) V[(e / K) * ldv + (e % K)] = (e / K == e % K) ? 1.0 : 0.0;
   __syncwarp();
@@ -82,7 +87,7 @@ __device__ inline int warp_jacobi_eig(double* A, int lda, double* V, int ldv, in
       const int p = e / K, q = e % K;
       if (p < q) {
         const double apq = A[p * lda + q];
-        if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(A[p * lda + p] * A[q * lda + q]))) big = 1;
+        if (big_off(apq, A[p * lda + p], A[q * lda + q])) big = 1;
       }
     }
     if (!__any_sync(0xffffffffu, big)) break;
@@ -96,7 +101,7 @@ __device__ inline int warp_jacobi_eig(double* A, int lda, double* V, int ldv, in
         if (q < K) {
           const double apq = A[p * lda + q];
           const double app = A[p * lda + p], aqq = A[q * lda + q];
-          if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
+          if (big_off(apq, app, aqq)) {
             const double zeta = (aqq - app) / (2.0 * apq);
             const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -148,6 +153,22 @@ __device__ inline int warp_jacobi_eig(double* A, int lda, double* V, int ldv, in
     }
   }
   return sweep;
+}
+
+// Jacobi with the absolute off-diagonal threshold eps * ||A||_F (LAPACK-level
+// eigenvalue accuracy); used where small eigenvalues only need absolute
+// accuracy (the stage-4 Rayleigh-Ritz problem). V is initialised to I.
+__device__ inline int warp_jacobi_eig_abs(double* A, int lda, double* V, int ldv, int K, double* cs,
+                                          int* pairs, int max_sweeps) {
+  const int lane = threadIdx.x & 31;
+  double f = 0.0;
+  for (int e = lane; e < K * K; e += 32) {
+    const double v = A[(e / K) * lda + (e % K)];
+    f += v * v;
+  }
+  f = warp_sum(f);
+  const double thr = 2.220446049250313e-16 * sqrt(f);
+  return warp_jacobi_eig(A, lda, V, ldv, K, cs, pairs, 0.0, max_sweeps, true, thr > 0.0 ? thr : 1e-300);
 }
 
 }  // namespace rsmd

@@ -374,10 +374,11 @@ class Context:
         return int(lib().rsm_ctx_launch_count(self.h))
 
     def solver_stats(self) -> dict:
-        buf = (C.c_double * 8)()
-        lib().rsm_ctx_solver_stats(self.h, C.cast(buf, C.c_void_p), 8)
-        keys = ["outer", "matvecs", "lambda_max", "ub", "max_residual", "block", "grid"]
-        return dict(zip(keys, buf[:7]))
+        buf = (C.c_double * 16)()
+        k = lib().rsm_ctx_solver_stats(self.h, C.cast(buf, C.c_void_p), 16)
+        keys = ["outer", "matvecs", "lambda_max", "ub", "max_residual", "block", "grid", "cyc_filter",
+                "cyc_cholqr", "cyc_rr", "cyc_eig", "cyc_rotate", "cyc_setup"]
+        return dict(zip(keys, buf[:k]))
 
 
 # ------------------------------------------------------- reference-shaped API
