@@ -24,6 +24,8 @@
 // the slices in a fixed order, so G is bitwise reproducible. Only tiles
 // touching the upper triangle are computed; stage 3b mirrors them (the
 // reference G is exactly symmetric).
+#include <cstdlib>
+
 #include "rsm_internal.h"
 #include "rsm_dev.cuh"
 
@@ -31,44 +33,75 @@ namespace rsmk {
 
 namespace {
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// 1-D bulk copy global -> shared through the TMA engine, completing on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
-template <int R, int CPL>
+template <int R, int CPL, int NW>
 struct GramCfg {
   static constexpr int RP = (R + 1) & ~1;  // padded row stride (doubles)
   static constexpr int TR = 64;
   static constexpr int TC = 32 * CPL;
-  static constexpr int CH = (R <= 4) ? 4 : 2;  // trials per pipeline group
-  static constexpr int NS = 3;                 // pipeline depth (groups)
-  static constexpr int MB = 64;                // metadata batch (trials)
+  static constexpr int RPW = TR / NW;          // rows per consumer warp
+  static constexpr int CH = (R <= 4) ? 4 : 2;  // trials per ring stage
+  static constexpr int NS = 4;                 // ring depth (stages)
   static constexpr int SLOT = (TR + TC) * RP;  // doubles per trial slot
 };
 
+// per-trial record the producer writes next to the trial's V segments
 struct TrialMeta {
-  long long srcI, srcJ;  // segment starts in V (doubles)
-  unsigned wI[2];
-  unsigned wJ[4];
-  int preI[2];  // support bits before each row-block word
-  int preJ[4];  // support bits before each column-block word
+  unsigned wI[2];  // support words of the tile's 64 rows
+  unsigned wJ[4];  // support words of the tile's columns
+  int preI1;       // popc(wI[0])
+  int preJ[4];     // support bits before each column word
+  int pad;
 };
 
 }  // namespace
 
-template <int R, int CPL>
-__global__ void __launch_bounds__(256, 2) k_gram(GramArgs a) {
-  using C = GramCfg<R, CPL>;
-  constexpr int RP = C::RP, TR = C::TR, TC = C::TC, CH = C::CH, NS = C::NS, MB = C::MB, SLOT = C::SLOT;
+// NW warps own RPW x TC register blocks of the 64 x TC tile. Warp 0 also
+// feeds the ring: per stage it writes CH trials' TrialMeta records and issues
+// two 1-D bulk copies per trial (the support rows of the tile's row block and
+// of its column block, contiguous in V) completing on the stage's full
+// barrier; every warp releases a stage through its empty barrier, and warp 0
+// refills it with the group NS ahead. The next group's metadata is loaded
+// into registers one group early. Row activity is made warp-uniform with a
+// redux so the compiler branches on the uniform datapath.
+template <int R, int CPL, int NW>
+__global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
+  using C = GramCfg<R, CPL, NW>;
+  constexpr int RP = C::RP, TR = C::TR, TC = C::TC, RPW = C::RPW, CH = C::CH, NS = C::NS, SLOT = C::SLOT;
   extern __shared__ __align__(16) double sm[];
-  double* ring = sm;                                              // [NS][CH][SLOT]
-  TrialMeta* meta = reinterpret_cast<TrialMeta*>(ring + NS * CH * SLOT);  // [2][MB]
+  double* ring = sm;                                                     // [NS][CH][SLOT]
+  TrialMeta* meta = reinterpret_cast<TrialMeta*>(ring + NS * CH * SLOT);  // [NS][CH]
+  int* stage_nt = reinterpret_cast<int*>(meta + NS * CH);                // [NS]
+  double* zeros = reinterpret_cast<double*>(stage_nt + 4 * ((NS + 3) / 4));  // [RP] (16-B aligned)
+  uint64_t* full = reinterpret_cast<uint64_t*>(zeros + RP);              // [NS]
+  uint64_t* empty = full + NS;                                           // [NS]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int2 tile = a.tiles[blockIdx.x];
@@ -81,120 +114,123 @@ __global__ void __launch_bounds__(256, 2) k_gram(GramArgs a) {
   const int64_t ntr = te > tb ? te - tb : 0;
   const int64_t ngroups = (ntr + CH - 1) / CH;
 
-  // ---- metadata of one batch: thread u < MB loads trial tb + b*MB + u ----
-  long long m_off = 0;
-  unsigned m_pI = 0, m_pJ = 0, m_w[2 + CPL];
-  auto meta_load = [&](int64_t b) {
-    const int64_t t = tb + b * MB + tid;
-    if (tid < MB && b * MB + tid < ntr) {
-      m_off = __ldg(a.t_off + t);
-      m_pI = __ldg(a.t_pre + t * a.cmw + wrow);
-      m_pJ = __ldg(a.t_pre + t * a.cmw + wcol);
-      m_w[0] = __ldg(a.t_cm + t * a.cmw + wrow);
-      m_w[1] = __ldg(a.t_cm + t * a.cmw + wrow + 1);
+  if (tid < RP) zeros[tid] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 32);
+      mbar_init(empty + s, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // ---- producer state (warp 0; lane u < CH owns trial g*CH + u) ----
+  long long n_off = 0;
+  unsigned n_pI = 0, n_pJ = 0, n_w[2 + CPL];
+  auto load = [&](int64_t g) {
+    const int64_t i = g * CH + lane;
+    if (lane < CH && g < ngroups && i < ntr) {
+      const int64_t t = tb + i;
+      n_off = __ldg(a.t_off + t);
+      n_pI = __ldg(a.t_pre + t * a.cmw + wrow);
+      n_pJ = __ldg(a.t_pre + t * a.cmw + wcol);
+      n_w[0] = __ldg(a.t_cm + t * a.cmw + wrow);
+      n_w[1] = __ldg(a.t_cm + t * a.cmw + wrow + 1);
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) m_w[2 + s] = __ldg(a.t_cm + t * a.cmw + wcol + s);
+      for (int s = 0; s < CPL; ++s) n_w[2 + s] = __ldg(a.t_cm + t * a.cmw + wcol + s);
     }
   };
-  auto meta_store = [&](int64_t b) {
-    if (tid < MB && b * MB + tid < ntr) {
-      TrialMeta& m = meta[(b & 1) * MB + tid];
-      m.srcI = m_off + (long long)m_pI * RP;
-      m.srcJ = m_off + (long long)m_pJ * RP;
-      m.wI[0] = m_w[0];
-      m.wI[1] = m_w[1];
-      m.preI[0] = 0;
-      m.preI[1] = __popc(m_w[0]);
+  // publish the prefetched metadata of group g into its stage, issue its
+  // copies, then prefetch group g + 1
+  auto produce = [&](int64_t g) {
+    const int st = (int)(g % NS);
+    const int64_t i = g * CH + lane;
+    const bool live = lane < CH && i < ntr;
+    unsigned bI = 0, bJ = 0;
+    if (live) {
+      TrialMeta& m = meta[st * CH + lane];
+      m.wI[0] = n_w[0];
+      m.wI[1] = n_w[1];
+      m.preI1 = __popc(n_w[0]);
       int run = 0;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        const unsigned w = s < CPL ? m_w[2 + s] : 0u;
-        m.wJ[s] = w;
+        const unsigned x = s < CPL ? n_w[2 + s] : 0u;
+        m.wJ[s] = x;
         m.preJ[s] = run;
-        run += __popc(w);
+        run += __popc(x);
       }
+      bI = (unsigned)((__popc(n_w[0]) + __popc(n_w[1])) * RP * 8);
+      bJ = (unsigned)(run * RP * 8);
     }
-  };
-  // Issue the copies of group g into ring stage g % NS: per trial the two
-  // compact segments (support rows of the tile's row block, support columns
-  // of its column block), contiguous in V, as 16-byte cp.async chunks.
-  auto issue = [&](int64_t g) {
-    if (g < ngroups) {
-      double* st = ring + (g % NS) * CH * SLOT;
-      const int64_t i0 = g * CH;
-      const int nt = (int)((ntr - i0) < CH ? (ntr - i0) : CH);
-#pragma unroll 1
-      for (int u = 0; u < nt; ++u) {
-        const int64_t i = i0 + u;
-        const TrialMeta& m = meta[((i / MB) & 1) * MB + (i % MB)];
-        double* slot = st + u * SLOT;
-        const int cI = (m.preI[1] + __popc(m.wI[1])) * (RP / 2);
-        const int cJ = (m.preJ[3] + __popc(m.wJ[3])) * (RP / 2);
-        for (int c = tid; c < cI + cJ; c += 256) {
-          if (c < cI) cp_async16(slot + 2 * c, a.V + m.srcI + 2 * c);
-          else cp_async16(slot + TR * RP + 2 * (c - cI), a.V + m.srcJ + 2 * (c - cI));
-        }
-      }
-    }
-    cp_async_commit();  // (possibly empty) group keeps the wait count uniform
-  };
-
-  double acc[8][CPL];
+    unsigned bytes = bI + bJ;
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    if (lane == 0) {
+      const int64_t rem = ntr - g * CH;
+      stage_nt[st] = (int)(rem < CH ? rem : CH);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(full + st, bytes);
+    else mbar_arrive(full + st);
+    if (live) {
+      double* slot = ring + (st * CH + lane) * SLOT;
+      if (bI) bulk_g2s(slot, a.V + n_off + (long long)n_pI * RP, bI, full + st);
+      if (bJ) bulk_g2s(slot + TR * RP, a.V + n_off + (long long)n_pJ * RP, bJ, full + st);
+    }
+    load(g + 1);
+  };
+  if (warp == 0) {
+    load(0);
+    for (int64_t g = 0; g < NS && g < ngroups; ++g) produce(g);
+  }
+
+  // ---------------- consumers ----------------
+  double acc[RPW][CPL];
+#pragma unroll
+  for (int i = 0; i < RPW; ++i)
 #pragma unroll
     for (int s = 0; s < CPL; ++s) acc[i][s] = 0.0;
 
-  if (ngroups > 0) {
-    meta_load(0);
-    meta_store(0);
-    meta_load(1);  // batch 1 in registers, published after the first group
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < NS - 1; ++g) issue(g);
-  }
-  const int shI = (warp & 3) * 8;
+  const int wword = (warp * RPW) >> 5;        // row word of this warp's rows
+  const int shI = (warp * RPW) & 31;          // bit offset inside it
+  constexpr unsigned RMASK = RPW >= 32 ? 0xffffffffu : ((1u << RPW) - 1u);
+  const unsigned lanelt = (1u << lane) - 1u;
   for (int64_t g = 0; g < ngroups; ++g) {
-    // publish the next metadata batch early enough for the copies that need it
-    // (batch b+1 is published one group after batch b starts, long before
-    // issue() reaches it; buffer (b+1)&1 last served batch b-1, which is done)
-    if (g >= 1 && ((g - 1) * CH) % MB == 0) {
-      const int64_t b = ((g - 1) * CH) / MB;
-      meta_store(b + 1);
-      meta_load(b + 2);
+    const int st = (int)(g % NS);
+    if (warp == 0 && g >= 1 && g + NS - 1 < ngroups) {
+      // refill the stage group g-1 used once every warp has released it
+      mbar_wait(empty + (int)((g - 1) % NS), (unsigned)(((g - 1) / NS) & 1));
+      produce(g + NS - 1);
     }
-    __syncthreads();  // meta visible; previous compute done with the stage we refill
-    issue(g + NS - 1);
-    cp_async_wait<NS - 1>();
-    __syncthreads();  // group g landed for every thread
-    const double* st = ring + (g % NS) * CH * SLOT;
+    mbar_wait(full + st, (unsigned)((g / NS) & 1));
+    const int nt = stage_nt[st];
 #pragma unroll 1
-    for (int u = 0; u < CH; ++u) {
-      const int64_t i = g * CH + u;
-      if (i >= ntr) break;
-      const TrialMeta& m = meta[((i / MB) & 1) * MB + (i % MB)];
-      const unsigned wI0 = m.wI[0], wI1 = m.wI[1];
-      const unsigned rb = ((warp < 4 ? wI0 : wI1) >> shI) & 0xffu;
-      if (rb == 0) continue;  // warp-uniform
-      const double* VI = st + u * SLOT;
+    for (int u = 0; u < nt; ++u) {
+      const TrialMeta& m = meta[st * CH + u];
+      const unsigned wIw = wword ? m.wI[1] : m.wI[0];
+      const unsigned rb = __reduce_or_sync(0xffffffffu, (wIw >> shI) & RMASK);
+      if (rb == 0) continue;
+      const double* VI = ring + (st * CH + u) * SLOT;
       const double* VJ = VI + TR * RP;
-      // this lane's columns: compact index = support bits below it (zeros outside)
+      // this lane's columns: compact index = support bits below it; columns
+      // outside the support read the zero row
       double vj[CPL][RP];
 #pragma unroll
       for (int s = 0; s < CPL; ++s) {
         const unsigned w = m.wJ[s];
-        const bool sel = (w >> lane) & 1u;
-        const int cj = m.preJ[s] + __popc(w & ((1u << lane) - 1u));
+        const double* src = ((w >> lane) & 1u) ? VJ + (m.preJ[s] + __popc(w & lanelt)) * RP : zeros;
 #pragma unroll
         for (int h = 0; h < RP / 2; ++h) {
-          const double2 t = sel ? reinterpret_cast<const double2*>(VJ + cj * RP)[h] : make_double2(0.0, 0.0);
+          const double2 t = reinterpret_cast<const double2*>(src)[h];
           vj[s][2 * h] = t.x;
           vj[s][2 * h + 1] = t.y;
         }
       }
-      int ci = (warp < 4) ? __popc(wI0 & ((1u << shI) - 1u)) : m.preI[1] + __popc(wI1 & ((1u << shI) - 1u));
+      int ci = (wword ? m.preI1 : 0) + __popc(wIw & ((1u << shI) - 1u));
+      ci = __shfl_sync(0xffffffffu, ci, 0);
 #pragma unroll
-      for (int r8 = 0; r8 < 8; ++r8) {
+      for (int r8 = 0; r8 < RPW; ++r8) {
         if (rb & (1u << r8)) {  // warp-uniform
           double x[RP];
 #pragma unroll
@@ -211,13 +247,14 @@ __global__ void __launch_bounds__(256, 2) k_gram(GramArgs a) {
         }
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
   }
-  cp_async_wait<0>();
   // ---- write the slice partial ----
   double* out = a.P + (int64_t)slice * a.npad * a.npad;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t row = row0 + warp * 8 + i;
+  for (int i = 0; i < RPW; ++i) {
+    const int64_t row = row0 + warp * RPW + i;
 #pragma unroll
     for (int s = 0; s < CPL; ++s) out[row * a.npad + col0 + lane + 32 * s] = acc[i][s];
   }
@@ -248,42 +285,57 @@ __global__ void k_gram_reduce(const double* __restrict__ P, int nslices, int64_t
   }
 }
 
-template <int R, int CPL>
+template <int R, int CPL, int NW>
 static size_t gram_smem() {
-  using C = GramCfg<R, CPL>;
-  return sizeof(double) * (size_t)C::NS * C::CH * C::SLOT + sizeof(TrialMeta) * 2 * C::MB;
+  using C = GramCfg<R, CPL, NW>;
+  return sizeof(double) * (size_t)C::NS * C::CH * C::SLOT + sizeof(TrialMeta) * C::NS * C::CH +
+         sizeof(int) * 4 * ((C::NS + 3) / 4) + sizeof(double) * C::RP + sizeof(uint64_t) * 2 * C::NS;
 }
 
-template <int R, int CPL>
+template <int R, int CPL, int NW>
 static void launch_gram_t(const GramArgs& a, int ntiles, cudaStream_t s) {
-  const size_t smem = gram_smem<R, CPL>();
-  cudaFuncSetAttribute(k_gram<R, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = gram_smem<R, CPL, NW>();
+  cudaFuncSetAttribute(k_gram<R, CPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)ntiles, (unsigned)a.nslices);
-  k_gram<R, CPL><<<grid, 256, smem, s>>>(a);
+  k_gram<R, CPL, NW><<<grid, 32 * NW, smem, s>>>(a);
 }
 
 int gram_cols_per_lane(int R) { return R <= 4 ? 4 : (R <= 8 ? 2 : 1); }
 
 int gram_ctas_per_sm(int) { return 2; }
 
+static int gram_warps() {
+  static int nw = [] {
+    const char* e = getenv("RSM_GRAM_WARPS");
+    return (e && atoi(e) == 4) ? 4 : 8;
+  }();
+  return nw;
+}
+
+template <int R, int CPL>
+static void launch_gram_r(const GramArgs& a, int ntiles, cudaStream_t s) {
+  if (gram_warps() == 4) launch_gram_t<R, CPL, 4>(a, ntiles, s);
+  else launch_gram_t<R, CPL, 8>(a, ntiles, s);
+}
+
 void launch_gram(const GramArgs& a, int ntiles, cudaStream_t s) {
   switch (a.R) {
-    case 1: launch_gram_t<1, 4>(a, ntiles, s); break;
-    case 2: launch_gram_t<2, 4>(a, ntiles, s); break;
-    case 3: launch_gram_t<3, 4>(a, ntiles, s); break;
-    case 4: launch_gram_t<4, 4>(a, ntiles, s); break;
-    case 5: launch_gram_t<5, 2>(a, ntiles, s); break;
-    case 6: launch_gram_t<6, 2>(a, ntiles, s); break;
-    case 7: launch_gram_t<7, 2>(a, ntiles, s); break;
-    case 8: launch_gram_t<8, 2>(a, ntiles, s); break;
-    case 9: launch_gram_t<9, 1>(a, ntiles, s); break;
-    case 10: launch_gram_t<10, 1>(a, ntiles, s); break;
-    case 11: launch_gram_t<11, 1>(a, ntiles, s); break;
-    case 12: launch_gram_t<12, 1>(a, ntiles, s); break;
-    case 13: launch_gram_t<13, 1>(a, ntiles, s); break;
-    case 14: launch_gram_t<14, 1>(a, ntiles, s); break;
-    case 15: launch_gram_t<15, 1>(a, ntiles, s); break;
-    default: launch_gram_t<16, 1>(a, ntiles, s); break;
+    case 1: launch_gram_r<1, 4>(a, ntiles, s); break;
+    case 2: launch_gram_r<2, 4>(a, ntiles, s); break;
+    case 3: launch_gram_r<3, 4>(a, ntiles, s); break;
+    case 4: launch_gram_r<4, 4>(a, ntiles, s); break;
+    case 5: launch_gram_r<5, 2>(a, ntiles, s); break;
+    case 6: launch_gram_r<6, 2>(a, ntiles, s); break;
+    case 7: launch_gram_r<7, 2>(a, ntiles, s); break;
+    case 8: launch_gram_r<8, 2>(a, ntiles, s); break;
+    case 9: launch_gram_r<9, 1>(a, ntiles, s); break;
+    case 10: launch_gram_r<10, 1>(a, ntiles, s); break;
+    case 11: launch_gram_r<11, 1>(a, ntiles, s); break;
+    case 12: launch_gram_r<12, 1>(a, ntiles, s); break;
+    case 13: launch_gram_r<13, 1>(a, ntiles, s); break;
+    case 14: launch_gram_r<14, 1>(a, ntiles, s); break;
+    case 15: launch_gram_r<15, 1>(a, ntiles, s); break;
+    default: launch_gram_r<16, 1>(a, ntiles, s); break;
   }
 }
 
