@@ -8,17 +8,15 @@
 // with count[c] = number of trials whose support holds column c.
 //
 // This kernel forms the second term with register-resident output tiles: a
-// CTA owns a 64 x (32*CPL) tile of G (8 warps x 8 rows, lane = column) and a
-// slice of the trial list. For every trial the compact V rows that fall into
-// the tile's row block and column block are two contiguous segments of the
-// trial's V array (k_svd writes the rows in support order with an even
-// stride RP), so they are streamed into shared memory with 16-byte
-// cp.async copies through an NS-stage ring of CH-trial groups: the copies of
-// group g+NS-1 are in flight while group g is computed. The per-trial
-// metadata (segment offsets, support words) is loaded one 64-trial batch
-// ahead into registers and published to shared memory. Each warp applies
-// the rank-R update to its 8 x 32*CPL register block, skipping rows outside
-// the support (warp-uniform) and reading zeros for columns outside it.
+// CTA owns a 64 x (32*CPL) tile of G (NW warps x RPW rows, lane = column)
+// and a slice of the trial list. Stage 2 stores each trial's top vectors
+// expanded (rp/2 planes of npad (v_2p, v_2p+1) pairs, zero outside the
+// support), so the tile's row block and column block of a plane are two
+// contiguous 16-byte-aligned runs: they are streamed into shared memory with
+// 1-D bulk copies (TMA) through an NS-stage ring of CH-trial groups guarded
+// by mbarriers. Each warp applies the rank-R update to its RPW x 32*CPL
+// register block, skipping rows outside the support (warp-uniform, on the
+// uniform datapath) and reading its columns' pairs conflict-free.
 //
 // No atomics: each tile x slice partial is written once and stage 3b sums
 // the slices in a fixed order, so G is bitwise reproducible. Only tiles
@@ -63,44 +61,38 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 template <int R, int CPL, int NW>
 struct GramCfg {
-  static constexpr int RP = (R + 1) & ~1;  // padded row stride (doubles)
+  static constexpr int RP = (R + 1) & ~1;  // planes * 2
+  static constexpr int NP = RP / 2;        // planes
   static constexpr int TR = 64;
   static constexpr int TC = 32 * CPL;
-  static constexpr int RPW = TR / NW;          // rows per consumer warp
+  static constexpr int RPW = TR / NW;          // rows per warp
   static constexpr int CH = (R <= 4) ? 4 : 2;  // trials per ring stage
   static constexpr int NS = 4;                 // ring depth (stages)
   static constexpr int SLOT = (TR + TC) * RP;  // doubles per trial slot
 };
 
-// per-trial record the producer writes next to the trial's V segments
-struct TrialMeta {
-  unsigned wI[2];  // support words of the tile's 64 rows
-  unsigned wJ[4];  // support words of the tile's columns
-  int preI1;       // popc(wI[0])
-  int preJ[4];     // support bits before each column word
-  int pad;
-};
-
 }  // namespace
 
-// NW warps own RPW x TC register blocks of the 64 x TC tile. Warp 0 also
-// feeds the ring: per stage it writes CH trials' TrialMeta records and issues
-// two 1-D bulk copies per trial (the support rows of the tile's row block and
-// of its column block, contiguous in V) completing on the stage's full
-// barrier; every warp releases a stage through its empty barrier, and warp 0
-// refills it with the group NS ahead. The next group's metadata is loaded
-// into registers one group early. Row activity is made warp-uniform with a
-// redux so the compiler branches on the uniform datapath.
+// NW warps own RPW x TC register blocks of the 64 x TC tile and take turns
+// feeding the ring (group h is produced by warp h % NW): lane u < CH of the
+// producer publishes trial g*CH+u's row-support words in the stage and
+// issues its 2*NP bulk copies (row block and column block of every plane),
+// completing on the stage's full barrier. Every warp releases a stage through
+// its empty barrier; the stage released `lag` groups ago is refilled with the
+// group NS ahead of it, so a producer rarely waits for the slowest warp. A
+// warp loads the support words of the next group it produces right after
+// producing one. Row activity is made warp-uniform with a redux so the
+// compiler branches on the uniform datapath.
 template <int R, int CPL, int NW>
 __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
   using C = GramCfg<R, CPL, NW>;
-  constexpr int RP = C::RP, TR = C::TR, TC = C::TC, RPW = C::RPW, CH = C::CH, NS = C::NS, SLOT = C::SLOT;
+  constexpr int RP = C::RP, NP = C::NP, TR = C::TR, TC = C::TC, RPW = C::RPW, CH = C::CH, NS = C::NS,
+                SLOT = C::SLOT;
   extern __shared__ __align__(16) double sm[];
   double* ring = sm;                                                     // [NS][CH][SLOT]
-  TrialMeta* meta = reinterpret_cast<TrialMeta*>(ring + NS * CH * SLOT);  // [NS][CH]
-  int* stage_nt = reinterpret_cast<int*>(meta + NS * CH);                // [NS]
-  double* zeros = reinterpret_cast<double*>(stage_nt + 4 * ((NS + 3) / 4));  // [RP] (16-B aligned)
-  uint64_t* full = reinterpret_cast<uint64_t*>(zeros + RP);              // [NS]
+  uint2* rowsup = reinterpret_cast<uint2*>(ring + NS * CH * SLOT);       // [NS][CH]
+  int* stage_nt = reinterpret_cast<int*>(rowsup + NS * CH);              // [NS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_nt + 2 * ((NS + 1) / 2));  // [NS]
   uint64_t* empty = full + NS;                                           // [NS]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -113,8 +105,8 @@ __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
   const int64_t te = (tb + per < a.T) ? tb + per : a.T;
   const int64_t ntr = te > tb ? te - tb : 0;
   const int64_t ngroups = (ntr + CH - 1) / CH;
+  const int64_t tstride = a.npad * RP;  // doubles per trial
 
-  if (tid < RP) zeros[tid] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(full + s, 32);
@@ -124,48 +116,26 @@ __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
   }
   __syncthreads();
 
-  // ---- producer state (warp 0; lane u < CH owns trial g*CH + u) ----
-  long long n_off = 0;
-  unsigned n_pI = 0, n_pJ = 0, n_w[2 + CPL];
+  // ---- producer state: lane u < CH owns trial g*CH + u of its groups ----
+  unsigned n_w0 = 0, n_w1 = 0, n_any = 0;
   auto load = [&](int64_t g) {
     const int64_t i = g * CH + lane;
+    n_w0 = n_w1 = n_any = 0;
     if (lane < CH && g < ngroups && i < ntr) {
-      const int64_t t = tb + i;
-      n_off = __ldg(a.t_off + t);
-      n_pI = __ldg(a.t_pre + t * a.cmw + wrow);
-      n_pJ = __ldg(a.t_pre + t * a.cmw + wcol);
-      n_w[0] = __ldg(a.t_cm + t * a.cmw + wrow);
-      n_w[1] = __ldg(a.t_cm + t * a.cmw + wrow + 1);
+      const uint32_t* cm = a.t_cm + (tb + i) * a.cmw;
+      n_w0 = __ldg(cm + wrow);
+      n_w1 = __ldg(cm + wrow + 1);
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) n_w[2 + s] = __ldg(a.t_cm + t * a.cmw + wcol + s);
+      for (int s = 0; s < CPL; ++s) n_any |= __ldg(cm + wcol + s);
     }
   };
-  // publish the prefetched metadata of group g into its stage, issue its
-  // copies, then prefetch group g + 1
   auto produce = [&](int64_t g) {
     const int st = (int)(g % NS);
     const int64_t i = g * CH + lane;
-    const bool live = lane < CH && i < ntr;
-    unsigned bI = 0, bJ = 0;
-    if (live) {
-      TrialMeta& m = meta[st * CH + lane];
-      m.wI[0] = n_w[0];
-      m.wI[1] = n_w[1];
-      m.preI1 = __popc(n_w[0]);
-      int run = 0;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const unsigned x = s < CPL ? n_w[2 + s] : 0u;
-        m.wJ[s] = x;
-        m.preJ[s] = run;
-        run += __popc(x);
-      }
-      bI = (unsigned)((__popc(n_w[0]) + __popc(n_w[1])) * RP * 8);
-      bJ = (unsigned)(run * RP * 8);
-    }
-    unsigned bytes = bI + bJ;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    // a trial with no support rows or no support columns in the tile adds nothing
+    const bool live = lane < CH && i < ntr && (n_w0 | n_w1) != 0 && n_any != 0;
+    if (lane < CH) rowsup[st * CH + lane] = live ? make_uint2(n_w0, n_w1) : make_uint2(0u, 0u);
+    const unsigned bytes = __popc(__ballot_sync(0xffffffffu, live)) * (unsigned)(SLOT * 8);
     if (lane == 0) {
       const int64_t rem = ntr - g * CH;
       stage_nt[st] = (int)(rem < CH ? rem : CH);
@@ -175,71 +145,65 @@ __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
     else mbar_arrive(full + st);
     if (live) {
       double* slot = ring + (st * CH + lane) * SLOT;
-      if (bI) bulk_g2s(slot, a.V + n_off + (long long)n_pI * RP, bI, full + st);
-      if (bJ) bulk_g2s(slot + TR * RP, a.V + n_off + (long long)n_pJ * RP, bJ, full + st);
+      const double* src = a.V + (tb + i) * tstride;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        bulk_g2s(slot + p * TR * 2, src + p * a.npad * 2 + row0 * 2, TR * 16, full + st);
+        bulk_g2s(slot + TR * RP + p * TC * 2, src + p * a.npad * 2 + col0 * 2, TC * 16, full + st);
+      }
     }
-    load(g + 1);
+    load(g + NW);  // this warp's next group
   };
-  if (warp == 0) {
-    load(0);
-    for (int64_t g = 0; g < NS && g < ngroups; ++g) produce(g);
-  }
+  // group h is produced by warp h % NW; groups 0..NS-1 fill the empty ring
+  load(warp);
+  for (int h = warp; h < NS && h < ngroups; h += NW) produce(h);
 
-  // ---------------- consumers ----------------
   double acc[RPW][CPL];
 #pragma unroll
   for (int i = 0; i < RPW; ++i)
 #pragma unroll
     for (int s = 0; s < CPL; ++s) acc[i][s] = 0.0;
 
-  const int wword = (warp * RPW) >> 5;        // row word of this warp's rows
-  const int shI = (warp * RPW) & 31;          // bit offset inside it
+  const int wword = (warp * RPW) >> 5;  // row-support word of this warp's rows
+  const int shI = (warp * RPW) & 31;    // bit offset inside it
+  const int rfirst = warp * RPW;
   constexpr unsigned RMASK = RPW >= 32 ? 0xffffffffu : ((1u << RPW) - 1u);
-  const unsigned lanelt = (1u << lane) - 1u;
   for (int64_t g = 0; g < ngroups; ++g) {
     const int st = (int)(g % NS);
-    if (warp == 0 && g >= 1 && g + NS - 1 < ngroups) {
-      // refill the stage group g-1 used once every warp has released it
-      mbar_wait(empty + (int)((g - 1) % NS), (unsigned)(((g - 1) / NS) & 1));
-      produce(g + NS - 1);
+    if (g >= a.lag && g + NS - a.lag < ngroups && (int)((g + NS - a.lag) % NW) == warp) {
+      // refill the stage group g-lag used once every warp has released it
+      mbar_wait(empty + (int)((g - a.lag) % NS), (unsigned)(((g - a.lag) / NS) & 1));
+      produce(g + NS - a.lag);
     }
     mbar_wait(full + st, (unsigned)((g / NS) & 1));
     const int nt = stage_nt[st];
 #pragma unroll 1
     for (int u = 0; u < nt; ++u) {
-      const TrialMeta& m = meta[st * CH + u];
-      const unsigned wIw = wword ? m.wI[1] : m.wI[0];
-      const unsigned rb = __reduce_or_sync(0xffffffffu, (wIw >> shI) & RMASK);
+      const uint2 ws = rowsup[st * CH + u];
+      const unsigned rb = __reduce_or_sync(0xffffffffu, ((wword ? ws.y : ws.x) >> shI) & RMASK);
       if (rb == 0) continue;
       const double* VI = ring + (st * CH + u) * SLOT;
       const double* VJ = VI + TR * RP;
-      // this lane's columns: compact index = support bits below it; columns
-      // outside the support read the zero row
+      // this lane's columns (zero outside the support)
       double vj[CPL][RP];
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) {
-        const unsigned w = m.wJ[s];
-        const double* src = ((w >> lane) & 1u) ? VJ + (m.preJ[s] + __popc(w & lanelt)) * RP : zeros;
+      for (int p = 0; p < NP; ++p)
 #pragma unroll
-        for (int h = 0; h < RP / 2; ++h) {
-          const double2 t = reinterpret_cast<const double2*>(src)[h];
-          vj[s][2 * h] = t.x;
-          vj[s][2 * h + 1] = t.y;
+        for (int s = 0; s < CPL; ++s) {
+          const double2 t = reinterpret_cast<const double2*>(VJ + p * TC * 2)[lane + 32 * s];
+          vj[s][2 * p] = t.x;
+          vj[s][2 * p + 1] = t.y;
         }
-      }
-      int ci = (wword ? m.preI1 : 0) + __popc(wIw & ((1u << shI) - 1u));
-      ci = __shfl_sync(0xffffffffu, ci, 0);
 #pragma unroll
       for (int r8 = 0; r8 < RPW; ++r8) {
         if (rb & (1u << r8)) {  // warp-uniform
           double x[RP];
 #pragma unroll
-          for (int h = 0; h < RP / 2; ++h) {
-            const double2 t = reinterpret_cast<const double2*>(VI + ci * RP)[h];
-            x[2 * h] = t.x;
-            x[2 * h + 1] = t.y;
+          for (int p = 0; p < NP; ++p) {
+            const double2 t = reinterpret_cast<const double2*>(VI + p * TR * 2)[rfirst + r8];
+            x[2 * p] = t.x;
+            x[2 * p + 1] = t.y;
           }
-          ++ci;
 #pragma unroll
           for (int s = 0; s < CPL; ++s)
 #pragma unroll
@@ -250,13 +214,16 @@ __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
   }
-  // ---- write the slice partial ----
+  // ---- write (or add to) the slice partial ----
   double* out = a.P + (int64_t)slice * a.npad * a.npad;
 #pragma unroll
   for (int i = 0; i < RPW; ++i) {
     const int64_t row = row0 + warp * RPW + i;
 #pragma unroll
-    for (int s = 0; s < CPL; ++s) out[row * a.npad + col0 + lane + 32 * s] = acc[i][s];
+    for (int s = 0; s < CPL; ++s) {
+      double* o = out + row * a.npad + col0 + lane + 32 * s;
+      *o = a.accumulate ? *o + acc[i][s] : acc[i][s];
+    }
   }
 }
 
@@ -288,12 +255,19 @@ __global__ void k_gram_reduce(const double* __restrict__ P, int nslices, int64_t
 template <int R, int CPL, int NW>
 static size_t gram_smem() {
   using C = GramCfg<R, CPL, NW>;
-  return sizeof(double) * (size_t)C::NS * C::CH * C::SLOT + sizeof(TrialMeta) * C::NS * C::CH +
-         sizeof(int) * 4 * ((C::NS + 3) / 4) + sizeof(double) * C::RP + sizeof(uint64_t) * 2 * C::NS;
+  return sizeof(double) * (size_t)C::NS * C::CH * C::SLOT + sizeof(uint2) * C::NS * C::CH +
+         sizeof(int) * 2 * ((C::NS + 1) / 2) + sizeof(uint64_t) * 2 * C::NS;
 }
 
 template <int R, int CPL, int NW>
-static void launch_gram_t(const GramArgs& a, int ntiles, cudaStream_t s) {
+static void launch_gram_t(const GramArgs& a0, int ntiles, cudaStream_t s) {
+  using C = GramCfg<R, CPL, NW>;
+  GramArgs a = a0;
+  static const int lag_env = [] {
+    const char* e = getenv("RSM_GRAM_LAG");
+    return e ? atoi(e) : 0;
+  }();
+  a.lag = lag_env > 0 && lag_env < C::NS ? lag_env : 2;
   const size_t smem = gram_smem<R, CPL, NW>();
   cudaFuncSetAttribute(k_gram<R, CPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)ntiles, (unsigned)a.nslices);

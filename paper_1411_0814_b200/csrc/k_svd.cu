@@ -109,10 +109,7 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
       warp0_popc_scan(cm, pre, a.cmw, &flags[0]);
       __syncthreads();
       L = flags[0];
-      for (int64_t w = tid; w < a.cmw; w += nth) {
-        a.t_cm[tl * a.cmw + w] = cm[w];
-        a.t_pre[tl * a.cmw + w] = pre[w];
-      }
+      for (int64_t w = tid; w < a.cmw; w += nth) a.t_cm[tl * a.cmw + w] = cm[w];
       // gather S (K x L) row-major into vec (sampler.cpp:80-84)
       for (int64_t j = tid; j < a.n; j += nth) {
         const uint32_t word = cm[j >> 5];
@@ -131,10 +128,7 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
       __syncthreads();
       warp0_popc_scan(cm, pre, a.cmw, &flags[1]);
       __syncthreads();
-      for (int64_t w = tid; w < a.cmw; w += nth) {
-        a.t_cm[tl * a.cmw + w] = cm[w];
-        a.t_pre[tl * a.cmw + w] = pre[w];
-      }
+      for (int64_t w = tid; w < a.cmw; w += nth) a.t_cm[tl * a.cmw + w] = cm[w];
       if (tid < K) atomicAdd(a.colcnt + idx[tid], 1);
       // surviving rows: AND of the K columns' words (sampler.cpp:34-43)
       for (int64_t w = tid; w < a.mwp; w += nth) {
@@ -245,27 +239,37 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
       }
     }
     __syncthreads();
-    // rows are stored with an even stride rp >= rex (zero padded) so every
-    // trial's per-block segment is 16-byte aligned for stage 3's cp.async
+    // expanded layout (stage 3 streams it with 1-D bulk copies): the trial's
+    // top vectors as rp/2 planes of npad (v_{2p}, v_{2p+1}) pairs, zero
+    // outside the column support; rp = rex rounded up to even
     const int rex = a.rex, rp = (a.rex + 1) & ~1;
-    // compact layout: support column c (ascending) -> row c, stride rp
-    double* vout = a.Vout + a.t_off[tl];
-    if (M2) {
-      // V_top rows over the column support: v_i[c] = rotated_row_i[c] / sigma_i
-      for (int64_t c = tid; c < L; c += nth)
-        for (int i = 0; i < rp; ++i) {
-          double v = 0.0;
-          if (i < rex) {
-            const int o = ord[i];
-            const double sg = sig[o];
-            v = sg > 0.0 ? vec[o * Lp + c] / sg : 0.0;
+    double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
+    for (int64_t j = tid; j < a.npad; j += nth) {
+      int c = -1;  // support position of column j
+      if (M2) {
+        const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
+        if (word & bit) c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
+      } else {
+        for (int q = 0; q < K; ++q)
+          if (idx[q] == j) c = q;
+      }
+      for (int p = 0; p < rp / 2; ++p) {
+        double v[2] = {0.0, 0.0};
+        if (c >= 0)
+          for (int h = 0; h < 2; ++h) {
+            const int i = 2 * p + h;
+            if (i < rex) {
+              if (M2) {
+                // V_top rows over the column support: rotated_row_i[c] / sigma_i
+                const int o = ord[i];
+                const double sg = sig[o];
+                v[h] = sg > 0.0 ? vec[o * Lp + c] / sg : 0.0;
+              } else {
+                v[h] = Vacc[c * KMAX + ord[i]];
+              }
+            }
           }
-          vout[c * rp + i] = v;
-        }
-    } else {
-      for (int e = tid; e < K * rp; e += nth) {
-        const int j = e / rp, i = e % rp;
-        vout[j * rp + i] = i < rex ? Vacc[j * KMAX + ord[i]] : 0.0;
+        vout[p * a.npad + j] = make_double2(v[0], v[1]);
       }
     }
     __syncthreads();
@@ -329,7 +333,6 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
         cm[w] = acc;
         pre[w] = (uint32_t)(run + incl - c);
         a.t_cm[tl * a.cmw + w] = acc;
-        a.t_pre[tl * a.cmw + w] = (uint32_t)(run + incl - c);
       }
       run += __shfl_sync(0xffffffffu, incl, 31);
     }
@@ -448,13 +451,23 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     double inv[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) inv[i] = sig[ord[i]] > 0.0 ? 1.0 / sig[ord[i]] : 0.0;
-    // compact layout: support column c (in ascending order) -> row c, stride rp
-    double* vout = a.Vout + a.t_off[tl];
-    for (int c = lane; c < L; c += 32) {
-      for (int i = 0; i < rp; ++i) {
-        // same rounding as the CTA kernel: rotated row / sigma
-        const double v = (i < rex && i < K && inv[i] > 0.0) ? S[ord[i] * Lp + c] / sig[ord[i]] : 0.0;
-        vout[c * rp + i] = v;
+    // expanded layout (see k_svd): rp/2 planes of npad pairs, zero outside
+    // the support; same rounding as the CTA kernel: rotated row / sigma
+    double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
+    for (int64_t j = lane; j < a.npad; j += 32) {
+      const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
+      const bool in = (word & bit) != 0;
+      const int c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
+#pragma unroll
+      for (int p = 0; p < (K + 1) / 2; ++p) {
+        if (p >= rp / 2) break;
+        double v[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = 2 * p + h;
+          if (i < K && in && i < rex && inv[i] > 0.0) v[h] = S[ord[i] * Lp + c] / sig[ord[i]];
+        }
+        vout[p * a.npad + j] = make_double2(v[0], v[1]);
       }
     }
     __syncwarp();

@@ -125,7 +125,7 @@ struct rsm_ctx {
   bool haveT = false, haveCt = false;
 
   // workspace
-  DevBuf sel_idx, sel_q, blockcnt, selstate, t_attempt, t_q, t_idx, t_off, t_cm, t_pre, Vtrial,
+  DevBuf sel_idx, sel_q, blockcnt, selstate, t_attempt, t_q, t_idx, t_cm, Vtrial,
       colcnt, svd_scr, svd_scr32, P, tiles, G, eX, eY, eZ, ePart, eW, eI, eD, Vhat, U, rowres,
       flagged, dsum, cnt64;
   int64_t tiles_n = -1;
@@ -359,27 +359,31 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   int64_t t_lo, t_hi;
   rsm_shard_range(Tacc, c->world, c->rank, &t_lo, &t_hi);
   const int64_t Tl = t_hi - t_lo;
-  std::vector<int64_t> off(Tl + 1, 0);
   uint64_t z = 0;
   for (int64_t t = 0; t < Tacc; ++t) z += m2 ? (uint64_t)(hq[t] - rex) : (uint64_t)p->ell;
-  // stage 2 writes each trial's top vectors compactly (support columns in
-  // ascending order) with an even row stride, so every per-block segment is
-  // 16-byte aligned for stage 3's cp.async
-  for (int64_t t = 0; t < Tl; ++t) {
-    const int64_t cols = m2 ? hq[t_lo + t] : K;
-    off[t + 1] = off[t] + cols * ((rex + 1) & ~1);
-  }
   out.z = z;
   c->G.ensure(sizeof(double) * n * n);
   c->colcnt.ensure(sizeof(int) * npad);
   ck(cudaMemsetAsync(c->colcnt.p, 0, sizeof(int) * npad, c->stream), "memset");
+  // stage 2 writes each trial's top vectors expanded (rp/2 planes of npad
+  // pairs, zero outside the support; k_svd.cu) so stage 3 streams fixed
+  // 16-byte-aligned runs. Trials go through stages 2-3 in chunks whose
+  // expanded vectors fit the buffer budget; stage 3 accumulates across chunks.
+  const int64_t rp = (rex + 1) & ~1;
+  const int64_t tbytes = npad * rp * (int64_t)sizeof(double);
+  const int64_t budget = (int64_t)6 << 30;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(Tl, budget / tbytes));
+  const int cpl = rsmk::gram_cols_per_lane(rex);
+  build_tiles(c, npad, cpl);
+  const int64_t ntiles = ntiles_for(npad, cpl);
+  int nslices = 1;
   if (Tl > 0) {
-    c->t_off.ensure(sizeof(int64_t) * (Tl + 1));
-    ck(cudaMemcpyAsync(c->t_off.p, off.data(), sizeof(int64_t) * (Tl + 1), cudaMemcpyHostToDevice, c->stream), "H2D off");
-    c->t_cm.ensure(sizeof(uint32_t) * Tl * cmw);
-    c->t_pre.ensure(sizeof(uint32_t) * Tl * cmw);
-    c->Vtrial.ensure(sizeof(double) * std::max<int64_t>(off[Tl], 1));
-    // stage 2
+    // at most one wave of the 2-CTA/SM kernel: floor(2*SMs / tiles) slices
+    nslices = (int)std::max<int64_t>(1, ((int64_t)rsmk::gram_ctas_per_sm(rex) * c->sms) / ntiles);
+    nslices = (int)std::min<int64_t>(nslices, std::max<int64_t>(1, chunk / 16));
+    c->P.ensure(sizeof(double) * (size_t)nslices * npad * npad);
+    c->t_cm.ensure(sizeof(uint32_t) * chunk * cmw);
+    c->Vtrial.ensure((size_t)tbytes * chunk);
     int64_t Lmax = m2 ? out.sel.qmax : 0;
     if (!m2) for (int64_t t = t_lo; t < t_hi; ++t) Lmax = std::max<int64_t>(Lmax, hq[t]);
     const int64_t Lpad = std::max<int64_t>(2, (Lmax + 1) & ~int64_t(1));
@@ -389,56 +393,49 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     const size_t smem = fixed + (use_smem ? vecb : 0);
     int occ = rsmk::svd_occupancy(m2, smem);
     if (occ < 1) occ = 1;
-    const int64_t grid = std::min<int64_t>(Tl, (int64_t)c->sms * occ);
-    rsmk::SvdArgs a{};
-    a.Y = v.Y; a.m = v.m; a.n = v.n;
-    a.bitsR = v.bitsR; a.nwp = v.nwp;
-    a.bitsC = v.bitsC; a.mwp = v.mwp;
-    a.t_idx = c->t_idx.as<int32_t>();
-    a.t_lo = t_lo; a.t_hi = t_hi;
-    a.block = K; a.rex = rex;
-    a.t_off = c->t_off.as<int64_t>();
-    a.t_cm = c->t_cm.as<uint32_t>(); a.t_pre = c->t_pre.as<uint32_t>(); a.cmw = cmw;
-    a.Vout = c->Vtrial.as<double>();
-    a.colcnt = c->colcnt.as<int>();
-    if (!use_smem) {
-      c->svd_scr.ensure(vecb * grid);
-      a.scratch = c->svd_scr.as<double>();
+    for (int64_t c0 = t_lo; c0 < t_hi; c0 += chunk) {
+      const int64_t c1 = std::min<int64_t>(t_hi, c0 + chunk);
+      // stage 2
+      const int64_t grid = std::min<int64_t>(c1 - c0, (int64_t)c->sms * occ);
+      rsmk::SvdArgs a{};
+      a.Y = v.Y; a.m = v.m; a.n = v.n;
+      a.bitsR = v.bitsR; a.nwp = v.nwp;
+      a.bitsC = v.bitsC; a.mwp = v.mwp;
+      a.t_idx = c->t_idx.as<int32_t>();
+      a.t_lo = c0; a.t_hi = c1;
+      a.block = K; a.rex = rex;
+      a.t_cm = c->t_cm.as<uint32_t>(); a.cmw = cmw; a.npad = npad;
+      a.Vout = c->Vtrial.as<double>();
+      a.colcnt = c->colcnt.as<int>();
+      if (!use_smem) {
+        c->svd_scr.ensure(vecb * grid);
+        a.scratch = c->svd_scr.as<double>();
+      }
+      if (!m2) {
+        c->svd_scr32.ensure(sizeof(uint32_t) * 2 * v.mwp * grid);
+        a.scratch_u32 = c->svd_scr32.as<uint32_t>();
+      }
+      a.Lpad = Lpad;
+      a.use_smem = use_smem ? 1 : 0;
+      // row branch with k <= 9: warp-per-trial kernel; otherwise CTA per trial
+      if (!(m2 && rsmk::launch_svd_warp(a, c->sms, c->stream))) rsmk::launch_svd(a, m2, (int)grid, smem, c->stream);
+      ++c->launches;
+      ck(cudaGetLastError(), "svd launch");
+      if (c0 == t_lo) record(c, 2);  // with several chunks, later stage-2 work counts as stage 3
+      // stage 3
+      rsmk::GramArgs g{};
+      g.t_cm = c->t_cm.as<uint32_t>();
+      g.V = c->Vtrial.as<double>();
+      g.T = c1 - c0; g.cmw = cmw; g.npad = npad; g.R = rex; g.nslices = nslices;
+      g.accumulate = c0 > t_lo ? 1 : 0;
+      g.tiles = c->tiles.as<int2>();
+      g.P = c->P.as<double>();
+      rsmk::launch_gram(g, (int)ntiles, c->stream);
+      ++c->launches;
+      ck(cudaGetLastError(), "gram launch");
     }
-    if (!m2) {
-      c->svd_scr32.ensure(sizeof(uint32_t) * 2 * v.mwp * grid);
-      a.scratch_u32 = c->svd_scr32.as<uint32_t>();
-    }
-    a.Lpad = Lpad;
-    a.use_smem = use_smem ? 1 : 0;
-    // row branch with k <= 9: warp-per-trial kernel; otherwise CTA per trial
-    if (!(m2 && rsmk::launch_svd_warp(a, c->sms, c->stream))) rsmk::launch_svd(a, m2, (int)grid, smem, c->stream);
-    ++c->launches;
-    ck(cudaGetLastError(), "svd launch");
-  }
-  record(c, 2);
-  // stage 3
-  const int cpl = rsmk::gram_cols_per_lane(rex);
-  build_tiles(c, npad, cpl);
-  const int64_t ntiles = ntiles_for(npad, cpl);
-  int nslices = 1;
-  if (Tl > 0) {
-    // at most one wave of the 2-CTA/SM kernel: floor(2*SMs / tiles) slices
-    nslices = (int)std::max<int64_t>(1, ((int64_t)rsmk::gram_ctas_per_sm(rex) * c->sms) / ntiles);
-    nslices = (int)std::min<int64_t>(nslices, std::max<int64_t>(1, Tl / 16));
-    c->P.ensure(sizeof(double) * (size_t)nslices * npad * npad);
-    rsmk::GramArgs g{};
-    g.t_cm = c->t_cm.as<uint32_t>();
-    g.t_pre = c->t_pre.as<uint32_t>();
-    g.t_off = c->t_off.as<int64_t>();
-    g.V = c->Vtrial.as<double>();
-    g.T = Tl; g.cmw = cmw; g.npad = npad; g.R = rex; g.nslices = nslices;
-    g.tiles = c->tiles.as<int2>();
-    g.P = c->P.as<double>();
-    rsmk::launch_gram(g, (int)ntiles, c->stream);
-    ++c->launches;
-    ck(cudaGetLastError(), "gram launch");
   } else {
+    record(c, 2);
     c->P.ensure(sizeof(double) * npad * npad);
     ck(cudaMemsetAsync(c->P.p, 0, sizeof(double) * npad * npad, c->stream), "memset");
   }
@@ -766,7 +763,7 @@ rsm_status rsm_ctx_destroy(rsm_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->Y, &c->M8, &c->bitsR, &c->bitsC, &c->Yt, &c->M8t, &c->bitsRt, &c->bitsCt,
                     &c->sel_idx, &c->sel_q, &c->blockcnt, &c->selstate, &c->t_attempt, &c->t_q,
-                    &c->t_idx, &c->t_off, &c->t_cm, &c->t_pre, &c->Vtrial, &c->colcnt, &c->svd_scr,
+                    &c->t_idx, &c->t_cm, &c->Vtrial, &c->colcnt, &c->svd_scr,
                     &c->svd_scr32, &c->P, &c->tiles, &c->G, &c->eX, &c->eY, &c->eZ, &c->ePart,
                     &c->eW, &c->eI, &c->eD, &c->Vhat, &c->U, &c->rowres, &c->flagged, &c->dsum,
                     &c->cnt64};

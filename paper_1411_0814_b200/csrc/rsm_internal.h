@@ -27,11 +27,10 @@ struct SvdArgs {
   int64_t t_lo, t_hi;    // this rank's trial range
   int block;             // K
   int rex;               // top vectors kept (q - ell)
-  const int64_t* t_off;  // local trial -> offset (doubles) into Vout
   uint32_t* t_cm;        // local trials x cmw support words
-  uint32_t* t_pre;       // local trials x cmw exclusive popcount prefix
   int64_t cmw;
-  double* Vout;
+  int64_t npad;          // expanded column count (multiple of 128)
+  double* Vout;          // local trials x (rp/2) planes x npad x 2 (see k_svd.cu)
   int* colcnt;           // n per-column trial counts
   double* scratch;       // per-CTA vector scratch when shared memory is too small
   uint32_t* scratch_u32; // per-CTA 2*mwp words (column branch)
@@ -41,14 +40,14 @@ struct SvdArgs {
 
 struct GramArgs {
   const uint32_t* t_cm;
-  const uint32_t* t_pre;
-  const int64_t* t_off;
-  const double* V;
+  const double* V;  // expanded top vectors, SvdArgs::Vout layout
   int64_t T;       // local trial count
   int64_t cmw;
   int64_t npad;
   int R;
   int nslices;
+  int lag;         // stage-3 ring: refill the stage released lag groups ago
+  int accumulate;  // add to P instead of overwriting (trial chunks after the first)
   const int2* tiles;
   double* P;       // nslices x npad x npad partials
 };
