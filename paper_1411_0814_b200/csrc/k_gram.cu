@@ -59,13 +59,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
-template <int R, int CPL, int NW>
+template <int R, int CPL, int RG>
 struct GramCfg {
+  static constexpr int NW = 8;             // warps
+  static constexpr int WPR = NW / RG;      // warps sharing a row group (split columns)
+  static constexpr int LCPL = CPL / WPR;   // columns per lane
   static constexpr int RP = (R + 1) & ~1;  // planes * 2
   static constexpr int NP = RP / 2;        // planes
   static constexpr int TR = 64;
   static constexpr int TC = 32 * CPL;
-  static constexpr int RPW = TR / NW;          // rows per warp
+  static constexpr int RPW = TR / RG;          // rows per warp
   static constexpr int CH = (R <= 4) ? 4 : 2;  // trials per ring stage
   static constexpr int NS = 4;                 // ring depth (stages)
   static constexpr int SLOT = (TR + TC) * RP;  // doubles per trial slot
@@ -83,11 +86,12 @@ struct GramCfg {
 // warp loads the support words of the next group it produces right after
 // producing one. Row activity is made warp-uniform with a redux so the
 // compiler branches on the uniform datapath.
-template <int R, int CPL, int NW>
-__global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
-  using C = GramCfg<R, CPL, NW>;
+template <int R, int CPL, int RG>
+__global__ void __launch_bounds__(256, 2) k_gram(GramArgs a) {
+  using C = GramCfg<R, CPL, RG>;
   constexpr int RP = C::RP, NP = C::NP, TR = C::TR, TC = C::TC, RPW = C::RPW, CH = C::CH, NS = C::NS,
-                SLOT = C::SLOT;
+                SLOT = C::SLOT, NW = C::NW, LCPL = C::LCPL;
+  static_assert(LCPL >= 1 && LCPL * C::WPR == CPL, "column split");
   extern __shared__ __align__(16) double sm[];
   double* ring = sm;                                                     // [NS][CH][SLOT]
   uint2* rowsup = reinterpret_cast<uint2*>(ring + NS * CH * SLOT);       // [NS][CH]
@@ -158,15 +162,16 @@ __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
   load(warp);
   for (int h = warp; h < NS && h < ngroups; h += NW) produce(h);
 
-  double acc[RPW][CPL];
+  double acc[RPW][LCPL];
 #pragma unroll
   for (int i = 0; i < RPW; ++i)
 #pragma unroll
-    for (int s = 0; s < CPL; ++s) acc[i][s] = 0.0;
+    for (int s = 0; s < LCPL; ++s) acc[i][s] = 0.0;
 
-  const int wword = (warp * RPW) >> 5;  // row-support word of this warp's rows
-  const int shI = (warp * RPW) & 31;    // bit offset inside it
-  const int rfirst = warp * RPW;
+  const int rfirst = (warp % RG) * RPW;      // this warp's rows within the tile
+  const int cfirst = (warp / RG) * 32 * LCPL;  // and its first column
+  const int wword = rfirst >> 5;             // row-support word of those rows
+  const int shI = rfirst & 31;               // bit offset inside it
   constexpr unsigned RMASK = RPW >= 32 ? 0xffffffffu : ((1u << RPW) - 1u);
   for (int64_t g = 0; g < ngroups; ++g) {
     const int st = (int)(g % NS);
@@ -185,12 +190,12 @@ __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
       const double* VI = ring + (st * CH + u) * SLOT;
       const double* VJ = VI + TR * RP;
       // this lane's columns (zero outside the support)
-      double vj[CPL][RP];
+      double vj[LCPL][RP];
 #pragma unroll
       for (int p = 0; p < NP; ++p)
 #pragma unroll
-        for (int s = 0; s < CPL; ++s) {
-          const double2 t = reinterpret_cast<const double2*>(VJ + p * TC * 2)[lane + 32 * s];
+        for (int s = 0; s < LCPL; ++s) {
+          const double2 t = reinterpret_cast<const double2*>(VJ + p * TC * 2)[cfirst + lane + 32 * s];
           vj[s][2 * p] = t.x;
           vj[s][2 * p + 1] = t.y;
         }
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
             x[2 * p + 1] = t.y;
           }
 #pragma unroll
-          for (int s = 0; s < CPL; ++s)
+          for (int s = 0; s < LCPL; ++s)
 #pragma unroll
             for (int k = 0; k < R; ++k) acc[r8][s] = fma(-x[k], vj[s][k], acc[r8][s]);
         }
@@ -218,10 +223,10 @@ __global__ void __launch_bounds__(32 * NW, 2) k_gram(GramArgs a) {
   double* out = a.P + (int64_t)slice * a.npad * a.npad;
 #pragma unroll
   for (int i = 0; i < RPW; ++i) {
-    const int64_t row = row0 + warp * RPW + i;
+    const int64_t row = row0 + rfirst + i;
 #pragma unroll
-    for (int s = 0; s < CPL; ++s) {
-      double* o = out + row * a.npad + col0 + lane + 32 * s;
+    for (int s = 0; s < LCPL; ++s) {
+      double* o = out + row * a.npad + col0 + cfirst + lane + 32 * s;
       *o = a.accumulate ? *o + acc[i][s] : acc[i][s];
     }
   }
@@ -252,44 +257,51 @@ __global__ void k_gram_reduce(const double* __restrict__ P, int nslices, int64_t
   }
 }
 
-template <int R, int CPL, int NW>
+template <int R, int CPL, int RG>
 static size_t gram_smem() {
-  using C = GramCfg<R, CPL, NW>;
+  using C = GramCfg<R, CPL, RG>;
   return sizeof(double) * (size_t)C::NS * C::CH * C::SLOT + sizeof(uint2) * C::NS * C::CH +
          sizeof(int) * 2 * ((C::NS + 1) / 2) + sizeof(uint64_t) * 2 * C::NS;
 }
 
-template <int R, int CPL, int NW>
+template <int R, int CPL, int RG>
 static void launch_gram_t(const GramArgs& a0, int ntiles, cudaStream_t s) {
-  using C = GramCfg<R, CPL, NW>;
+  using C = GramCfg<R, CPL, RG>;
   GramArgs a = a0;
   static const int lag_env = [] {
     const char* e = getenv("RSM_GRAM_LAG");
     return e ? atoi(e) : 0;
   }();
   a.lag = lag_env > 0 && lag_env < C::NS ? lag_env : 2;
-  const size_t smem = gram_smem<R, CPL, NW>();
-  cudaFuncSetAttribute(k_gram<R, CPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = gram_smem<R, CPL, RG>();
+  cudaFuncSetAttribute(k_gram<R, CPL, RG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)ntiles, (unsigned)a.nslices);
-  k_gram<R, CPL, NW><<<grid, 32 * NW, smem, s>>>(a);
+  k_gram<R, CPL, RG><<<grid, 256, smem, s>>>(a);
 }
 
 int gram_cols_per_lane(int R) { return R <= 4 ? 4 : (R <= 8 ? 2 : 1); }
 
 int gram_ctas_per_sm(int) { return 2; }
 
-static int gram_warps() {
-  static int nw = [] {
-    const char* e = getenv("RSM_GRAM_WARPS");
+// row groups per tile: 8 (8 rows x all tile columns per warp) or 4 (16 rows
+// x half the columns: half the column reads per trial, twice the row reads)
+static int gram_row_groups() {
+  static int rg = [] {
+    const char* e = getenv("RSM_GRAM_RG");
     return (e && atoi(e) == 4) ? 4 : 8;
   }();
-  return nw;
+  return rg;
 }
 
 template <int R, int CPL>
 static void launch_gram_r(const GramArgs& a, int ntiles, cudaStream_t s) {
-  if (gram_warps() == 4) launch_gram_t<R, CPL, 4>(a, ntiles, s);
-  else launch_gram_t<R, CPL, 8>(a, ntiles, s);
+  if constexpr (CPL >= 2) {
+    if (gram_row_groups() == 4) {
+      launch_gram_t<R, CPL, 4>(a, ntiles, s);
+      return;
+    }
+  }
+  launch_gram_t<R, CPL, 8>(a, ntiles, s);
 }
 
 void launch_gram(const GramArgs& a, int ntiles, cudaStream_t s) {

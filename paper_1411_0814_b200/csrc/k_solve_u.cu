@@ -31,30 +31,7 @@ using namespace rsmd;
 
 namespace {
 
-constexpr int SU_WARPS = 4;
-
-template <int R>
-struct RowAcc {
-  static constexpr int NP = R * (R + 1) / 2;
-  double A[NP];
-  double b[R];
-  int nj;
-};
-
-template <int R>
-__device__ __forceinline__ void acc_add(RowAcc<R>& s, const double* v, double y) {
-  int p = 0;
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-#pragma unroll
-    for (int j = i; j < R; ++j) {
-      s.A[p] = fma(v[i], v[j], s.A[p]);
-      ++p;
-    }
-    s.b[i] = fma(y, v[i], s.b[i]);
-  }
-  ++s.nj;
-}
+constexpr int SU_MAXW = 16;  // warps per CTA (upper bound; chosen at launch)
 
 // minimum-norm solution via eigendecomposition of the (symmetric PSD) normal
 // matrix; returns the numerical rank
@@ -123,110 +100,214 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes
   else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 
-// issue the copies of one row (values + mask words) into a warp buffer
-__device__ __forceinline__ void issue_row(const SolveUArgs& a, int64_t row, double* ybuf, uint32_t* wbuf,
-                                          bool vec16) {
-  const int lane = threadIdx.x & 31;
-  const double* y = a.Y + row * a.n;
-  if (vec16) {
-    for (int64_t c = lane; c < a.n / 2; c += 32) cp_async(ybuf + 2 * c, y + 2 * c, 1);
-  } else {
-    for (int64_t c = lane; c < a.n; c += 32) cp_async(ybuf + c, y + c, 0);
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// Sum N (power of two) per-lane values over the warp by recursive halving:
+// at each of the first log2(min(N,32)) exchanges a lane keeps one half of its
+// values and receives its partner's copy of that half, so the shuffle count
+// is ~N instead of 5N. On return lane l holds max(1, N/32) totals in v[0..]:
+// value j sits in lane (j / PL) * max(1, 32/N), slot j % PL.
+template <int N>
+__device__ __forceinline__ void warp_reduce_halving(double (&v)[N], int lane) {
+  constexpr int STEPS = N >= 32 ? 5 : (N >= 16 ? 4 : (N >= 8 ? 3 : (N >= 4 ? 2 : (N >= 2 ? 1 : 0))));
+#pragma unroll
+  for (int st = 0; st < STEPS; ++st) {
+    const int o = 16 >> st;
+    const int K = N >> st;  // values still held
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      if (i < K / 2) {
+        const double mine = up ? v[i + K / 2] : v[i];
+        const double other = up ? v[i] : v[i + K / 2];
+        v[i] = mine + __shfl_xor_sync(0xffffffffu, other, o);
+      }
+    }
   }
-  const uint32_t* w = a.bitsR + row * a.nwp;  // nwp is a multiple of 4 words
-  for (int64_t c = lane; c < a.nwp / 4; c += 32) cp_async(wbuf + 4 * c, w + 4 * c, 1);
-  asm volatile("cp.async.commit_group;\n" ::);
+  // remaining lane bits: plain butterfly on the single held value
+  if (N < 32) {
+#pragma unroll
+    for (int o = 16 >> STEPS; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  }
 }
+
+template <int N>
+__device__ __forceinline__ double warp_total(const double (&v)[N], int j) {
+  constexpr int PL = N > 32 ? N / 32 : 1;
+  constexpr int LPV = N < 32 ? 32 / N : 1;
+  double x = v[0];
+#pragma unroll
+  for (int s = 1; s < PL; ++s)
+    if (j % PL == s) x = v[s];
+  return __shfl_sync(0xffffffffu, x, (j / PL) * LPV);
+}
+
+__host__ __device__ constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
 }  // namespace
 
-template <int R, bool VSMEM>
-__global__ void __launch_bounds__(SU_WARPS * 32) k_solve_u(SolveUArgs a) {
+// One warp per row (rows strided over the grid's warps), two row buffers per
+// warp in shared memory. With BULK (even n) the next row's values and mask
+// words arrive by two 1-D bulk copies (TMA) on the buffer's mbarrier, issued
+// by one lane; otherwise by per-lane cp.async. V-hat sits in shared memory as
+// ceil(R/2) planes of (v_2p, v_2p+1) pairs (VSMEM) or is read from global.
+template <int R, bool VSMEM, bool BULK>
+__global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u(SolveUArgs a) {
+  constexpr int NP = (R + 1) / 2;           // V planes
+  constexpr int NA = R * (R + 1) / 2;       // packed normal matrix
+  constexpr int NV = pow2_at_least(NA + R + 1);  // reduced values (A, b, count, pad)
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int64_t npd = (n + 1) & ~int64_t(1);
-  double* Vs = sm;
-  double* wb = sm + (VSMEM ? ((n * R + 1) & ~int64_t(1)) : 0);
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);  // [SU_MAXW][2]
+  double2* Vp = reinterpret_cast<double2*>(sm + 2 * SU_MAXW);
+  double* wb = sm + 2 * SU_MAXW + (VSMEM ? 2 * NP * n : 0);
   const int64_t bufd = npd + a.nwp / 2;  // doubles per row buffer (values + words)
-  double* yb0 = wb + (2 * warp) * bufd;
-  double* yb1 = wb + (2 * warp + 1) * bufd;
-  // V in shared memory is stored component-major (Vs[k*n + c]) so the 32
-  // lanes of a warp, which own 32 consecutive columns, read consecutive words
-  if (VSMEM) {
-    for (int64_t e = threadIdx.x; e < n * R; e += blockDim.x) Vs[(e % R) * n + e / R] = a.V[e];
-    __syncthreads();
+  auto ybuf = [&](int b) { return wb + (2 * warp + b) * bufd; };
+  if (BULK && threadIdx.x < 2 * nwarps) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + threadIdx.x)), "r"(1));
   }
-  auto vrow = [&](int64_t c, double* v) {
+  if (BULK && threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  if (VSMEM) {
+    for (int64_t e = threadIdx.x; e < NP * n; e += blockDim.x) {
+      const int64_t p = e / n, c = e % n;
+      const double x0 = a.V[c * R + 2 * p];
+      const double x1 = (2 * p + 1 < R) ? a.V[c * R + 2 * p + 1] : 0.0;
+      Vp[e] = make_double2(x0, x1);
+    }
+  }
+  __syncthreads();
+  auto vload = [&](int64_t c, double* v) {
 #pragma unroll
-    for (int k = 0; k < R; ++k) v[k] = VSMEM ? Vs[k * n + c] : __ldg(a.V + c * R + k);
+    for (int p = 0; p < NP; ++p) {
+      double2 t;
+      if (VSMEM) t = Vp[p * n + c];
+      else {
+        t.x = __ldg(a.V + c * R + 2 * p);
+        t.y = (2 * p + 1 < R) ? __ldg(a.V + c * R + 2 * p + 1) : 0.0;
+      }
+      v[2 * p] = t.x;
+      if (2 * p + 1 < R) v[2 * p + 1] = t.y;
+    }
   };
-  const bool vec16 = (n % 2) == 0;
-  const int64_t gw = (int64_t)blockIdx.x * SU_WARPS + warp;
-  const int64_t nw = (int64_t)gridDim.x * SU_WARPS;
+  const uint32_t ybytes = (uint32_t)(n * 8), wbytes = (uint32_t)(a.nwp * 4);
+  auto issue = [&](int64_t row, int b) {
+    double* yb = ybuf(b);
+    uint32_t* wdst = reinterpret_cast<uint32_t*>(yb + npd);
+    if (BULK) {
+      if (lane == 0) {
+        const unsigned bar = smem_u32(bars + 2 * warp + b);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(ybytes + wbytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                smem_u32(yb)),
+            "l"(a.Y + row * n), "r"(ybytes), "r"(bar)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                smem_u32(wdst)),
+            "l"(a.bitsR + row * a.nwp), "r"(wbytes), "r"(bar)
+            : "memory");
+      }
+    } else {
+      const double* y = a.Y + row * n;
+      for (int64_t c = lane; c < n; c += 32) cp_async(yb + c, y + c, 0);
+      const uint32_t* w = a.bitsR + row * a.nwp;  // nwp is a multiple of 4 words
+      for (int64_t c = lane; c < a.nwp / 4; c += 32) cp_async(wdst + 4 * c, w + 4 * c, 1);
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
+  };
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t nw = (int64_t)gridDim.x * nwarps;
+  unsigned phase = 0u;  // bit b: parity of buffer b's next completion
   int cur = 0;
   int64_t row = a.row_lo + gw;
-  if (row < a.row_hi) issue_row(a, row, yb0, reinterpret_cast<uint32_t*>(yb0 + npd), vec16);
+  if (row < a.row_hi) issue(row, 0);
+  const int nfull = (int)(n >> 5);
   for (; row < a.row_hi; row += nw) {
-    double* ycur = cur ? yb1 : yb0;
-    double* ynxt = cur ? yb0 : yb1;
     const int64_t nxt = row + nw;
-    if (nxt < a.row_hi) {
-      issue_row(a, nxt, ynxt, reinterpret_cast<uint32_t*>(ynxt + npd), vec16);
-      asm volatile("cp.async.wait_group 1;\n" ::);
+    if (nxt < a.row_hi) issue(nxt, cur ^ 1);
+    if (BULK) {
+      const unsigned bar = smem_u32(bars + 2 * warp + cur);
+      unsigned done = 0;
+      do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"((phase >> cur) & 1u)
+            : "memory");
+      } while (!done);
+      phase ^= 1u << cur;
     } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
+      if (nxt < a.row_hi) asm volatile("cp.async.wait_group 1;\n" ::);
+      else asm volatile("cp.async.wait_group 0;\n" ::);
+      __syncwarp();
     }
-    __syncwarp();
-    const double* y = ycur;
-    const uint32_t* wd = reinterpret_cast<const uint32_t*>(ycur + npd);
-    RowAcc<R> s;
+    const double* y = ybuf(cur);
+    const uint32_t* wd = reinterpret_cast<const uint32_t*>(y + npd);
+    // normal equations over the observed cells; hidden cells are skipped by
+    // predication (their NaN never enters arithmetic)
+    double acc[NV];
 #pragma unroll
-    for (int p = 0; p < RowAcc<R>::NP; ++p) s.A[p] = 0.0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) s.b[i] = 0.0;
-    s.nj = 0;
-    // branchless: unknown cells contribute zero vectors (selected, never
-    // multiplied, so the NaN at hidden cells never enters arithmetic)
-    const int nfull = (int)(n >> 5);
-    for (int w = 0; w < nfull; ++w) {
-      const int c = w * 32 + lane;
-      const bool k = (wd[w] >> lane) & 1u;
+    for (int p = 0; p < NV; ++p) acc[p] = 0.0;
+    // branchless (so the loads of consecutive columns pipeline): a hidden
+    // cell's basis row is scaled by 0 and its value selected away, so the NaN
+    // stored there never enters arithmetic
+    auto add = [&](int64_t c, bool k) {
       double v[R];
-      vrow(c, v);
+      vload(c, v);
+      const double yc = k ? y[c] : 0.0;
+      const double kf = k ? 1.0 : 0.0;
+      double t[R];
 #pragma unroll
-      for (int q = 0; q < R; ++q) v[q] = k ? v[q] : 0.0;
-      acc_add<R>(s, v, k ? y[c] : 0.0);
-      s.nj += k ? 0 : -1;  // acc_add counted one
+      for (int i = 0; i < R; ++i) t[i] = kf * v[i];
+      int p = 0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+#pragma unroll
+        for (int j = i; j < R; ++j) {
+          acc[p] = fma(t[i], v[j], acc[p]);
+          ++p;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i) acc[NA + i] = fma(yc, v[i], acc[NA + i]);
+    };
+#pragma unroll 2
+    for (int w = 0; w < nfull; ++w) add(w * 32 + lane, (wd[w] >> lane) & 1u);
+    if ((int64_t)nfull * 32 + lane < n) add(nfull * 32 + lane, (wd[nfull] >> lane) & 1u);
+    {
+      int cnt = 0;  // observed cells (mask words are zero beyond n)
+      for (int64_t w = lane; w < a.nwp; w += 32) cnt += __popc(wd[w]);
+      acc[NA + R] = (double)cnt;
     }
-    if ((int64_t)nfull * 32 + lane < n && ((wd[nfull] >> lane) & 1u)) {
-      const int c = nfull * 32 + lane;
-      double v[R];
-      vrow(c, v);
-      acc_add<R>(s, v, y[c]);
-    }
-    // butterfly reduction: every lane ends with the row totals
+    warp_reduce_halving<NV>(acc, lane);
+    double A[NA], bv[R];
 #pragma unroll
-    for (int p = 0; p < RowAcc<R>::NP; ++p) s.A[p] = warp_sum(s.A[p]);
+    for (int p = 0; p < NA; ++p) A[p] = warp_total<NV>(acc, p);
 #pragma unroll
-    for (int i = 0; i < R; ++i) s.b[i] = warp_sum(s.b[i]);
-    const int nj = warp_sum_int(s.nj);
+    for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, NA + i);
+    const int nj = (int)warp_total<NV>(acc, NA + R);
 
     double u[R];
     bool flagged = false;
     bool slow = nj < R;
     if (!slow) {
       // Cholesky of the packed normal matrix (lower factor, row-major packed)
-      double L[RowAcc<R>::NP];
+      double L[NA];
       double dmax = 0.0;
 #pragma unroll
-      for (int i = 0; i < R; ++i) dmax = fmax(dmax, s.A[i * R - i * (i - 1) / 2]);
+      for (int i = 0; i < R; ++i) dmax = fmax(dmax, A[i * R - i * (i - 1) / 2]);
       int q = 0;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
 #pragma unroll
         for (int j = 0; j <= i; ++j) {
-          double v = s.A[j * R - j * (j - 1) / 2 + (i - j)];
+          double v = A[j * R - j * (j - 1) / 2 + (i - j)];
 #pragma unroll
           for (int k = 0; k < j; ++k) v -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
           if (i == j) {
@@ -242,7 +323,7 @@ __global__ void __launch_bounds__(SU_WARPS * 32) k_solve_u(SolveUArgs a) {
         double z[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-          double v = s.b[i];
+          double v = bv[i];
 #pragma unroll
           for (int k = 0; k < i; ++k) v -= L[i * (i + 1) / 2 + k] * z[k];
           z[i] = v / L[i * (i + 1) / 2 + i];
@@ -257,32 +338,23 @@ __global__ void __launch_bounds__(SU_WARPS * 32) k_solve_u(SolveUArgs a) {
       }
     }
     if (slow) {
-      const int rank = pinv_solve<R>(s.A, s.b, u);
+      const int rank = pinv_solve<R>(A, bv, u);
       flagged = (nj < R) || (rank < R);
     }
     // second pass over the row still in shared memory: direct residual
     double ss = 0.0;
-    for (int w = 0; w < nfull; ++w) {
-      const int c = w * 32 + lane;
-      const bool k = (wd[w] >> lane) & 1u;
+    auto res = [&](int64_t c, bool k) {
       double v[R];
-      vrow(c, v);
+      vload(c, v);
       double p = 0.0;
 #pragma unroll
       for (int q = 0; q < R; ++q) p = fma(u[q], v[q], p);
       const double d = k ? y[c] - p : 0.0;
       ss = fma(d, d, ss);
-    }
-    if ((int64_t)nfull * 32 + lane < n && ((wd[nfull] >> lane) & 1u)) {
-      const int c = nfull * 32 + lane;
-      double v[R];
-      vrow(c, v);
-      double p = 0.0;
-#pragma unroll
-      for (int q = 0; q < R; ++q) p = fma(u[q], v[q], p);
-      const double d = y[c] - p;
-      ss = fma(d, d, ss);
-    }
+    };
+#pragma unroll 2
+    for (int w = 0; w < nfull; ++w) res(w * 32 + lane, (wd[w] >> lane) & 1u);
+    if ((int64_t)nfull * 32 + lane < n) res(nfull * 32 + lane, (wd[nfull] >> lane) & 1u);
     ss = warp_sum(ss);
     if (lane < R) {
       double uk = 0.0;
@@ -344,30 +416,42 @@ void launch_residual(const double* Y, const uint32_t* bitsR, int64_t m, int64_t 
   k_residual<<<(unsigned)blocks, 256, 0, s>>>(Y, bitsR, m, n, nwp, U, V, r, rowres);
 }
 
+template <int R, bool VSMEM, bool BULK>
+static void launch_solve_u_k(const SolveUArgs& a, size_t fixed, size_t per_warp, int sms, cudaStream_t s) {
+  // one CTA per SM with as many warps as the row buffers allow: V-hat is
+  // staged once per SM and every warp keeps two rows in flight
+  const size_t cap = 227 * 1024;
+  int w = (int)std::min<size_t>(SU_MAXW, (cap - fixed) / per_warp);
+  if (w < 1) w = 1;
+  const size_t smem = fixed + (size_t)w * per_warp;
+  cudaFuncSetAttribute(k_solve_u<R, VSMEM, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t rows = a.row_hi - a.row_lo;
+  int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
+  if (blocks < 1) blocks = 1;
+  k_solve_u<R, VSMEM, BULK><<<(unsigned)blocks, w * 32, smem, s>>>(a);
+}
+
 template <int R>
 static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t vbytes = sizeof(double) * (size_t)(((a.n * R) + 1) & ~int64_t(1));
+  constexpr int NP = (R + 1) / 2;
+  const size_t head = sizeof(double) * 2 * SU_MAXW;  // mbarriers
+  const size_t vbytes = sizeof(double) * 2 * NP * (size_t)a.n;
   const size_t bufb = sizeof(double) * (size_t)(((a.n + 1) & ~int64_t(1)) + a.nwp / 2);
-  const size_t rows_b = (size_t)SU_WARPS * 2 * bufb;
-  const bool vsm = vbytes + rows_b <= 112 * 1024;
-  const size_t smem = rows_b + (vsm ? vbytes : 0);
-  const int64_t rows = a.row_hi - a.row_lo;
-  int occ = 0;
+  const size_t per_warp = 2 * bufb;
+  // V-hat in shared memory when it leaves room for at least 8 warps
+  const bool vsm = head + vbytes + 8 * per_warp <= 227 * 1024;
+  const bool bulk = (a.n % 2) == 0;
+  const size_t fixed = head + (vsm ? vbytes : 0);
   if (vsm) {
-    cudaFuncSetAttribute(k_solve_u<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_solve_u<R, true>, SU_WARPS * 32, smem);
+    if (bulk) launch_solve_u_k<R, true, true>(a, fixed, per_warp, sms, s);
+    else launch_solve_u_k<R, true, false>(a, fixed, per_warp, sms, s);
   } else {
-    cudaFuncSetAttribute(k_solve_u<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_solve_u<R, false>, SU_WARPS * 32, smem);
+    if (bulk) launch_solve_u_k<R, false, true>(a, fixed, per_warp, sms, s);
+    else launch_solve_u_k<R, false, false>(a, fixed, per_warp, sms, s);
   }
-  if (occ < 1) occ = 1;
-  int64_t blocks = std::min<int64_t>((rows + SU_WARPS - 1) / SU_WARPS, (int64_t)sms * occ);
-  if (blocks < 1) blocks = 1;
-  if (vsm) k_solve_u<R, true><<<(unsigned)blocks, SU_WARPS * 32, smem, s>>>(a);
-  else k_solve_u<R, false><<<(unsigned)blocks, SU_WARPS * 32, smem, s>>>(a);
 }
 
 void launch_solve_u(const SolveUArgs& a, cudaStream_t s) {
