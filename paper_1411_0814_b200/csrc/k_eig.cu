@@ -38,8 +38,7 @@ namespace {
 constexpr int ET = 256;        // threads per CTA
 constexpr int BMAX = 16;       // max block size
 constexpr int LDM = BMAX + 1;  // + power column
-constexpr int XS_BYTES = 96 * 1024;  // dynamic shared memory for the staged iterate
-constexpr int RPW = 2;         // rows per warp per pass
+constexpr int DYN_BYTES = 212 * 1024;  // dynamic shared memory: staged iterate (+ the CTA's rows of G)
 
 struct EigShared {
   double pad0;
@@ -47,71 +46,127 @@ struct EigShared {
   double S[BMAX * BMAX];
   double red[LDM * (LDM + 1) / 2 + 2 * LDM + 8];
   double theta[BMAX];
+  double dinv[BMAX];  // reciprocal diagonal of the Cholesky factor in S
   double cs[64];
   int pairs[64];
   int flag[4];
+  double red2[(ET / 32) * 34];  // matvec cross-warp partials
+  unsigned long long xbar;      // mbarrier of the iterate's bulk copies
 };
 
 __device__ __forceinline__ int pw_of(int b) { return (b + 1) * (b + 2) / 2 + 2 * (b + 1) + 8; }
 
-// Y(rows) = G * X(all rows), ncol columns, leading dimension ld. The iterate
-// is staged into shared memory (xs, kc rows at a time; the whole of it when
-// it fits) with 16-byte loads, all in flight at once.
-__device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double* __restrict__ Yout,
-                       int ncol, int ld, int row_lo, int row_hi, double* xs, int kc) {
+// Y(rows) = G * X, ncol <= NC columns, leading dimension ld. The CTA's rows
+// are taken in pairs; each pair gets 8/npairs warps that split the k range,
+// and a lane accumulates both rows x all columns over its k's in registers
+// (every x element is loaded once per pair, every G element once). Partials
+// are reduced by recursive halving within the warp and in a fixed order
+// across the k-split warps, so Y is bitwise reproducible. gs holds the CTA's
+// G rows in shared memory (nullptr: read them from global / L2); X is read
+// with coherent loads (it was written by other CTAs before the grid sync).
+template <int NC>
+__device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double* __restrict__ Yout, int ncol,
+                       int ld, int row_lo, int row_hi, const double* gs, double* xs, EigShared& sh,
+                       unsigned& xphase) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t n = a.n;
-  for (int rbase = row_lo; rbase < row_hi; rbase += 8 * RPW) {
-    double acc[RPW][LDM];
+  const int npair = (row_hi - row_lo + 1) / 2;
+  constexpr int W = ET / 32;
+  const int kc = a.kc;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&sh.xbar);
+  for (int pb = 0; pb < npair; pb += W) {
+    const int np = (npair - pb) < W ? (npair - pb) : W;
+    const int wk = W / np;  // warps per pair
+    const int pi = warp / wk, ks = warp % wk;
+    double v[32];  // [row][col] for cols 0..15
+    double ext[2] = {0.0, 0.0};  // col 16
 #pragma unroll
-    for (int rr = 0; rr < RPW; ++rr)
-#pragma unroll
-      for (int j = 0; j < LDM; ++j) acc[rr][j] = 0.0;
+    for (int q = 0; q < 32; ++q) v[q] = 0.0;
+    const int i0 = row_lo + 2 * (pb + pi);
+    const bool act = pi < np;
+    const bool has1 = act && i0 + 1 < row_hi;
+    // the second row of an odd tail re-reads the first; its sums are dropped
+    const double* g0 = gs ? gs + (int64_t)(i0 - row_lo) * n : a.G + (int64_t)i0 * n;
+    const double* g1 = has1 ? g0 + n : g0;
     for (int64_t k0 = 0; k0 < n; k0 += kc) {
       const int kn = (int)((n - k0) < kc ? (n - k0) : kc);
-      __syncthreads();
+      __syncthreads();  // the previous chunk (or matvec) is done with xs
+      if (tid == 0) {
+        // X was written by other CTAs before the grid sync (generic proxy);
+        // order those writes before the bulk copy's (async proxy) reads
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        const unsigned bytes = (unsigned)(((int64_t)kn * ld + 1) / 2 * 16);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                (unsigned)__cvta_generic_to_shared(xs)),
+            "l"(Xin + k0 * ld), "r"(bytes), "r"(bar)
+            : "memory");
+      }
       {
-        const int tot = kn * ld;  // doubles; chunk start k0*ld is even when ld is even or k0 even
-        const double* src = Xin + k0 * ld;
-        if ((((uintptr_t)src) & 15) == 0) {
-          const double2* s2 = reinterpret_cast<const double2*>(src);
-          double2* d2 = reinterpret_cast<double2*>(xs);
-          for (int e = tid; e < tot / 2; e += ET) d2[e] = s2[e];
-          if ((tot & 1) && tid == 0) xs[tot - 1] = src[tot - 1];
-        } else {
-          for (int e = tid; e < tot; e += ET) xs[e] = src[e];
-        }
+        unsigned done = 0;
+        do {
+          asm volatile(
+              "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+              : "=r"(done)
+              : "r"(bar), "r"(xphase)
+              : "memory");
+        } while (!done);
+        xphase ^= 1u;
       }
-      __syncthreads();
+      if (act) {
+        // NC columns are read per row regardless of ncol (xs is padded;
+        // products in columns >= ncol are never written out)
+        const int kb = kn * ks / wk, ke = kn * (ks + 1) / wk;
+        auto body = [&](auto ldg) {
+#pragma unroll 2
+          for (int k = kb + lane; k < ke; k += 32) {
+            const double* x = xs + (int64_t)k * ld;
+            double xv[NC];
 #pragma unroll
-      for (int rr = 0; rr < RPW; ++rr) {
-        const int i = rbase + warp + rr * 8;
-        if (i < row_hi) {
-          const double* grow = a.G + (int64_t)i * n + k0;
-#pragma unroll 4
-          for (int kk = lane; kk < kn; kk += 32) {
-            const double g = __ldg(grow + kk);
-            const double* x = xs + kk * ld;
+            for (int j = 0; j < NC; ++j) xv[j] = x[j];
+            const double ga = ldg(g0 + k0 + k);
+            const double gb = ldg(g1 + k0 + k);
 #pragma unroll
-            for (int j = 0; j < LDM; ++j)
-              if (j < ncol) acc[rr][j] = fma(g, x[j], acc[rr][j]);
+            for (int j = 0; j < NC && j < 16; ++j) {
+              v[j] = fma(ga, xv[j], v[j]);
+              v[16 + j] = fma(gb, xv[j], v[16 + j]);
+            }
+            if (NC > 16) {
+              ext[0] = fma(ga, xv[NC > 16 ? 16 : 0], ext[0]);
+              ext[1] = fma(gb, xv[NC > 16 ? 16 : 0], ext[1]);
+            }
           }
-        }
+        };
+        if (gs) body([](const double* p) { return *p; });
+        else body([](const double* p) { return __ldg(p); });
       }
     }
+    warp_reduce_halving<32>(v, lane);  // lane l: value l = (row l/16, col l%16)
+    if (NC > 16) {
 #pragma unroll
-    for (int rr = 0; rr < RPW; ++rr) {
-      const int i = rbase + warp + rr * 8;
-#pragma unroll
-      for (int j = 0; j < LDM; ++j) {
-        if (j < ncol) {
-          const double v = warp_sum(acc[rr][j]);
-          if (lane == 0 && i < row_hi) Yout[(int64_t)i * ld + j] = v;
-        }
+      for (int o = 16; o > 0; o >>= 1) {
+        ext[0] += __shfl_xor_sync(0xffffffffu, ext[0], o);
+        ext[1] += __shfl_xor_sync(0xffffffffu, ext[1], o);
       }
     }
+    double* red2 = sh.red2;
+    red2[warp * 34 + lane] = v[0];
+    if (lane < 2) red2[warp * 34 + 32 + lane] = ext[lane & 1];
+    __syncthreads();
+    if (act && ks == 0) {
+      double s = 0.0;
+      for (int q = 0; q < wk; ++q) s += red2[(pi * wk + q) * 34 + lane];
+      const int row = i0 + (lane >> 4), col = lane & 15;
+      if (col < ncol && (lane < 16 || has1)) Yout[(int64_t)row * ld + col] = s;
+      if (NC > 16 && ncol > 16 && lane < 2 && (lane == 0 || has1)) {
+        double e = 0.0;
+        for (int q = 0; q < wk; ++q) e += red2[(pi * wk + q) * 34 + 32 + lane];
+        Yout[(int64_t)(i0 + lane) * ld + 16] = e;
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
 }
 
 // partial of value e of this CTA for reduction buffer buf; layout [buf][e][cta]
@@ -127,21 +182,36 @@ __device__ void grid_reduce(const EigArgs& a, cg::grid_group& grid, int buf, int
                             int pw, EigShared& sh) {
   grid.sync();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nc = (int)gridDim.x;
-  for (int e = warp; e < cnt; e += ET / 32) {
-    const double* base = a.part + ((size_t)buf * pw + e) * nc;
-    double s = op ? -1.0 : 0.0;
-#pragma unroll 4
-    for (int c = lane; c < nc; c += 32) {
-      const double v = base[c];
-      s = op ? fmax(s, v) : s + v;
+  const int nc = (int)gridDim.x;  // <= 32 * 5
+  constexpr int VU = 4;            // values per warp per round (all loads in flight)
+  for (int e0 = warp; e0 < cnt; e0 += (ET / 32) * VU) {
+    double s[VU];
+#pragma unroll
+    for (int u = 0; u < VU; ++u) {
+      const int e = e0 + u * (ET / 32);
+      s[u] = op ? -1.0 : 0.0;
+      if (e < cnt) {
+        const double* base = a.part + ((size_t)buf * pw + e) * nc;
+#pragma unroll
+        for (int cc = 0; cc < 5; ++cc) {
+          const int c = lane + 32 * cc;
+          if (c < nc) {
+            const double v = base[c];
+            s[u] = op ? fmax(s[u], v) : s[u] + v;
+          }
+        }
+      }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double t = __shfl_xor_sync(0xffffffffu, s, o);
-      s = op ? fmax(s, t) : s + t;
+    for (int u = 0; u < VU; ++u) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_xor_sync(0xffffffffu, s[u], o);
+        s[u] = op ? fmax(s[u], t) : s[u] + t;
+      }
+      const int e = e0 + u * (ET / 32);
+      if (lane == 0 && e < cnt) sh.red[e] = s[u];
     }
-    if (lane == 0) sh.red[e] = s;
   }
   __syncthreads();
 }
@@ -198,7 +268,10 @@ __device__ void chol_small(int nc, EigShared& sh) {
       __syncwarp();
     }
     ok = __all_sync(0xffffffffu, ok);
-    if (ok) break;
+    if (ok) {
+      if (lane < nc) sh.dinv[lane] = 1.0 / sh.S[lane * BMAX + lane];
+      break;
+    }
     double tr = 0.0;
     for (int k = 0; k < nc; ++k) tr += fabs(sh.red[k * nc - k * (k - 1) / 2]);
     shift = (shift == 0.0) ? 1e-14 * tr : shift * 100.0;
@@ -218,7 +291,7 @@ __device__ void apply_rinv(double* X, int nc, int ld, int row_lo, int row_hi, Ei
 #pragma unroll
         for (int i = 0; i < BMAX; ++i)
           if (i < j) s -= y[i] * sh.S[j * BMAX + i];
-        y[j] = s / sh.S[j * BMAX + j];
+        y[j] = s * sh.dinv[j];
       }
     }
 #pragma unroll
@@ -246,11 +319,11 @@ __device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, int nc
 
 }  // namespace
 
+template <int NC>
 __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ EigShared sh;
-  extern __shared__ __align__(16) double xs_dyn[];
-  const int kc_rows = (int)((XS_BYTES / 8) / (a.b + 1));
+  extern __shared__ __align__(16) double dyn[];
   const int tid = threadIdx.x;
   const int64_t n = a.n;
   const int b = a.b, r = a.r, ld = b + 1, pcol = b;
@@ -260,6 +333,22 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   int buf = 0;
   int matvecs = 0;
   const bool full = (b >= n);  // block = whole space
+  // dynamic shared memory: [the CTA's rows of G when resident][iterate chunk]
+  const double* gs = nullptr;
+  double* xs = dyn + (a.gres ? (((int64_t)a.rows_per_cta * n + 1) & ~int64_t(1)) : 0);
+  if (a.gres) {
+    const int64_t tot = (int64_t)(row_hi - row_lo) * n;
+    const double* src = a.G + (int64_t)row_lo * n;
+    for (int64_t e = tid; e < tot; e += ET) dyn[e] = __ldg(src + e);
+    gs = dyn;
+  }
+  unsigned xphase = 0;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&sh.xbar)),
+                 "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
   // ---- ub: an upper bound of the spectrum ----
   // With the accumulator's structure G = diag(count) - sum E V V^T E^T (a PSD
@@ -318,6 +407,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   long long tacc[6] = {0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
   const bool tme = blockIdx.x == 0 && tid == 0;
+  long long jac_sweeps = 0, jac_cyc = 0, mv_cyc = 0, sync_cyc = 0;
 #define EIG_T(i)                          \
   do {                                    \
     if (tme) {                            \
@@ -338,7 +428,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       double sigma = e / (0.0 - c);
       const double tau = 2.0 / sigma;
       grid.sync();  // X complete
-      matvec(a, X, Z, ld, ld, row_lo, row_hi, xs_dyn, kc_rows);
+      matvec<NC>(a, X, Z, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
       ++matvecs;
       for (int row = row_lo + tid; row < row_hi; row += ET) {
         const int64_t o = (int64_t)row * ld;
@@ -346,8 +436,14 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
         Y[o + pcol] = Z[o + pcol] / ub;
       }
       for (int it = 2; it <= d; ++it) {
+        const long long t0 = clock64();
         grid.sync();  // Y complete
-        matvec(a, Y, Z, ld, ld, row_lo, row_hi, xs_dyn, kc_rows);
+        const long long t1 = clock64();
+        matvec<NC>(a, Y, Z, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
+        if (tme) {
+          sync_cyc += t1 - t0;
+          mv_cyc += clock64() - t1;
+        }
         ++matvecs;
         const double sigma2 = 1.0 / (tau - sigma);
         for (int row = row_lo + tid; row < row_hi; row += ET) {
@@ -369,7 +465,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     }
     // ---- Rayleigh-Ritz ----
     grid.sync();  // X complete
-    matvec(a, X, Z, ld, ld, row_lo, row_hi, xs_dyn, kc_rows);
+    matvec<NC>(a, X, Z, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
     ++matvecs;
     {
       const int P = b * (b + 1) / 2;
@@ -403,7 +499,12 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       __syncthreads();
       EIG_T(2);
       if (tid < 32) {
-        warp_jacobi_eig_abs(sh.H, BMAX, sh.S, BMAX, b, sh.cs, sh.pairs, 60);
+        const long long tj = clock64();
+        const int sw = warp_jacobi_abs(sh.H, BMAX, sh.S, BMAX, b, sh.cs, sh.pairs, 60);
+        if (tme) {
+          jac_sweeps += sw;
+          jac_cyc += clock64() - tj;
+        }
         if (tid == 0) {
           // ascending order: selection sort of eigenpairs
           for (int i = 0; i < b; ++i) sh.theta[i] = sh.H[i * BMAX + i];
@@ -499,6 +600,10 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     a.dstat[1] = ub;
     a.dstat[2] = maxres;
     for (int i = 0; i < 6; ++i) a.dstat[3 + i] = (double)tacc[i];
+    a.dstat[9] = (double)jac_sweeps;
+    a.dstat[10] = (double)jac_cyc;
+    a.dstat[11] = (double)mv_cyc;
+    a.dstat[12] = (double)sync_cyc;
   }
 #undef EIG_T
 }
@@ -530,15 +635,37 @@ int eig_max_grid() {
   int dev = 0, sms = 0, nb = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, XS_BYTES);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eig, ET, XS_BYTES);
+  cudaFuncSetAttribute(k_eig<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eig<17>, ET, DYN_BYTES);
   return sms * (nb > 0 ? nb : 1);
 }
 
-cudaError_t launch_eig(const EigArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_eig(const EigArgs& a0, int grid, cudaStream_t s) {
+  EigArgs a = a0;
+  const int ld = a.b + 1;
+  // the whole iterate in shared memory when it fits, else even-sized chunks;
+  // the CTA's G rows stay resident when there is room next to it
+  const size_t xrow = sizeof(double) * (size_t)ld;
+  const size_t pad = sizeof(double) * 32;
+  const size_t xfull = xrow * (size_t)a.n + pad;
+  const size_t gbytes = sizeof(double) * (((size_t)a.rows_per_cta * (size_t)a.n + 1) & ~(size_t)1);
+  size_t dyn;
+  if (xfull <= (size_t)DYN_BYTES) {
+    a.kc = (int)a.n;
+    a.gres = xfull + gbytes <= (size_t)DYN_BYTES ? 1 : 0;
+    dyn = xfull + (a.gres ? gbytes : 0);
+  } else {
+    a.gres = 0;
+    a.kc = (int)(((DYN_BYTES - pad) / xrow) & ~(size_t)1);
+    dyn = xrow * (size_t)a.kc + pad;
+  }
   void* args[] = {(void*)&a};
-  cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, XS_BYTES);
-  return cudaLaunchCooperativeKernel((void*)k_eig, dim3(grid), dim3(ET), args, XS_BYTES, s);
+  if (a.b + 1 <= 12) {
+    cudaFuncSetAttribute(k_eig<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_BYTES);
+    return cudaLaunchCooperativeKernel((void*)k_eig<12>, dim3(grid), dim3(ET), args, dyn, s);
+  }
+  cudaFuncSetAttribute(k_eig<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_BYTES);
+  return cudaLaunchCooperativeKernel((void*)k_eig<17>, dim3(grid), dim3(ET), args, dyn, s);
 }
 
 void launch_sign_fix(double* V, int64_t n, int r, cudaStream_t s) {

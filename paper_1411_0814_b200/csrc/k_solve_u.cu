@@ -102,46 +102,6 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-// Sum N (power of two) per-lane values over the warp by recursive halving:
-// at each of the first log2(min(N,32)) exchanges a lane keeps one half of its
-// values and receives its partner's copy of that half, so the shuffle count
-// is ~N instead of 5N. On return lane l holds max(1, N/32) totals in v[0..]:
-// value j sits in lane (j / PL) * max(1, 32/N), slot j % PL.
-template <int N>
-__device__ __forceinline__ void warp_reduce_halving(double (&v)[N], int lane) {
-  constexpr int STEPS = N >= 32 ? 5 : (N >= 16 ? 4 : (N >= 8 ? 3 : (N >= 4 ? 2 : (N >= 2 ? 1 : 0))));
-#pragma unroll
-  for (int st = 0; st < STEPS; ++st) {
-    const int o = 16 >> st;
-    const int K = N >> st;  // values still held
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < N / 2; ++i) {
-      if (i < K / 2) {
-        const double mine = up ? v[i + K / 2] : v[i];
-        const double other = up ? v[i] : v[i + K / 2];
-        v[i] = mine + __shfl_xor_sync(0xffffffffu, other, o);
-      }
-    }
-  }
-  // remaining lane bits: plain butterfly on the single held value
-  if (N < 32) {
-#pragma unroll
-    for (int o = 16 >> STEPS; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
-  }
-}
-
-template <int N>
-__device__ __forceinline__ double warp_total(const double (&v)[N], int j) {
-  constexpr int PL = N > 32 ? N / 32 : 1;
-  constexpr int LPV = N < 32 ? 32 / N : 1;
-  double x = v[0];
-#pragma unroll
-  for (int s = 1; s < PL; ++s)
-    if (j % PL == s) x = v[s];
-  return __shfl_sync(0xffffffffu, x, (j / PL) * LPV);
-}
-
 __host__ __device__ constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
 }  // namespace

@@ -478,9 +478,11 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   const int rows_per_cta = (int)ceil_div(n, grid);
   grid = (int)ceil_div(n, rows_per_cta);
   const int pw = rsmk::eig_part_width(b);
-  c->eX.ensure(sizeof(double) * n * ld);
-  c->eY.ensure(sizeof(double) * n * ld);
-  c->eZ.ensure(sizeof(double) * n * ld);
+  // + 32 doubles: the matvec reads a fixed 12/17 columns per row, running
+  // past the last row by up to 16 (those products are discarded)
+  c->eX.ensure(sizeof(double) * (n * ld + 32));
+  c->eY.ensure(sizeof(double) * (n * ld + 32));
+  c->eZ.ensure(sizeof(double) * (n * ld + 32));
   c->ePart.ensure(sizeof(double) * 2 * (size_t)grid * pw);
   c->eW.ensure(sizeof(double) * 32);
   c->eI.ensure(sizeof(int) * 8);
@@ -506,7 +508,7 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   double dstat[16];
   ck(cudaMemcpyAsync(w, c->eW.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaMemcpyAsync(istat, c->eI.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
-  ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 9, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 13, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "solve_v");
   ck(cudaGetLastError(), "eig kernels");
   c->solver_stats[0] = istat[3];
@@ -517,6 +519,9 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   c->solver_stats[5] = b;
   c->solver_stats[6] = grid;
   for (int i = 0; i < 6; ++i) c->solver_stats[7 + i] = dstat[3 + i];  // phase clocks (cycles)
+  c->solver_stats[13] = dstat[9];   // Rayleigh-Ritz Jacobi sweeps (total)
+  c->solver_stats[14] = dstat[10];  // and their cycles
+  c->solver_stats[15] = dstat[11];  // filter matvec cycles (CTA 0)
   if (istat[0] != 0) fail(RSM_ERR_INTERNAL, "symmetric eigensolver failed to converge");
   c->Vhat_n = n;
   c->Vhat_r = r;
@@ -916,7 +921,7 @@ int rsm_ctx_stage_ms(rsm_ctx* c, double* ms, int cap) {
 int64_t rsm_ctx_launch_count(rsm_ctx* c) { return c ? c->launches : 0; }
 
 int rsm_ctx_solver_stats(rsm_ctx* c, double* out, int cap) {
-  const int k = std::min(cap, 13);
+  const int k = std::min(cap, 16);
   for (int i = 0; i < k; ++i) out[i] = c->solver_stats[i];
   return k;
 }

@@ -55,6 +55,46 @@ __device__ __forceinline__ int warp_sum_int(int v) {
   return v;
 }
 
+// Sum N (power of two) per-lane values over the warp by recursive halving:
+// at each of the first log2(min(N,32)) exchanges a lane keeps one half of its
+// values and receives its partner's copy of that half, so the shuffle count
+// is ~N instead of 5N. On return lane l holds max(1, N/32) totals in v[0..]:
+// value j sits in lane (j / PL) * max(1, 32/N), slot j % PL.
+template <int N>
+__device__ __forceinline__ void warp_reduce_halving(double (&v)[N], int lane) {
+  constexpr int STEPS = N >= 32 ? 5 : (N >= 16 ? 4 : (N >= 8 ? 3 : (N >= 4 ? 2 : (N >= 2 ? 1 : 0))));
+#pragma unroll
+  for (int st = 0; st < STEPS; ++st) {
+    const int o = 16 >> st;
+    const int K = N >> st;  // values still held
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      if (i < K / 2) {
+        const double mine = up ? v[i + K / 2] : v[i];
+        const double other = up ? v[i] : v[i + K / 2];
+        v[i] = mine + __shfl_xor_sync(0xffffffffu, other, o);
+      }
+    }
+  }
+  // remaining lane bits: plain butterfly on the single held value
+  if (N < 32) {
+#pragma unroll
+    for (int o = 16 >> STEPS; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ double warp_total(const double (&v)[N], int j) {
+  constexpr int PL = N > 32 ? N / 32 : 1;
+  constexpr int LPV = N < 32 ? 32 / N : 1;
+  double x = v[0];
+#pragma unroll
+  for (int s = 1; s < PL; ++s)
+    if (j % PL == s) x = v[s];
+  return __shfl_sync(0xffffffffu, x, (j / PL) * LPV);
+}
+
 // Warp-parallel cyclic Jacobi on a symmetric K x K matrix A (smem,
 // row-major, leading dim lda), K <= 32. Uses the round-robin (tournament)
 // ordering: each step rotates floor(Kp/2) disjoint pairs at once, one lane
@@ -155,7 +195,7 @@ __device__ inline int warp_jacobi_eig(double* A, int lda, double* V, int ldv, in
   return sweep;
 }
 
-// Jacobi with the absolute off-diagonal threshold eps * ||A||_F (LAPACK-level
+// Jacobi with the absolute off-diagonal threshold 16 eps * ||A||_F (LAPACK-level
 // eigenvalue accuracy); used where small eigenvalues only need absolute
 // accuracy (the stage-4 Rayleigh-Ritz problem). V is initialised to I.
 __device__ inline int warp_jacobi_eig_abs(double* A, int lda, double* V, int ldv, int K, double* cs,
@@ -167,8 +207,115 @@ __device__ inline int warp_jacobi_eig_abs(double* A, int lda, double* V, int ldv
     f += v * v;
   }
   f = warp_sum(f);
-  const double thr = 2.220446049250313e-16 * sqrt(f);
+  // 16 eps: rounding keeps re-creating off-diagonals of ~eps ||A||, so a
+  // threshold at exactly eps ||A|| can rotate until max_sweeps
+  const double thr = 16.0 * 2.220446049250313e-16 * sqrt(f);
   return warp_jacobi_eig(A, lda, V, ldv, K, cs, pairs, 0.0, max_sweeps, true, thr > 0.0 ? thr : 1e-300);
+}
+
+// Compile-time-K variant of the round-robin warp Jacobi with the absolute
+// threshold 16 eps ||A||_F (see warp_jacobi_eig_abs); V is set to I. Kept out
+// of line so a large caller's register pressure cannot spill its loop state.
+template <int K>
+__device__ __noinline__ int warp_jacobi_abs_k(double* A, int lda, double* V, int ldv, double* cs, int* pairs,
+                                              int max_sweeps) {
+  constexpr int Kp = (K + 1) & ~1;
+  constexpr int NPAIR = Kp / 2;
+  const int lane = threadIdx.x & 31;
+  double f = 0.0;
+#pragma unroll
+  for (int e = lane; e < K * K; e += 32) {
+    const double v = A[(e / K) * lda + (e % K)];
+    f += v * v;
+  }
+  f = warp_sum(f);
+  const double thr = fmax(16.0 * 2.220446049250313e-16 * sqrt(f), 1e-300);
+#pragma unroll
+  for (int e = lane; e < K * K; e += 32) V[(e / K) * ldv + (e % K)] = (e / K == e % K) ? 1.0 : 0.0;
+  __syncwarp();
+  if (K < 2) return 0;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    int big = 0;
+#pragma unroll
+    for (int e = lane; e < K * K; e += 32) {
+      const int p = e / K, q = e % K;
+      if (p < q && fabs(A[p * lda + q]) > thr) big = 1;
+    }
+    if (!__any_sync(0xffffffffu, big)) break;
+#pragma unroll 1
+    for (int step = 0; step < Kp - 1; ++step) {
+      if (lane < NPAIR) {
+        const int a = (lane == 0) ? 0 : ((lane - 1 + step) % (Kp - 1)) + 1;
+        const int b = ((Kp - 2 - lane + step) % (Kp - 1)) + 1;
+        const int p = a < b ? a : b, q = a < b ? b : a;
+        double c = 1.0, sn = 0.0;
+        if (q < K) {
+          const double apq = A[p * lda + q];
+          if (fabs(apq) > thr) {
+            const double zeta = (A[q * lda + q] - A[p * lda + p]) / (2.0 * apq);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            c = rsqrt(1.0 + t * t);
+            sn = c * t;
+          }
+        }
+        pairs[2 * lane] = p;
+        pairs[2 * lane + 1] = q;
+        cs[2 * lane] = c;
+        cs[2 * lane + 1] = sn;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int e = lane; e < NPAIR * K; e += 32) {
+        const int pr = e / K, row = e % K;
+        const int p = pairs[2 * pr], q = pairs[2 * pr + 1];
+        const double c = cs[2 * pr], sn = cs[2 * pr + 1];
+        if (q < K && sn != 0.0) {
+          const double x = A[row * lda + p], y = A[row * lda + q];
+          A[row * lda + p] = c * x - sn * y;
+          A[row * lda + q] = sn * x + c * y;
+          const double vx = V[row * ldv + p], vy = V[row * ldv + q];
+          V[row * ldv + p] = c * vx - sn * vy;
+          V[row * ldv + q] = sn * vx + c * vy;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int e = lane; e < NPAIR * K; e += 32) {
+        const int pr = e / K, col = e % K;
+        const int p = pairs[2 * pr], q = pairs[2 * pr + 1];
+        const double c = cs[2 * pr], sn = cs[2 * pr + 1];
+        if (q < K && sn != 0.0) {
+          const double x = A[p * lda + col], y = A[q * lda + col];
+          A[p * lda + col] = c * x - sn * y;
+          A[q * lda + col] = sn * x + c * y;
+        }
+      }
+      __syncwarp();
+      if (lane < NPAIR) {
+        const int p = pairs[2 * lane], q = pairs[2 * lane + 1];
+        if (q < K && cs[2 * lane + 1] != 0.0) {
+          A[p * lda + q] = 0.0;
+          A[q * lda + p] = 0.0;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  return sweep;
+}
+
+// dispatch on the runtime size (K <= KMAX)
+__device__ __forceinline__ int warp_jacobi_abs(double* A, int lda, double* V, int ldv, int K, double* cs,
+                                               int* pairs, int max_sweeps) {
+  switch (K) {
+#define RSM_JK(k) \
+  case k: return warp_jacobi_abs_k<k>(A, lda, V, ldv, cs, pairs, max_sweeps);
+    RSM_JK(1) RSM_JK(2) RSM_JK(3) RSM_JK(4) RSM_JK(5) RSM_JK(6) RSM_JK(7) RSM_JK(8)
+    RSM_JK(9) RSM_JK(10) RSM_JK(11) RSM_JK(12) RSM_JK(13) RSM_JK(14) RSM_JK(15) RSM_JK(16)
+#undef RSM_JK
+    default: return warp_jacobi_eig_abs(A, lda, V, ldv, K, cs, pairs, max_sweeps);
+  }
 }
 
 }  // namespace rsmd

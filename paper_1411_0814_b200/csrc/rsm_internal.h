@@ -59,6 +59,8 @@ struct EigArgs {
   double tol;       // gram_rank_tol
   int rows_per_cta;
   int rpw;          // rows per warp
+  int gres;         // set by launch_eig: G rows resident in shared memory
+  int kc;           // set by launch_eig: iterate rows staged per bulk copy
   double* X;        // n x ld  (3 buffers)
   double* Y;
   double* Z;

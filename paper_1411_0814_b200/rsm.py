@@ -377,7 +377,7 @@ class Context:
         buf = (C.c_double * 16)()
         k = lib().rsm_ctx_solver_stats(self.h, C.cast(buf, C.c_void_p), 16)
         keys = ["outer", "matvecs", "lambda_max", "ub", "max_residual", "block", "grid", "cyc_filter",
-                "cyc_cholqr", "cyc_rr", "cyc_eig", "cyc_rotate", "cyc_setup"]
+                "cyc_cholqr", "cyc_rr", "cyc_eig", "cyc_rotate", "cyc_setup", "jac_sweeps", "cyc_jacobi", "cyc_matvec"]
         return dict(zip(keys, buf[:k]))
 
 
