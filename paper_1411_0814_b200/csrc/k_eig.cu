@@ -65,9 +65,9 @@ __device__ __forceinline__ int pw_of(int b) { return (b + 1) * (b + 2) / 2 + 2 *
 // G rows in shared memory (nullptr: read them from global / L2); X is read
 // with coherent loads (it was written by other CTAs before the grid sync).
 template <int NC>
-__device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double* __restrict__ Yout, int ncol,
-                       int ld, int row_lo, int row_hi, const double* gs, double* xs, EigShared& sh,
-                       unsigned& xphase) {
+__device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double* __restrict__ Yout,
+                       double* __restrict__ Yown, int ncol, int ld, int row_lo, int row_hi, const double* gs,
+                       double* xs, EigShared& sh, unsigned& xphase) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t n = a.n;
   const int npair = (row_hi - row_lo + 1) / 2;
@@ -158,11 +158,15 @@ __device__ void matvec(const EigArgs& a, const double* __restrict__ Xin, double*
       double s = 0.0;
       for (int q = 0; q < wk; ++q) s += red2[(pi * wk + q) * 34 + lane];
       const int row = i0 + (lane >> 4), col = lane & 15;
-      if (col < ncol && (lane < 16 || has1)) Yout[(int64_t)row * ld + col] = s;
+      if (col < ncol && (lane < 16 || has1)) {
+        Yout[(int64_t)row * ld + col] = s;
+        Yown[(row - row_lo) * ld + col] = s;
+      }
       if (NC > 16 && ncol > 16 && lane < 2 && (lane == 0 || has1)) {
         double e = 0.0;
         for (int q = 0; q < wk; ++q) e += red2[(pi * wk + q) * 34 + 32 + lane];
         Yout[(int64_t)(i0 + lane) * ld + 16] = e;
+        Yown[(i0 + lane - row_lo) * ld + 16] = e;
       }
     }
     __syncthreads();
@@ -218,8 +222,8 @@ __device__ void grid_reduce(const EigArgs& a, cg::grid_group& grid, int buf, int
 
 // local Gram partial of columns [0, nc) of X over own rows -> part[buf]; plus
 // optional squared norm of column pc (pc < 0: none) at index nc*(nc+1)/2
-__device__ void gram_partial(const EigArgs& a, const double* X, int nc, int ld, int pc,
-                             int row_lo, int row_hi, int buf, int pw) {
+__device__ void gram_partial(const EigArgs& a, const double* Xo, int nc, int ld, int pc, int nr, int buf,
+                             int pw) {
   const int P = nc * (nc + 1) / 2;
   for (int p = threadIdx.x; p < P + 1; p += ET) {
     int i = 0, j = 0;
@@ -232,7 +236,7 @@ __device__ void gram_partial(const EigArgs& a, const double* X, int nc, int ld, 
       i = j = pc;
     }
     double s = 0.0;
-    for (int row = row_lo; row < row_hi; ++row) s += X[(int64_t)row * ld + i] * X[(int64_t)row * ld + j];
+    for (int lr = 0; lr < nr; ++lr) s += Xo[lr * ld + i] * Xo[lr * ld + j];
     *pslot(a, buf, pw, p) = s;
   }
 }
@@ -279,11 +283,12 @@ __device__ void chol_small(int nc, EigShared& sh) {
   __syncwarp();
 }
 
-// X(own rows) <- X R^{-1}, R = L^T with L in sh.S
-__device__ void apply_rinv(double* X, int nc, int ld, int row_lo, int row_hi, EigShared& sh) {
-  for (int row = row_lo + threadIdx.x; row < row_hi; row += ET) {
+// X(own rows) <- X R^{-1}, R = L^T with L in sh.S (smem copy and global)
+__device__ void apply_rinv(double* X, double* Xo, int nc, int ld, int row_lo, int nr, EigShared& sh) {
+  for (int lr = threadIdx.x; lr < nr; lr += ET) {
     double y[BMAX];
-    double* x = X + (int64_t)row * ld;
+    double* x = Xo + lr * ld;
+    double* xg = X + (int64_t)(row_lo + lr) * ld;
 #pragma unroll
     for (int j = 0; j < BMAX; ++j) {
       if (j < nc) {
@@ -296,23 +301,30 @@ __device__ void apply_rinv(double* X, int nc, int ld, int row_lo, int row_hi, Ei
     }
 #pragma unroll
     for (int j = 0; j < BMAX; ++j)
-      if (j < nc) x[j] = y[j];
+      if (j < nc) {
+        x[j] = y[j];
+        xg[j] = y[j];
+      }
   }
 }
 
-__device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, int nc, int ld, int pc,
-                       int row_lo, int row_hi, int& buf, int pw, EigShared& sh) {
-  gram_partial(a, X, nc, ld, pc, row_lo, row_hi, buf, pw);
+__device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, double* Xo, int nc, int ld, int pc,
+                       int row_lo, int nr, int& buf, int pw, EigShared& sh) {
+  gram_partial(a, Xo, nc, ld, pc, nr, buf, pw);
   const int P = nc * (nc + 1) / 2;
   grid_reduce(a, grid, buf, P + 1, 0, pw, sh);
   buf ^= 1;
   chol_small(nc, sh);
   __syncthreads();
-  apply_rinv(X, nc, ld, row_lo, row_hi, sh);
+  apply_rinv(X, Xo, nc, ld, row_lo, nr, sh);
   if (pc >= 0) {
     const double nrm = sqrt(sh.red[P]);
     const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-    for (int row = row_lo + threadIdx.x; row < row_hi; row += ET) X[(int64_t)row * ld + pc] *= inv;
+    for (int lr = threadIdx.x; lr < nr; lr += ET) {
+      const double v = Xo[lr * ld + pc] * inv;
+      Xo[lr * ld + pc] = v;
+      X[(int64_t)(row_lo + lr) * ld + pc] = v;
+    }
   }
   __syncthreads();
 }
@@ -333,14 +345,21 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   int buf = 0;
   int matvecs = 0;
   const bool full = (b >= n);  // block = whole space
-  // dynamic shared memory: [the CTA's rows of G when resident][iterate chunk]
+  // dynamic shared memory: [own rows of X, Y, Z][G rows when resident][iterate chunk]
+  const int nr = row_hi - row_lo;
+  const int own = ((a.rows_per_cta * ld) + 1) & ~1;
+  double* Xo = dyn;
+  double* Yo = dyn + own;
+  double* Zo = dyn + 2 * own;
+  double* Wo = dyn + 3 * own;  // scratch
+  double* gdyn = dyn + 4 * own;
   const double* gs = nullptr;
-  double* xs = dyn + (a.gres ? (((int64_t)a.rows_per_cta * n + 1) & ~int64_t(1)) : 0);
+  double* xs = gdyn + (a.gres ? (((int64_t)a.rows_per_cta * n + 1) & ~int64_t(1)) : 0);
   if (a.gres) {
     const int64_t tot = (int64_t)(row_hi - row_lo) * n;
     const double* src = a.G + (int64_t)row_lo * n;
-    for (int64_t e = tid; e < tot; e += ET) dyn[e] = __ldg(src + e);
-    gs = dyn;
+    for (int64_t e = tid; e < tot; e += ET) gdyn[e] = __ldg(src + e);
+    gs = gdyn;
   }
   unsigned xphase = 0;
   if (tid == 0) {
@@ -385,18 +404,19 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   double* X = a.X;
   double* Y = a.Y;
   double* Z = a.Z;
-  for (int row = row_lo + tid; row < row_hi; row += ET)
-    for (int j = 0; j < ld; ++j) {
-      double v;
-      if (full) v = (j == row) ? 1.0 : 0.0;
-      else v = (double)(mix(0x51ed270b27c3e1a5ull ^ ((uint64_t)row * 131 + j)) >> 11) * 0x1.0p-53 - 0.5;
-      if (j == pcol) v = 1.0 + 0.01 * ((double)(mix(0xabcdefull + row) >> 11) * 0x1.0p-53);
-      X[(int64_t)row * ld + j] = v;
-    }
+  for (int e = tid; e < nr * ld; e += ET) {
+    const int lr = e / ld, j = e % ld, row = row_lo + lr;
+    double v;
+    if (full) v = (j == row) ? 1.0 : 0.0;
+    else v = (double)(mix(0x51ed270b27c3e1a5ull ^ ((uint64_t)row * 131 + j)) >> 11) * 0x1.0p-53 - 0.5;
+    if (j == pcol) v = 1.0 + 0.01 * ((double)(mix(0xabcdefull + row) >> 11) * 0x1.0p-53);
+    X[(int64_t)row * ld + j] = v;
+    Xo[e] = v;
+  }
   __syncthreads();
   if (!full) {
-    cholqr(a, grid, X, b, ld, pcol, row_lo, row_hi, buf, pw, sh);
-    cholqr(a, grid, X, b, ld, -1, row_lo, row_hi, buf, pw, sh);
+    cholqr(a, grid, X, Xo, b, ld, pcol, row_lo, nr, buf, pw, sh);
+    cholqr(a, grid, X, Xo, b, ld, -1, row_lo, nr, buf, pw, sh);
   }
 
   double acut = 0.5 * ub;
@@ -428,44 +448,47 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       double sigma = e / (0.0 - c);
       const double tau = 2.0 / sigma;
       grid.sync();  // X complete
-      matvec<NC>(a, X, Z, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
+      matvec<NC>(a, X, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
       ++matvecs;
-      for (int row = row_lo + tid; row < row_hi; row += ET) {
-        const int64_t o = (int64_t)row * ld;
-        for (int j = 0; j < b; ++j) Y[o + j] = (Z[o + j] - c * X[o + j]) * (sigma / e);
-        Y[o + pcol] = Z[o + pcol] / ub;
+      for (int q = tid; q < nr * ld; q += ET) {
+        const int j = q % ld;
+        const double y = (j == pcol) ? Zo[q] / ub : (Zo[q] - c * Xo[q]) * (sigma / e);
+        Yo[q] = y;
+        Y[(int64_t)row_lo * ld + q] = y;
       }
       for (int it = 2; it <= d; ++it) {
         const long long t0 = clock64();
         grid.sync();  // Y complete
         const long long t1 = clock64();
-        matvec<NC>(a, Y, Z, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
+        matvec<NC>(a, Y, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
         if (tme) {
           sync_cyc += t1 - t0;
           mv_cyc += clock64() - t1;
         }
         ++matvecs;
         const double sigma2 = 1.0 / (tau - sigma);
-        for (int row = row_lo + tid; row < row_hi; row += ET) {
-          const int64_t o = (int64_t)row * ld;
-          for (int j = 0; j < b; ++j)
-            Z[o + j] = (Z[o + j] - c * Y[o + j]) * (2.0 * sigma2 / e) - sigma * sigma2 * X[o + j];
-          Z[o + pcol] = Z[o + pcol] / ub;
+        for (int q = tid; q < nr * ld; q += ET) {
+          const int j = q % ld;
+          const double z = (j == pcol) ? Zo[q] / ub
+                                       : (Zo[q] - c * Yo[q]) * (2.0 * sigma2 / e) - sigma * sigma2 * Xo[q];
+          Zo[q] = z;
+          Z[(int64_t)row_lo * ld + q] = z;
         }
         double* t = X; X = Y; Y = Z; Z = t;
+        t = Xo; Xo = Yo; Yo = Zo; Zo = t;
         sigma = sigma2;
       }
       // filtered block is in Y
-      { double* t = X; X = Y; Y = t; }
+      { double* t = X; X = Y; Y = t; t = Xo; Xo = Yo; Yo = t; }
       __syncthreads();
       EIG_T(0);
-      cholqr(a, grid, X, b, ld, pcol, row_lo, row_hi, buf, pw, sh);
-      cholqr(a, grid, X, b, ld, -1, row_lo, row_hi, buf, pw, sh);
+      cholqr(a, grid, X, Xo, b, ld, pcol, row_lo, nr, buf, pw, sh);
+      cholqr(a, grid, X, Xo, b, ld, -1, row_lo, nr, buf, pw, sh);
       EIG_T(1);
     }
     // ---- Rayleigh-Ritz ----
     grid.sync();  // X complete
-    matvec<NC>(a, X, Z, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
+    matvec<NC>(a, X, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
     ++matvecs;
     {
       const int P = b * (b + 1) / 2;
@@ -475,14 +498,11 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
           int i = 0, rem = p;
           while (rem >= b - i) { rem -= b - i; ++i; }
           const int j = i + rem;
-          for (int row = row_lo; row < row_hi; ++row)
-            s += X[(int64_t)row * ld + i] * Z[(int64_t)row * ld + j];
+          for (int lr = 0; lr < nr; ++lr) s += Xo[lr * ld + i] * Zo[lr * ld + j];
         } else if (p == P) {
-          for (int row = row_lo; row < row_hi; ++row)
-            s += X[(int64_t)row * ld + pcol] * Z[(int64_t)row * ld + pcol];
+          for (int lr = 0; lr < nr; ++lr) s += Xo[lr * ld + pcol] * Zo[lr * ld + pcol];
         } else {
-          for (int row = row_lo; row < row_hi; ++row)
-            s += X[(int64_t)row * ld + pcol] * X[(int64_t)row * ld + pcol];
+          for (int lr = 0; lr < nr; ++lr) s += Xo[lr * ld + pcol] * Xo[lr * ld + pcol];
         }
         *pslot(a, buf, pw, p) = s;
       }
@@ -526,37 +546,32 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     EIG_T(3);
     // X <- X S, Z <- Z S (own rows); residual partials
     {
-      for (int row = row_lo + tid; row < row_hi; row += ET) {
-        double xr[BMAX], zr[BMAX];
-        const int64_t o = (int64_t)row * ld;
-#pragma unroll
-        for (int j = 0; j < BMAX; ++j) {
-          xr[j] = (j < b) ? X[o + j] : 0.0;
-          zr[j] = (j < b) ? Z[o + j] : 0.0;
+      // X <- X S (own rows); the rotated Z only enters the residuals
+      // ||Z S_j - theta_j X S_j||^2, so it is not stored. New X values and the
+      // squared residual terms go to scratch first (X is still being read).
+      for (int q = tid; q < nr * b; q += ET) {
+        const int lr = q / b, j = q % b;
+        double sx = 0.0, sz = 0.0;
+        for (int i = 0; i < b; ++i) {
+          const double sij = sh.S[i * BMAX + j];
+          sx = fma(Xo[lr * ld + i], sij, sx);
+          sz = fma(Zo[lr * ld + i], sij, sz);
         }
-#pragma unroll
-        for (int j = 0; j < BMAX; ++j) {
-          if (j < b) {
-            double sx = 0.0, sz = 0.0;
-#pragma unroll
-            for (int i = 0; i < BMAX; ++i)
-              if (i < b) {
-                sx += xr[i] * sh.S[i * BMAX + j];
-                sz += zr[i] * sh.S[i * BMAX + j];
-              }
-            X[o + j] = sx;
-            Z[o + j] = sz;
-          }
-        }
+        const double d = sz - sh.theta[j] * sx;
+        Yo[lr * ld + j] = sx;
+        Wo[lr * ld + j] = d * d;
       }
       __syncthreads();
+      for (int q = tid; q < nr * b; q += ET) {
+        const int lr = q / b, j = q % b;
+        const double v = Yo[lr * ld + j];
+        Xo[lr * ld + j] = v;
+        X[(int64_t)(row_lo + lr) * ld + j] = v;
+      }
       for (int j = tid; j < b; j += ET) {
-        double s = 0.0;
-        for (int row = row_lo; row < row_hi; ++row) {
-          const double d = Z[(int64_t)row * ld + j] - sh.theta[j] * X[(int64_t)row * ld + j];
-          s += d * d;
-        }
-        *pslot(a, buf, pw, j) = s;
+        double s2 = 0.0;
+        for (int lr = 0; lr < nr; ++lr) s2 += Wo[lr * ld + j];
+        *pslot(a, buf, pw, j) = s2;
       }
       grid_reduce(a, grid, buf, b, 0, pw, sh);
       buf ^= 1;
@@ -589,8 +604,10 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   }
   if (status != 0 && maxres <= 1e-9 * ub) status = 0;  // converged to a looser bound
   // ---- outputs ----
-  for (int row = row_lo + tid; row < row_hi; row += ET)
-    for (int j = 0; j < r; ++j) a.V[(int64_t)row * r + j] = X[(int64_t)row * ld + j];
+  for (int q = tid; q < nr * r; q += ET) {
+    const int lr = q / r, j = q % r;
+    a.V[(int64_t)(row_lo + lr) * r + j] = Xo[lr * ld + j];
+  }
   if (blockIdx.x == 0 && tid == 0) {
     for (int j = 0; j < b; ++j) a.w[j] = sh.theta[j];
     a.istat[0] = status;
@@ -646,7 +663,8 @@ cudaError_t launch_eig(const EigArgs& a0, int grid, cudaStream_t s) {
   // the whole iterate in shared memory when it fits, else even-sized chunks;
   // the CTA's G rows stay resident when there is room next to it
   const size_t xrow = sizeof(double) * (size_t)ld;
-  const size_t pad = sizeof(double) * 32;
+  const size_t own = sizeof(double) * 4 * ((((size_t)a.rows_per_cta * ld) + 1) & ~(size_t)1);
+  const size_t pad = sizeof(double) * 32 + own;  // own-row buffers ride along with the padding
   const size_t xfull = xrow * (size_t)a.n + pad;
   const size_t gbytes = sizeof(double) * (((size_t)a.rows_per_cta * (size_t)a.n + 1) & ~(size_t)1);
   size_t dyn;

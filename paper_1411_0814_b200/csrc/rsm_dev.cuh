@@ -305,12 +305,130 @@ __device__ __noinline__ int warp_jacobi_abs_k(double* A, int lda, double* V, int
   return sweep;
 }
 
+// circle method on Kp (even) slots: slot l holds round-robin position
+// pos(l) (pairs are positions (i, Kp-1-i) = slots (2i, 2i+1)); position 0
+// stays and the others advance by one per step. circle_src(l) is the slot
+// whose content moves into slot l.
+__host__ __device__ constexpr int circle_pos(int l, int Kp) { return (l & 1) ? (Kp - 1 - (l >> 1)) : (l >> 1); }
+__host__ __device__ constexpr int circle_slot(int p, int Kp) {
+  return (p <= (Kp - 1) / 2) ? 2 * p : 2 * (Kp - 1 - p) + 1;
+}
+__host__ __device__ constexpr int circle_src(int l, int Kp) {
+  return circle_slot(circle_pos(l, Kp) == 0 ? 0 : (circle_pos(l, Kp) == 1 ? Kp - 1 : circle_pos(l, Kp) - 1), Kp);
+}
+
+// Register-resident parallel Jacobi (circle-method ordering, Brent-Luk
+// style) for the symmetric K x K matrix A (smem, lda), K <= 16, one warp.
+// Lane l holds slot l's column of A (rows in slot order) and of V (rows in
+// the original order). Each step rotates the slot pairs (2i, 2i+1) at once:
+// partners exchange columns by shuffles, every lane applies all pairs' row
+// rotations to its column, and a fixed permutation then moves indices between
+// slots (columns by shuffle, rows by a compile-time register renaming) so
+// every index pair meets once per sweep. Threshold as warp_jacobi_eig_abs.
+// On return A's diagonal holds the eigenvalues and V's columns the matching
+// eigenvectors (in some order). Returns the sweep count.
+template <int K>
+__device__ __noinline__ int warp_jacobi_reg(double* A, int lda, double* V, int ldv, int max_sweeps) {
+  constexpr int Kp = (K + 1) & ~1;
+  const int lane = threadIdx.x & 31;
+  const bool live = lane < Kp;
+  double a[Kp], v[Kp];
+#pragma unroll
+  for (int r = 0; r < Kp; ++r) {
+    a[r] = (live && lane < K && r < K) ? A[r * lda + lane] : 0.0;
+    v[r] = (r == lane) ? 1.0 : 0.0;
+  }
+  int idx = lane;  // original index held by this slot
+  // circle method: slot l holds round-robin position pos(l); pairs are the
+  // positions (i, Kp-1-i) = slots (2i, 2i+1); position 0 stays, the others
+  // advance by one each step. src(l) = slot whose content moves into slot l.
+  const int src = live ? circle_src(lane, Kp) : lane;
+  double f = 0.0;
+#pragma unroll
+  for (int r = 0; r < Kp; ++r) f += a[r] * a[r];
+  f = warp_sum(f);
+  const double thr = fmax(16.0 * 2.220446049250313e-16 * sqrt(f), 1e-300);
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    double mo = 0.0;
+#pragma unroll
+    for (int r = 0; r < Kp; ++r)
+      if (r != lane) mo = fmax(mo, fabs(a[r]));
+    if (!__any_sync(0xffffffffu, live && mo > thr)) break;
+#pragma unroll 1
+    for (int step = 0; step < Kp - 1; ++step) {
+      // this slot's diagonal and its pair's off-diagonal entry
+      double d = 0.0, off = 0.0;
+#pragma unroll
+      for (int r = 0; r < Kp; ++r) {
+        d = (r == lane) ? a[r] : d;
+        off = (r == (lane ^ 1)) ? a[r] : off;
+      }
+      const double dp = __shfl_xor_sync(0xffffffffu, d, 1);
+      const bool isp = (lane & 1) == 0;
+      const double app = isp ? d : dp, aqq = isp ? dp : d;
+      double c = 1.0, sn = 0.0;
+      if (live && fabs(off) > thr) {
+        const double zeta = (aqq - app) / (2.0 * off);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        c = rsqrt(1.0 + t * t);
+        sn = c * t;
+      }
+      // columns: A <- A J, V <- V J
+#pragma unroll
+      for (int r = 0; r < Kp; ++r) {
+        const double oa = __shfl_xor_sync(0xffffffffu, a[r], 1);
+        const double ov = __shfl_xor_sync(0xffffffffu, v[r], 1);
+        a[r] = isp ? fma(c, a[r], -sn * oa) : fma(sn, oa, c * a[r]);
+        v[r] = isp ? fma(c, v[r], -sn * ov) : fma(sn, ov, c * v[r]);
+      }
+      // rows: A <- J^T A with every pair's rotation
+#pragma unroll
+      for (int i = 0; i < Kp / 2; ++i) {
+        const double ci = __shfl_sync(0xffffffffu, c, 2 * i);
+        const double si = __shfl_sync(0xffffffffu, sn, 2 * i);
+        const double x = a[2 * i], y = a[2 * i + 1];
+        a[2 * i] = fma(ci, x, -si * y);
+        a[2 * i + 1] = fma(si, x, ci * y);
+      }
+      // the rotated pair's off-diagonal is zero by construction
+#pragma unroll
+      for (int r = 0; r < Kp; ++r) a[r] = (r == (lane ^ 1) && sn != 0.0) ? 0.0 : a[r];
+      // advance the circle: columns move between slots, rows are renamed
+      double t2[Kp];
+#pragma unroll
+      for (int r = 0; r < Kp; ++r) {
+        t2[r] = __shfl_sync(0xffffffffu, a[r], src);
+        v[r] = __shfl_sync(0xffffffffu, v[r], src);
+      }
+#pragma unroll
+      for (int r = 0; r < Kp; ++r) a[r] = t2[circle_src(r, Kp)];
+      idx = __shfl_sync(0xffffffffu, idx, src);
+    }
+  }
+  __syncwarp();
+  // write back: eigenvalue of slot l on A's diagonal, its vector as V's column
+  // (slots holding the padding index are skipped)
+  const unsigned dmask = __ballot_sync(0xffffffffu, live && idx >= K);
+  if (live && idx < K) {
+    const int col = lane - __popc(dmask & ((1u << lane) - 1u));
+    double d = 0.0;
+#pragma unroll
+    for (int r = 0; r < Kp; ++r) d = (r == lane) ? a[r] : d;
+    A[col * lda + col] = d;
+#pragma unroll
+    for (int r = 0; r < K; ++r) V[r * ldv + col] = v[r];
+  }
+  __syncwarp();
+  return sweep;
+}
+
 // dispatch on the runtime size (K <= KMAX)
 __device__ __forceinline__ int warp_jacobi_abs(double* A, int lda, double* V, int ldv, int K, double* cs,
                                                int* pairs, int max_sweeps) {
   switch (K) {
 #define RSM_JK(k) \
-  case k: return warp_jacobi_abs_k<k>(A, lda, V, ldv, cs, pairs, max_sweeps);
+  case k: return warp_jacobi_reg<k>(A, lda, V, ldv, max_sweeps);
     RSM_JK(1) RSM_JK(2) RSM_JK(3) RSM_JK(4) RSM_JK(5) RSM_JK(6) RSM_JK(7) RSM_JK(8)
     RSM_JK(9) RSM_JK(10) RSM_JK(11) RSM_JK(12) RSM_JK(13) RSM_JK(14) RSM_JK(15) RSM_JK(16)
 #undef RSM_JK
