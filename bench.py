@@ -300,7 +300,7 @@ def main():
     if dist is not None:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_ms = et.item() / args.steps
-    h2d = m * n * 8 + m * n
+    h2d = ctx.last_load_h2d_bytes()  # values + the mask as bit-packed on the host
     d2h = (m + n) * r * 8
 
     # ---- roofline of the dominant kernel ----

@@ -140,9 +140,13 @@ rsm_status rsm_ctx_solve_u(rsm_ctx* ctx, const double* V, int64_t r, double* U /
 int rsm_ctx_stage_ms(rsm_ctx* ctx, double* ms, int cap);
 /* Kernel launches issued by the last decompose. */
 int64_t rsm_ctx_launch_count(rsm_ctx* ctx);
+/* Bytes the last rsm_ctx_load copied host -> device: the values plus the
+ * mask bit-packed on the host (rsm_ctx_load_device: 0). */
+int64_t rsm_ctx_last_load_h2d_bytes(rsm_ctx* ctx);
 /* Stage-4 eigensolver diagnostics of the last solve_v: [0] outer iterations,
  * [1] matvecs, [2] lambda_max, [3] spectrum upper bound, [4] max residual of
- * the wanted Ritz pairs, [5] block size, [6] cooperative grid. */
+ * the wanted Ritz pairs, [5] block size, [6] cooperative grid, [7..] phase
+ * clocks (cycles, CTA 0). */
 int rsm_ctx_solver_stats(rsm_ctx* ctx, double* out, int cap);
 
 /* --------------------------------------------------------- one-shot API */

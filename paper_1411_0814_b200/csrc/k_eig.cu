@@ -241,44 +241,56 @@ __device__ void gram_partial(const EigArgs& a, const double* Xo, int nc, int ld,
   }
 }
 
-// warp 0: Cholesky of the nc x nc matrix in sh.H (from packed sh.red),
-// lower factor in sh.S; retries with a diagonal shift when not positive.
-__device__ void chol_small(int nc, EigShared& sh) {
+// warp 0: Cholesky of the nc x nc matrix given packed (upper) in sh.red;
+// lower factor to sh.S and its reciprocal diagonal to sh.dinv. Lane i holds
+// row i in registers; column k of the factor is broadcast by shuffles.
+// Retries with a diagonal shift when the matrix is not numerically positive.
+__device__ __noinline__ void chol_small(int nc, EigShared& sh) {
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
+  double tr = 0.0;
+  for (int k = 0; k < nc; ++k) tr += fabs(sh.red[k * nc - k * (k - 1) / 2]);
   double shift = 0.0;
+  double a[BMAX];
   for (int attempt = 0; attempt < 4; ++attempt) {
-    for (int e = lane; e < nc * nc; e += 32) {
-      int i = e / nc, j = e % nc;
-      if (i < j) { int t = i; i = j; j = t; }
-      // packed upper index of (j, i), j <= i
-      const int p = j * nc - j * (j - 1) / 2 + (i - j);
-      sh.S[(e / nc) * BMAX + (e % nc)] = sh.red[p] + ((e / nc == e % nc) ? shift : 0.0);
-    }
-    __syncwarp();
-    int ok = 1;
-    for (int k = 0; k < nc; ++k) {
-      const double d = sh.S[k * BMAX + k];
-      if (!(d > 0.0)) { ok = 0; break; }
-      const double l = sqrt(d);
-      __syncwarp();
-      if (lane == 0) sh.S[k * BMAX + k] = l;
-      if (lane > k && lane < nc) sh.S[lane * BMAX + k] /= l;
-      __syncwarp();
-      for (int e = lane; e < nc * nc; e += 32) {
-        const int i = e / nc, j = e % nc;
-        if (j > k && i >= j) sh.S[i * BMAX + j] -= sh.S[i * BMAX + k] * sh.S[j * BMAX + k];
+#pragma unroll
+    for (int j = 0; j < BMAX; ++j) {
+      double v = 0.0;
+      if (lane < nc && j < nc) {
+        const int i0 = lane < j ? lane : j, j0 = lane < j ? j : lane;
+        v = sh.red[i0 * nc - i0 * (i0 - 1) / 2 + (j0 - i0)] + (lane == j ? shift : 0.0);
       }
-      __syncwarp();
+      a[j] = v;
     }
-    ok = __all_sync(0xffffffffu, ok);
-    if (ok) {
-      if (lane < nc) sh.dinv[lane] = 1.0 / sh.S[lane * BMAX + lane];
-      break;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < BMAX; ++k) {
+      if (k < nc) {
+        const double d = __shfl_sync(0xffffffffu, a[k], k);
+        if (!(d > 0.0)) ok = false;
+        const double l = sqrt(fmax(d, 0.0));
+        const double inv = l > 0.0 ? 1.0 / l : 0.0;
+        if (lane == k) a[k] = l;
+        if (lane > k) a[k] *= inv;
+        // trailing update: a[j] -= L(lane,k) L(j,k) for k < j <= lane
+#pragma unroll
+        for (int j = k + 1; j < BMAX; ++j) {
+          const double ljk = __shfl_sync(0xffffffffu, a[k], j);
+          if (j < nc && j <= lane) a[j] = fma(-a[k], ljk, a[j]);
+        }
+      }
     }
-    double tr = 0.0;
-    for (int k = 0; k < nc; ++k) tr += fabs(sh.red[k * nc - k * (k - 1) / 2]);
+    if (__all_sync(0xffffffffu, ok)) break;
     shift = (shift == 0.0) ? 1e-14 * tr : shift * 100.0;
+  }
+  if (lane < nc) {
+    double dg = 1.0;
+#pragma unroll
+    for (int j = 0; j < BMAX; ++j) {
+      if (j <= lane) sh.S[lane * BMAX + j] = a[j];
+      if (j == lane) dg = a[j];
+    }
+    sh.dinv[lane] = 1.0 / dg;
   }
   __syncwarp();
 }
@@ -310,13 +322,24 @@ __device__ void apply_rinv(double* X, double* Xo, int nc, int ld, int row_lo, in
 
 __device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, double* Xo, int nc, int ld, int pc,
                        int row_lo, int nr, int& buf, int pw, EigShared& sh) {
+  const bool tme = blockIdx.x == 0 && threadIdx.x == 0;
+  long long t0 = clock64();
   gram_partial(a, Xo, nc, ld, pc, nr, buf, pw);
+  long long t1 = clock64();
   const int P = nc * (nc + 1) / 2;
   grid_reduce(a, grid, buf, P + 1, 0, pw, sh);
+  long long t2 = clock64();
   buf ^= 1;
   chol_small(nc, sh);
   __syncthreads();
+  long long t3 = clock64();
   apply_rinv(X, Xo, nc, ld, row_lo, nr, sh);
+  if (tme) {
+    a.dstat[16] += (double)(t1 - t0);
+    a.dstat[17] += (double)(t2 - t1);
+    a.dstat[18] += (double)(t3 - t2);
+    a.dstat[19] += (double)(clock64() - t3);
+  }
   if (pc >= 0) {
     const double nrm = sqrt(sh.red[P]);
     const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
@@ -335,6 +358,7 @@ template <int NC>
 __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ EigShared sh;
+  if (blockIdx.x == 0 && threadIdx.x < 8) a.dstat[16 + threadIdx.x] = 0.0;
   extern __shared__ __align__(16) double dyn[];
   const int tid = threadIdx.x;
   const int64_t n = a.n;

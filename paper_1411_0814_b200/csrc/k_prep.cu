@@ -26,6 +26,18 @@ __global__ void k_pack_rows(const uint8_t* __restrict__ mask, int64_t m, int64_t
   }
 }
 
+// inverse of k_pack_rows (the byte mask is rebuilt on demand when the host
+// delivered packed words): one thread per byte
+__global__ void k_unpack_rows(const uint32_t* __restrict__ bits, int64_t m, int64_t n, int64_t nwp,
+                              uint8_t* __restrict__ mask) {
+  const int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n, j = t % n;
+    mask[t] = (uint8_t)((bits[i * nwp + (j >> 5)] >> (j & 31)) & 1u);
+  }
+}
+
 // column-major: word (j, w) holds rows 32w..32w+31 of column j. Consecutive
 // threads take consecutive columns so each byte load instruction is one
 // contiguous 32-byte segment of a mask row.
@@ -79,6 +91,13 @@ __global__ void k_count_bits(const uint32_t* __restrict__ bits, int64_t nwords,
     c += __popc(bits[t]);
   c = __reduce_add_sync(0xffffffffu, (unsigned)c);  // per-warp partial fits in 32 bits
   if ((threadIdx.x & 31) == 0) atomicAdd(out, c);   // integer: order-independent
+}
+
+void launch_unpack_rows(const uint32_t* bits, int64_t m, int64_t n, int64_t nwp, uint8_t* mask,
+                        cudaStream_t s) {
+  int64_t blocks = (m * n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_unpack_rows<<<(unsigned)blocks, 256, 0, s>>>(bits, m, n, nwp, mask);
 }
 
 void launch_pack_rows(const uint8_t* mask, int64_t m, int64_t n, uint32_t* bits, int64_t nwp,

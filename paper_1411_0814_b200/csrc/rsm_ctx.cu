@@ -120,6 +120,10 @@ struct rsm_ctx {
   unsigned long long known = 0;
   DevBuf Y, M8, bitsR, bitsC;
   bool haveC = false;
+  bool haveM8 = false;          // byte mask on the device (else rebuilt from bitsR on demand)
+  uint32_t* hstage = nullptr;   // pinned host staging for the packed mask
+  size_t hstage_bytes = 0;
+  int64_t last_h2d = 0;         // bytes copied host -> device by the last load
   // its transpose, built on demand for decompose when m < n
   DevBuf Yt, M8t, bitsRt, bitsCt;
   bool haveT = false, haveCt = false;
@@ -138,7 +142,7 @@ struct rsm_ctx {
 
   cudaEvent_t ev[8] = {};
   double stage_ms[8] = {};
-  double solver_stats[16] = {};  // eig: outer its, matvecs, lambda_max, ub, max residual, block, grid
+  double solver_stats[24] = {};  // eig: outer its, matvecs, lambda_max, ub, max residual, block, grid
   int64_t launches = 0;
 
   void set_err(const std::string& s) { err = s; }
@@ -151,6 +155,16 @@ thread_local std::string g_err;
 void record(rsm_ctx* c, int i) { ck(cudaEventRecord(c->ev[i], c->stream), "cudaEventRecord"); }
 
 // ---------------------------------------------------------------- layout
+// the byte mask, rebuilt from the packed rows when the host delivered words
+void ensure_m8(rsm_ctx* c) {
+  if (c->haveM8) return;
+  c->M8.ensure((size_t)c->m * c->n);
+  rsmk::launch_unpack_rows(c->bitsR.as<uint32_t>(), c->m, c->n, ceil_div(c->n, 128) * 4, c->M8.as<uint8_t>(),
+                           c->stream);
+  ++c->launches;
+  c->haveM8 = true;
+}
+
 View make_view(rsm_ctx* c, bool transposed, bool needC) {
   if (!c->loaded) fail(RSM_ERR_INVALID_CONFIG, "no matrix loaded");
   View v{};
@@ -160,6 +174,7 @@ View make_view(rsm_ctx* c, bool transposed, bool needC) {
     v.nwp = ceil_div(c->n, 128) * 4;
     v.mwp = ceil_div(c->m, 32);
     if (needC && !c->haveC) {
+      ensure_m8(c);
       c->bitsC.ensure(sizeof(uint32_t) * v.n * v.mwp);
       rsmk::launch_pack_cols(c->M8.as<uint8_t>(), v.m, v.n, c->bitsC.as<uint32_t>(), v.mwp, c->stream);
       ++c->launches;
@@ -174,6 +189,7 @@ View make_view(rsm_ctx* c, bool transposed, bool needC) {
     v.nwp = ceil_div(v.n, 128) * 4;
     v.mwp = ceil_div(v.m, 32);
     if (!c->haveT) {
+      ensure_m8(c);
       c->Yt.ensure(sizeof(double) * c->m * c->n);
       c->M8t.ensure((size_t)c->m * c->n);
       rsmk::launch_transpose(c->Y.as<double>(), c->M8.as<uint8_t>(), c->m, c->n, c->Yt.as<double>(),
@@ -196,17 +212,61 @@ View make_view(rsm_ctx* c, bool transposed, bool needC) {
   return v;
 }
 
-void load_common(rsm_ctx* c, int64_t m, int64_t n) {
+// row words of the byte mask on the host (bit j%32 of word j/32, nonzero =
+// observed, zero padded to nwp words), split over host threads; 8 bytes at a
+// time: OR-fold every byte into its low bit, then gather the 8 bits
+void pack_rows_host(const uint8_t* mask, int64_t m, int64_t n, int64_t nwp, uint32_t* out) {
+  auto work = [&](int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i) {
+      const uint8_t* row = mask + i * n;
+      uint32_t* o = out + i * nwp;
+      int64_t w = 0;
+      for (; (w + 1) * 32 <= n; ++w) {
+        uint32_t word = 0;
+        for (int q = 0; q < 4; ++q) {
+          uint64_t x;
+          std::memcpy(&x, row + w * 32 + q * 8, 8);
+          uint64_t t = x | (x >> 4);
+          t |= t >> 2;
+          t |= t >> 1;
+          t &= 0x0101010101010101ull;
+          word |= (uint32_t)((t * 0x0102040810204080ull) >> 56) << (8 * q);
+        }
+        o[w] = word;
+      }
+      if (w * 32 < n) {
+        uint32_t word = 0;
+        for (int64_t j = w * 32; j < n; ++j) word |= (row[j] ? 1u : 0u) << (j - w * 32);
+        o[w++] = word;
+      }
+      for (; w < nwp; ++w) o[w] = 0u;
+    }
+  };
+  const int64_t bytes = m * n;
+  int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 16);
+  if (bytes < ((int64_t)8 << 20)) nt = 1;
+  nt = (int)std::min<int64_t>(nt, m);
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, m * t / nt, m * (t + 1) / nt);
+  work(0, m / nt);
+  for (auto& x : th) x.join();
+}
+
+void load_common(rsm_ctx* c, int64_t m, int64_t n, bool packed_on_host) {
   c->m = m;
   c->n = n;
   c->haveC = c->haveT = c->haveCt = false;
   const int64_t nwp = ceil_div(n, 128) * 4;
   c->bitsR.ensure(sizeof(uint32_t) * m * nwp);
-  rsmk::launch_pack_rows(c->M8.as<uint8_t>(), m, n, c->bitsR.as<uint32_t>(), nwp, c->stream);
+  if (!packed_on_host) {
+    rsmk::launch_pack_rows(c->M8.as<uint8_t>(), m, n, c->bitsR.as<uint32_t>(), nwp, c->stream);
+    ++c->launches;
+  }
+  c->haveM8 = !packed_on_host;
   c->cnt64.ensure(sizeof(unsigned long long));
   ck(cudaMemsetAsync(c->cnt64.p, 0, sizeof(unsigned long long), c->stream), "memset");
   rsmk::launch_count_bits(c->bitsR.as<uint32_t>(), m * nwp, c->cnt64.as<unsigned long long>(), c->stream);
-  c->launches += 2;
+  c->launches += 1;
   ck(cudaMemcpyAsync(&c->known, c->cnt64.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "sync");
   ck(cudaGetLastError(), "load kernels");
@@ -486,7 +546,7 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   c->ePart.ensure(sizeof(double) * 2 * (size_t)grid * pw);
   c->eW.ensure(sizeof(double) * 32);
   c->eI.ensure(sizeof(int) * 8);
-  c->eD.ensure(sizeof(double) * 16);
+  c->eD.ensure(sizeof(double) * 32);
   c->Vhat.ensure(sizeof(double) * n * r);
   rsmk::EigArgs a{};
   a.G = c->G.as<double>();
@@ -505,10 +565,10 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   c->launches += 2;
   double w[32];
   int istat[8];
-  double dstat[16];
+  double dstat[32];
   ck(cudaMemcpyAsync(w, c->eW.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaMemcpyAsync(istat, c->eI.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
-  ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 13, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 32, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "solve_v");
   ck(cudaGetLastError(), "eig kernels");
   c->solver_stats[0] = istat[3];
@@ -522,6 +582,7 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   c->solver_stats[13] = dstat[9];   // Rayleigh-Ritz Jacobi sweeps (total)
   c->solver_stats[14] = dstat[10];  // and their cycles
   c->solver_stats[15] = dstat[11];  // filter matvec cycles (CTA 0)
+  for (int i = 0; i < 8; ++i) c->solver_stats[16 + i] = dstat[16 + i];  // CholQR sub-phase cycles
   if (istat[0] != 0) fail(RSM_ERR_INTERNAL, "symmetric eigensolver failed to converge");
   c->Vhat_n = n;
   c->Vhat_r = r;
@@ -773,6 +834,7 @@ rsm_status rsm_ctx_destroy(rsm_ctx* c) {
                     &c->eW, &c->eI, &c->eD, &c->Vhat, &c->U, &c->rowres, &c->flagged, &c->dsum,
                     &c->cnt64};
   for (DevBuf* b : bufs) b->release();
+  if (c->hstage) cudaFreeHost(c->hstage);
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   cudaStreamDestroy(c->stream);
@@ -800,11 +862,27 @@ rsm_status rsm_ctx_load(rsm_ctx* c, const double* values, const uint8_t* mask, i
   return guard(c, [&] {
     if (m < 1 || n < 1) fail(RSM_ERR_INVALID_CONFIG, "matrix dimensions must be positive");
     if (!values || !mask) fail(RSM_ERR_INVALID_CONFIG, "null matrix buffers");
+    // the values stream to the device while host threads bit-pack the mask
+    // into pinned staging; only the packed words (1/8 of the byte mask) cross
+    // the link after them
     c->Y.ensure(sizeof(double) * m * n);
-    c->M8.ensure((size_t)m * n);
     ck(cudaMemcpyAsync(c->Y.p, values, sizeof(double) * m * n, cudaMemcpyHostToDevice, c->stream), "H2D Y");
-    ck(cudaMemcpyAsync(c->M8.p, mask, (size_t)m * n, cudaMemcpyHostToDevice, c->stream), "H2D mask");
-    load_common(c, m, n);
+    const int64_t nwp = ceil_div(n, 128) * 4;
+    const size_t wbytes = sizeof(uint32_t) * (size_t)m * nwp;
+    if (c->hstage_bytes < wbytes) {
+      if (c->hstage) cudaFreeHost(c->hstage);
+      c->hstage = nullptr;
+      c->hstage_bytes = 0;
+      ck(cudaHostAlloc((void**)&c->hstage, wbytes, cudaHostAllocDefault), "pinned staging");
+      c->hstage_bytes = wbytes;
+    }
+    // (the previous load's copy out of the staging buffer completed: every
+    // load ends with a stream synchronisation)
+    pack_rows_host(mask, m, n, nwp, c->hstage);
+    c->bitsR.ensure(wbytes);
+    ck(cudaMemcpyAsync(c->bitsR.p, c->hstage, wbytes, cudaMemcpyHostToDevice, c->stream), "H2D mask words");
+    c->last_h2d = (int64_t)(sizeof(double) * m * n + wbytes);
+    load_common(c, m, n, true);
   });
 }
 
@@ -815,7 +893,8 @@ rsm_status rsm_ctx_load_device(rsm_ctx* c, const double* d_values, const uint8_t
     c->M8.ensure((size_t)m * n);
     ck(cudaMemcpyAsync(c->Y.p, d_values, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c->stream), "D2D Y");
     ck(cudaMemcpyAsync(c->M8.p, d_mask, (size_t)m * n, cudaMemcpyDeviceToDevice, c->stream), "D2D mask");
-    load_common(c, m, n);
+    c->last_h2d = 0;
+    load_common(c, m, n, false);
   });
 }
 
@@ -920,8 +999,10 @@ int rsm_ctx_stage_ms(rsm_ctx* c, double* ms, int cap) {
 
 int64_t rsm_ctx_launch_count(rsm_ctx* c) { return c ? c->launches : 0; }
 
+int64_t rsm_ctx_last_load_h2d_bytes(rsm_ctx* c) { return c ? c->last_h2d : 0; }
+
 int rsm_ctx_solver_stats(rsm_ctx* c, double* out, int cap) {
-  const int k = std::min(cap, 16);
+  const int k = std::min(cap, 24);
   for (int i = 0; i < k; ++i) out[i] = c->solver_stats[i];
   return k;
 }

@@ -88,6 +88,8 @@ struct SolveUArgs {
 // k_prep.cu
 void launch_pack_rows(const uint8_t* mask, int64_t m, int64_t n, uint32_t* bits, int64_t nwp,
                       cudaStream_t s);
+void launch_unpack_rows(const uint32_t* bits, int64_t m, int64_t n, int64_t nwp, uint8_t* mask,
+                        cudaStream_t s);
 void launch_pack_cols(const uint8_t* mask, int64_t m, int64_t n, uint32_t* bits, int64_t mwp,
                       cudaStream_t s);
 void launch_transpose(const double* Y, const uint8_t* M, int64_t m, int64_t n, double* Yt,

@@ -98,6 +98,7 @@ def lib():
         "rsm_ctx_solve_u": (i32, [_P, _P, i64, _P, C.POINTER(i64), C.POINTER(dbl)]),
         "rsm_ctx_stage_ms": (C.c_int, [_P, _P, C.c_int]),
         "rsm_ctx_launch_count": (i64, [_P]),
+        "rsm_ctx_last_load_h2d_bytes": (i64, [_P]),
         "rsm_ctx_solver_stats": (C.c_int, [_P, _P, C.c_int]),
         "rsm_make_trial_params": (i32, [C.POINTER(_Config), i64, i64, C.POINTER(_TrialParams)]),
         "rsm_decompose": (i32, [_P, _P, i64, i64, C.POINTER(_Config), _P, _P, C.POINTER(_Report)]),
@@ -124,7 +125,7 @@ def exported_symbols():
     return ["rsm_config_default", "rsm_last_error", "rsm_ctx_create", "rsm_ctx_destroy", "rsm_nccl_unique_id",
             "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_decompose", "rsm_ctx_fetch_factors",
             "rsm_ctx_select", "rsm_ctx_harvest_gram", "rsm_ctx_solve_v", "rsm_ctx_solve_u", "rsm_ctx_stage_ms",
-            "rsm_ctx_launch_count", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_harvest_gram", "rsm_solve_v",
+            "rsm_ctx_launch_count", "rsm_ctx_last_load_h2d_bytes", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_harvest_gram", "rsm_solve_v",
             "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_fp64_peak_tflops",
             "rsm_dmma_peak_tflops", "rsm_shard_range"]
 
@@ -373,11 +374,16 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().rsm_ctx_launch_count(self.h))
 
+    def last_load_h2d_bytes(self) -> int:
+        """Bytes the last host load copied to the device (values + packed mask)."""
+        return int(lib().rsm_ctx_last_load_h2d_bytes(self.h))
+
     def solver_stats(self) -> dict:
-        buf = (C.c_double * 16)()
-        k = lib().rsm_ctx_solver_stats(self.h, C.cast(buf, C.c_void_p), 16)
+        buf = (C.c_double * 24)()
+        k = lib().rsm_ctx_solver_stats(self.h, C.cast(buf, C.c_void_p), 24)
         keys = ["outer", "matvecs", "lambda_max", "ub", "max_residual", "block", "grid", "cyc_filter",
-                "cyc_cholqr", "cyc_rr", "cyc_eig", "cyc_rotate", "cyc_setup", "jac_sweeps", "cyc_jacobi", "cyc_matvec"]
+                "cyc_cholqr", "cyc_rr", "cyc_eig", "cyc_rotate", "cyc_setup", "jac_sweeps", "cyc_jacobi", "cyc_matvec", "cyc_cq_gram", "cyc_cq_reduce", "cyc_cq_chol",
+                "cyc_cq_apply", "cyc_x4", "cyc_x5", "cyc_x6", "cyc_x7"]
         return dict(zip(keys, buf[:k]))
 
 

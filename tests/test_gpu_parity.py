@@ -303,3 +303,26 @@ def test_decompose_deterministic():
     F1, r1 = rsm.decompose(M, cfg)
     F2, r2 = rsm.decompose(M, cfg)
     assert np.array_equal(F1.u, F2.u) and np.array_equal(F1.v, F2.v) and r1.e == r2.e
+
+
+def test_host_packed_mask_matches_device_load():
+    # rsm_ctx_load packs the byte mask on the host (any nonzero byte is an
+    # observation, core.hpp:26); rsm_ctx_load_device packs it on the device.
+    # Both loads must give bitwise identical decompositions, for both branches.
+    import torch
+    M = gen(3000, 96, 3, 0.7, 1e-3, 12)
+    W = M.mask.astype(np.uint8) * np.array([1, 7, 255], dtype=np.uint8)[np.arange(M.mask.size) % 3].reshape(M.mask.shape)
+    for mode, block in [(rsm.Mode.M2, 4), (rsm.Mode.M1, 5)]:
+        cfg = rsm.RsmConfig(rank=3, mode=mode, block=block, plan=rsm.TrialPlan(800), seed=4)
+        c1 = rsm.Context(0)
+        c1.load_arrays(M.values, W)
+        assert c1.last_load_h2d_bytes() == M.values.nbytes + 4 * 3000 * 4  # 96 cols -> 4 words per row
+        F1, r1 = c1.decompose(cfg)
+        Yd = torch.from_numpy(np.ascontiguousarray(M.values)).cuda()
+        Wd = torch.from_numpy(np.ascontiguousarray(M.mask.astype(np.uint8))).cuda()
+        c2 = rsm.Context(0)
+        c2.load_device(Yd.data_ptr(), Wd.data_ptr(), 3000, 96)
+        torch.cuda.synchronize()
+        F2, r2 = c2.decompose(cfg)
+        assert np.array_equal(F1.u, F2.u) and np.array_equal(F1.v, F2.v)
+        assert r1.e == r2.e and r1.z == r2.z and r1.trials_accepted == r2.trials_accepted
