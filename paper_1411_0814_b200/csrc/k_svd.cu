@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
         if (stop) {
           if (lane < K) sig[lane] = sqrt(fmax(gram[lane * KMAX + lane], 0.0));
         } else {
-          warp_jacobi_eig(gram, KMAX, W, KMAX, K, cs, pairs, 2.220446049250313e-16, 40, true);
+          warp_jacobi_rel(gram, KMAX, W, KMAX, K, cs, pairs, 2.220446049250313e-16, 40);
         }
         if (lane == 0) flags[2] = stop ? 1 : 0;
       }
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
           }
       }
       __syncwarp();
-      warp_jacobi_eig(Gs, K, Ws, K, K, cs, pairs, 2.220446049250313e-16, 40, true);
+      warp_jacobi_reg<K, true>(Gs, K, Ws, K, 40);
       __syncwarp();
       for (int c = lane; c < L; c += 32) {
         double x[K];

@@ -327,8 +327,9 @@ __host__ __device__ constexpr int circle_src(int l, int Kp) {
 // every index pair meets once per sweep. Threshold as warp_jacobi_eig_abs.
 // On return A's diagonal holds the eigenvalues and V's columns the matching
 // eigenvectors (in some order). Returns the sweep count.
-template <int K>
-__device__ __noinline__ int warp_jacobi_reg(double* A, int lda, double* V, int ldv, int max_sweeps) {
+template <int K, bool REL = false>
+__device__ __noinline__ int warp_jacobi_reg(double* A, int lda, double* V, int ldv, int max_sweeps,
+                                            double rtol = 2.220446049250313e-16) {
   constexpr int Kp = (K + 1) & ~1;
   const int lane = threadIdx.x & 31;
   const bool live = lane < Kp;
@@ -348,13 +349,23 @@ __device__ __noinline__ int warp_jacobi_reg(double* A, int lda, double* V, int l
   for (int r = 0; r < Kp; ++r) f += a[r] * a[r];
   f = warp_sum(f);
   const double thr = fmax(16.0 * 2.220446049250313e-16 * sqrt(f), 1e-300);
+  // REL: |a_pq| <= rtol sqrt(|a_pp a_qq|) (or exactly 0) for every pair, as
+  // warp_jacobi_eig's relative test; else the absolute threshold above
+  auto big = [&](double apq, double app, double aqq) {
+    return REL ? (apq != 0.0 && fabs(apq) > rtol * sqrt(fabs(app * aqq))) : fabs(apq) > thr;
+  };
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    double mo = 0.0;
+    double dme = 0.0;
 #pragma unroll
-    for (int r = 0; r < Kp; ++r)
-      if (r != lane) mo = fmax(mo, fabs(a[r]));
-    if (!__any_sync(0xffffffffu, live && mo > thr)) break;
+    for (int r = 0; r < Kp; ++r) dme = (r == lane) ? a[r] : dme;
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < Kp; ++r) {
+      const double drr = __shfl_sync(0xffffffffu, dme, r);
+      if (r != lane && big(a[r], drr, dme)) any = true;
+    }
+    if (!__any_sync(0xffffffffu, live && any)) break;
 #pragma unroll 1
     for (int step = 0; step < Kp - 1; ++step) {
       // this slot's diagonal and its pair's off-diagonal entry
@@ -368,11 +379,18 @@ __device__ __noinline__ int warp_jacobi_reg(double* A, int lda, double* V, int l
       const bool isp = (lane & 1) == 0;
       const double app = isp ? d : dp, aqq = isp ? dp : d;
       double c = 1.0, sn = 0.0;
-      if (live && fabs(off) > thr) {
-        const double zeta = (aqq - app) / (2.0 * off);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        c = rsqrt(1.0 + t * t);
-        sn = c * t;
+      if (live && big(off, app, aqq)) {
+        // t = sign(d) e / (|d| + r) with d = a_qq - a_pp, e = 2 a_pq,
+        // r = hypot(d, e) (Rutishauser's root); with w = r + |d|,
+        // c = w / sqrt(2 r w) and s = sign(d) e / sqrt(2 r w): two rsqrt and
+        // no division on the step's critical path
+        const double dd = aqq - app, ee = 2.0 * off;
+        const double r2 = fma(dd, dd, ee * ee);
+        const double rr = r2 * rsqrt(r2);
+        const double w = rr + fabs(dd);
+        const double g = rsqrt(2.0 * rr * w);
+        c = w * g;
+        sn = (dd >= 0.0 ? ee : -ee) * g;
       }
       // columns: A <- A J, V <- V J
 #pragma unroll
@@ -421,6 +439,19 @@ __device__ __noinline__ int warp_jacobi_reg(double* A, int lda, double* V, int l
   }
   __syncwarp();
   return sweep;
+}
+
+// relative-threshold register Jacobi dispatched on the runtime size (K <= 16)
+__device__ __forceinline__ int warp_jacobi_rel(double* A, int lda, double* V, int ldv, int K, double* cs,
+                                               int* pairs, double tol, int max_sweeps) {
+  switch (K) {
+#define RSM_JR(k) \
+  case k: return warp_jacobi_reg<k, true>(A, lda, V, ldv, max_sweeps, tol);
+    RSM_JR(1) RSM_JR(2) RSM_JR(3) RSM_JR(4) RSM_JR(5) RSM_JR(6) RSM_JR(7) RSM_JR(8)
+    RSM_JR(9) RSM_JR(10) RSM_JR(11) RSM_JR(12) RSM_JR(13) RSM_JR(14) RSM_JR(15) RSM_JR(16)
+#undef RSM_JR
+    default: return warp_jacobi_eig(A, lda, V, ldv, K, cs, pairs, tol, max_sweeps, true);
+  }
 }
 
 // dispatch on the runtime size (K <= KMAX)
