@@ -190,7 +190,7 @@ View make_view(rsm_ctx* c, bool transposed, bool needC) {
     v.mwp = ceil_div(v.m, 32);
     if (!c->haveT) {
       ensure_m8(c);
-      c->Yt.ensure(sizeof(double) * c->m * c->n);
+      c->Yt.ensure(sizeof(double) * c->m * c->n + 16);  // stage 5 may read 8 bytes past the end
       c->M8t.ensure((size_t)c->m * c->n);
       rsmk::launch_transpose(c->Y.as<double>(), c->M8.as<uint8_t>(), c->m, c->n, c->Yt.as<double>(),
                              c->M8t.as<uint8_t>(), c->stream);
@@ -865,7 +865,7 @@ rsm_status rsm_ctx_load(rsm_ctx* c, const double* values, const uint8_t* mask, i
     // the values stream to the device while host threads bit-pack the mask
     // into pinned staging; only the packed words (1/8 of the byte mask) cross
     // the link after them
-    c->Y.ensure(sizeof(double) * m * n);
+    c->Y.ensure(sizeof(double) * m * n + 16);  // stage 5 may read 8 bytes past the end
     ck(cudaMemcpyAsync(c->Y.p, values, sizeof(double) * m * n, cudaMemcpyHostToDevice, c->stream), "H2D Y");
     const int64_t nwp = ceil_div(n, 128) * 4;
     const size_t wbytes = sizeof(uint32_t) * (size_t)m * nwp;
@@ -889,7 +889,7 @@ rsm_status rsm_ctx_load(rsm_ctx* c, const double* values, const uint8_t* mask, i
 rsm_status rsm_ctx_load_device(rsm_ctx* c, const double* d_values, const uint8_t* d_mask, int64_t m, int64_t n) {
   return guard(c, [&] {
     if (m < 1 || n < 1) fail(RSM_ERR_INVALID_CONFIG, "matrix dimensions must be positive");
-    c->Y.ensure(sizeof(double) * m * n);
+    c->Y.ensure(sizeof(double) * m * n + 16);  // stage 5 may read 8 bytes past the end
     c->M8.ensure((size_t)m * n);
     ck(cudaMemcpyAsync(c->Y.p, d_values, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c->stream), "D2D Y");
     ck(cudaMemcpyAsync(c->M8.p, d_mask, (size_t)m * n, cudaMemcpyDeviceToDevice, c->stream), "D2D mask");
