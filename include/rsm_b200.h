@@ -117,6 +117,14 @@ rsm_status rsm_ctx_decompose(rsm_ctx* ctx, const rsm_config* cfg, double* U, dou
                              rsm_report* rep);
 rsm_status rsm_ctx_fetch_factors(rsm_ctx* ctx, double* U, double* V);
 
+/* Alternating masked least squares baseline on the loaded matrix; replaces
+ * rsm::baseline_als (include/rsm/solver.hpp:79-81, src/als.cpp:11-44):
+ * V from Rng(seed, ALS_INIT=6, column).next_normal(), `iterations` rounds of
+ * U = rows(M; V), V = rows(M^T; U), then U = rows(M; V). The report carries
+ * e, underdetermined_rows (last U step) and wall_time. */
+rsm_status rsm_ctx_als(rsm_ctx* ctx, int64_t r, int64_t iterations, uint64_t seed, double* U, double* V,
+                       rsm_report* rep);
+
 /* Stage entry points on the loaded matrix, for the oriented problem
  * (m >= n as loaded; call these only for the matrix as given). */
 rsm_status rsm_ctx_select(rsm_ctx* ctx, const rsm_trial_params* p, uint64_t trials,
@@ -154,6 +162,8 @@ int rsm_ctx_solver_stats(rsm_ctx* ctx, double* out, int cap);
 rsm_status rsm_make_trial_params(const rsm_config* cfg, int64_t m, int64_t n, rsm_trial_params* out);
 rsm_status rsm_decompose(const double* values, const uint8_t* mask, int64_t m, int64_t n,
                          const rsm_config* cfg, double* U, double* V, rsm_report* rep);
+rsm_status rsm_als(const double* values, const uint8_t* mask, int64_t m, int64_t n, int64_t r,
+                   int64_t iterations, uint64_t seed, double* U, double* V, rsm_report* rep);
 rsm_status rsm_harvest_gram(const double* values, const uint8_t* mask, int64_t m, int64_t n,
                             const rsm_trial_params* p, uint64_t trials, double* G,
                             uint64_t* attempted, uint64_t* accepted, uint64_t* z);

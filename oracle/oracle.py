@@ -75,6 +75,8 @@ def lib():
         L.orc_decompose.restype = C.c_int
         L.orc_decompose.argtypes = [P, P, i64, i64, C.POINTER(Config), P, P, C.POINTER(Report)]
         L.orc_generate_rows.argtypes = [i64, i64, i64, d, d, u64, i64, i64, P, P]
+        L.orc_als.restype = C.c_int
+        L.orc_als.argtypes = [P, P, i64, i64, i64, i64, u64, P, P, C.POINTER(i64), C.POINTER(d)]
         _lib = L
     return _lib
 
@@ -166,6 +168,18 @@ def solve_u(Y, mask, V, r):
     _chk(lib().orc_solve_u(_p(np.ascontiguousarray(Y)), _p(np.ascontiguousarray(mask, np.uint8)), m, n,
                            _p(np.ascontiguousarray(V, np.float64)), r, _p(U), C.byref(fl)))
     return U, fl.value
+
+
+def als(Y, mask, r, iterations, seed):
+    """baseline_als restatement (als.cpp:11-44) -> (U, V, flagged, e)."""
+    m, n = Y.shape
+    U = np.zeros((m, r))
+    V = np.zeros((n, r))
+    fl = C.c_int64()
+    e = C.c_double()
+    _chk(lib().orc_als(_p(np.ascontiguousarray(Y)), _p(np.ascontiguousarray(mask, np.uint8)), m, n, r, iterations,
+                       seed, _p(U), _p(V), C.byref(fl), C.byref(e)))
+    return U, V, fl.value, e.value
 
 
 def masked_residual_norm(Y, mask, U, V):

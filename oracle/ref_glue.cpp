@@ -148,6 +148,18 @@ int ref_solve_u(const double* Y, const uint8_t* mask, int64_t m, int64_t n, cons
   });
 }
 
+int ref_als(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int64_t r, int64_t iterations,
+            uint64_t seed, int workers, double* U, double* V, int64_t* flagged, double* e) {
+  return guard([&] {
+    MaskedMatrix M = make(Y, mask, m, n);
+    auto [F, rep] = baseline_als(M, r, iterations, seed, workers);
+    std::memcpy(U, F.u.data(), sizeof(double) * m * r);
+    std::memcpy(V, F.v.data(), sizeof(double) * n * r);
+    *flagged = rep.underdetermined_rows;
+    *e = rep.e;
+  });
+}
+
 int ref_decompose(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int64_t rank, int mode,
                   int64_t block, int64_t vpt, uint64_t trials, double epsilon, uint64_t seed, double tol,
                   int64_t min_dim, int workers, double* U, double* V, double* out_e, uint64_t* out_u64,

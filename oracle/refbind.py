@@ -30,6 +30,7 @@ def lib():
         L.ref_solve_u.argtypes = [P, P, i64, i64, P, i64, C.c_int, P, C.POINTER(i64), C.POINTER(d)]
         L.ref_decompose.argtypes = [P, P, i64, i64, i64, C.c_int, i64, i64, u64, d, u64, d, i64, C.c_int, P, P,
                                     C.POINTER(d), P, P, C.POINTER(d)]
+        L.ref_als.argtypes = [P, P, i64, i64, i64, i64, u64, C.c_int, P, P, C.POINTER(i64), C.POINTER(d)]
         L.ref_masked_residual_norm.restype = d
         L.ref_masked_residual_norm.argtypes = [P, P, i64, i64, P, P, i64]
         _lib = L
@@ -107,6 +108,16 @@ def solve_u(Y, W, V, r, workers=0, timed=False):
     _chk(lib().ref_solve_u(_p(Y), _p(W), m, n, _p(np.ascontiguousarray(V)), r, workers, _p(U), C.byref(fl),
                            C.byref(secs)))
     return (U, fl.value, secs.value) if timed else (U, fl.value)
+
+
+def als(Y, W, r, iterations, seed, workers=0):
+    """The reference's baseline_als -> (U, V, flagged, e)."""
+    m, n = Y.shape
+    U = np.zeros((m, r))
+    V = np.zeros((n, r))
+    fl, e = C.c_int64(), C.c_double()
+    _chk(lib().ref_als(_p(Y), _p(W), m, n, r, iterations, seed, workers, _p(U), _p(V), C.byref(fl), C.byref(e)))
+    return U, V, fl.value, e.value
 
 
 def decompose(Y, W, rank, trials, mode=0, block=0, vectors_per_trial=0, seed=0, tol=1e-9, min_dim=0,

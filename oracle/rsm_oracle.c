@@ -691,6 +691,41 @@ int orc_decompose(const double* Y, const uint8_t* mask, int64_t m, int64_t n,
 
 /* ----------------------------------------------------------------- synth --- */
 
+int orc_als(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int64_t r, int64_t iterations,
+            uint64_t seed, double* U, double* V, int64_t* flagged, double* e) {
+  /* als.cpp:17-20 */
+  if (r < 1 || r >= (m < n ? m : n)) return 2;
+  if (iterations < 1) return 2;
+  int64_t known = 0;
+  for (int64_t q = 0; q < m * n; ++q) known += mask[q] ? 1 : 0;
+  if (known == 0) return 4;
+  for (int64_t i = 0; i < n; ++i) { /* als.cpp:22-26 */
+    uint64_t st = orc_rng_state(seed, 6 /* ALS_INIT */, (uint64_t)i);
+    for (int64_t k = 0; k < r; ++k) V[i * r + k] = orc_next_normal(&st);
+  }
+  /* M^T (core.hpp MaskedMatrix::transposed) */
+  double* YT = (double*)malloc(sizeof(double) * (size_t)(m * n));
+  uint8_t* WT = (uint8_t*)malloc((size_t)(m * n));
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      YT[j * m + i] = Y[i * n + j];
+      WT[j * m + i] = mask[i * n + j];
+    }
+  int64_t fl = 0, flt = 0;
+  int st = 0;
+  for (int64_t it = 0; it < iterations && st == 0; ++it) { /* als.cpp:29-32 */
+    st = orc_solve_u(Y, mask, m, n, V, r, U, &fl);
+    if (st == 0) st = orc_solve_u(YT, WT, n, m, U, r, V, &flt);
+  }
+  if (st == 0) st = orc_solve_u(Y, mask, m, n, V, r, U, &fl); /* als.cpp:33 */
+  free(YT);
+  free(WT);
+  if (st) return st;
+  *flagged = fl;
+  *e = orc_masked_residual_norm(Y, mask, m, n, U, V, r); /* als.cpp:40 */
+  return 0;
+}
+
 void orc_generate_rows(int64_t m, int64_t n, int64_t r, double rho, double sigma, uint64_t seed,
                        int64_t row0, int64_t rows, double* Y, uint8_t* mask) {
   /* synth.cpp:12-57 (observed matrix only; streams are per row, so any row

@@ -115,6 +115,12 @@ int orc_solve_u(const double* Y, const uint8_t* mask, int64_t m, int64_t n, cons
 int orc_solve_row(const double* A, const double* y, int64_t nj, int64_t r, double* u);
 
 /* core.cpp:15-39 */
+/* baseline_als (src/als.cpp:11-44): V from Rng(seed, ALS_INIT=6, i).next_normal,
+ * `iterations` rounds of U = solve_u(M, V), V = solve_u(M^T, U), a final U step;
+ * e = masked_residual_norm(M, F), flagged = the last U step's count. */
+int orc_als(const double* Y, const uint8_t* mask, int64_t m, int64_t n, int64_t r, int64_t iterations,
+            uint64_t seed, double* U, double* V, int64_t* flagged, double* e);
+
 double orc_masked_residual_norm(const double* Y, const uint8_t* mask, int64_t m, int64_t n,
                                 const double* U, const double* V, int64_t r);
 

@@ -26,6 +26,7 @@
 #include "../../include/rsm_b200.h"
 #include "rsm_internal.h"
 #include "rsm_dev.cuh"
+#include "host_rng.h"
 
 namespace {
 
@@ -614,11 +615,14 @@ struct SolveUOut {
   double ss = 0.0;
 };
 
-SolveUOut solve_u_impl(rsm_ctx* c, const View& v, int64_t r) {
+// stage 5 on view v: rows of `out` (v.m x r) from the basis (v.n x r), plus
+// the residual sum and the flagged-row count; row-sharded over ranks with
+// the shards gathered into `out` (detail/row_solve.hpp:12-36, solver.cpp:64-89)
+SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& outbuf, int64_t r) {
   if (r < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_u: rank must be positive");
   if (r > 8) fail(RSM_ERR_INVALID_CONFIG, "device row solver supports r <= 8");
-  if (c->Vhat_n != v.n || c->Vhat_r != r) fail(RSM_ERR_INVALID_CONFIG, "solve_u: basis shape does not match matrix");
-  c->U.ensure(sizeof(double) * v.m * r);
+  outbuf.ensure(sizeof(double) * v.m * r);
+  double* out = outbuf.as<double>();
   c->rowres.ensure(sizeof(double) * v.m);
   c->flagged.ensure(sizeof(int) * 2);
   c->dsum.ensure(sizeof(double) * 2);
@@ -629,8 +633,8 @@ SolveUOut solve_u_impl(rsm_ctx* c, const View& v, int64_t r) {
   a.Y = v.Y; a.bitsR = v.bitsR;
   a.m = v.m; a.n = v.n; a.nwp = v.nwp;
   a.row_lo = lo; a.row_hi = hi;
-  a.V = c->Vhat.as<double>();
-  a.U = c->U.as<double>();
+  a.V = basis;
+  a.U = out;
   a.rowres = c->rowres.as<double>();
   a.flagged = c->flagged.as<int>();
   a.r = (int)r;
@@ -664,13 +668,13 @@ SolveUOut solve_u_impl(rsm_ctx* c, const View& v, int64_t r) {
     DevBuf pad;
     pad.ensure(sizeof(double) * maxrows * r * (c->world + 1));
     double* sendb = pad.as<double>() + (size_t)maxrows * r * c->world;
-    ck(cudaMemcpyAsync(sendb, c->U.as<double>() + lo * r, sizeof(double) * (hi - lo) * r, cudaMemcpyDeviceToDevice, c->stream), "D2D");
+    ck(cudaMemcpyAsync(sendb, out + lo * r, sizeof(double) * (hi - lo) * r, cudaMemcpyDeviceToDevice, c->stream), "D2D");
     if (g_nccl.allGather(sendb, pad.p, (size_t)(maxrows * r), kNcclFloat64, c->comm, c->stream) != 0)
       fail(RSM_ERR_INTERNAL, "ncclAllGather failed");
     for (int g = 0; g < c->world; ++g) {
       int64_t glo, ghi;
       rsm_shard_range(v.m, c->world, g, &glo, &ghi);
-      ck(cudaMemcpyAsync(c->U.as<double>() + glo * r, pad.as<double>() + (size_t)g * maxrows * r,
+      ck(cudaMemcpyAsync(out + glo * r, pad.as<double>() + (size_t)g * maxrows * r,
                          sizeof(double) * (ghi - glo) * r, cudaMemcpyDeviceToDevice, c->stream), "D2D");
     }
     ck(cudaStreamSynchronize(c->stream), "sync");
@@ -684,11 +688,17 @@ SolveUOut solve_u_impl(rsm_ctx* c, const View& v, int64_t r) {
     ck(cudaStreamSynchronize(c->stream), "solve_u");
   }
   ck(cudaGetLastError(), "solve_u kernels");
-  c->U_m = v.m;
-  c->U_r = r;
   SolveUOut o;
   o.flagged = fl;
   o.ss = ss;
+  return o;
+}
+
+SolveUOut solve_u_impl(rsm_ctx* c, const View& v, int64_t r) {
+  if (c->Vhat_n != v.n || c->Vhat_r != r) fail(RSM_ERR_INVALID_CONFIG, "solve_u: basis shape does not match matrix");
+  SolveUOut o = solve_rows(c, v, c->Vhat.as<double>(), c->U, r);
+  c->U_m = v.m;
+  c->U_r = r;
   return o;
 }
 
@@ -734,6 +744,49 @@ void decompose_impl(rsm_ctx* c, const rsm_config* cfg, double* Uout, double* Vou
   }
   ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[6]), "event");
   c->stage_ms[6] = ms;
+  rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ------------------------------------------------------------------- ALS
+// baseline_als (als.cpp:11-44): V from Rng(seed, ALS_INIT, column).next_normal
+// on the host, then `iterations` rounds of U = rows(M; V), V = rows(M^T; U),
+// and a final U = rows(M; V) whose fused residual gives e; every half-step is
+// the stage-5 kernel, on the loaded matrix and on its device transpose.
+void als_impl(rsm_ctx* c, int64_t r, int64_t iterations, uint64_t seed, double* Uout, double* Vout,
+              rsm_report* rep) {
+  const auto t0 = std::chrono::steady_clock::now();
+  c->launches = 0;
+  std::memset(rep, 0, sizeof(*rep));
+  if (!c->loaded) fail(RSM_ERR_INVALID_CONFIG, "no matrix loaded");
+  const int64_t m = c->m, n = c->n;
+  if (r < 1 || r >= std::min(m, n)) fail(RSM_ERR_INVALID_CONFIG, "rank must lie in [1, min(rows, cols))");
+  if (iterations < 1) fail(RSM_ERR_INVALID_CONFIG, "iteration count must be positive");
+  if (c->known == 0) fail(RSM_ERR_INSUFFICIENT_COVERAGE, "matrix has no observed entries");
+  std::vector<double> v0((size_t)(n * r));
+  for (int64_t i = 0; i < n; ++i) {
+    rsmh::Rng rng(seed, rsmh::stream::ALS_INIT, (uint64_t)i);
+    for (int64_t k = 0; k < r; ++k) v0[(size_t)(i * r + k)] = rng.next_normal();
+  }
+  const View vm = make_view(c, false, false);
+  const View vt = make_view(c, true, false);
+  c->Vhat.ensure(sizeof(double) * n * r);
+  ck(cudaMemcpyAsync(c->Vhat.p, v0.data(), sizeof(double) * n * r, cudaMemcpyHostToDevice, c->stream), "H2D V0");
+  SolveUOut us;
+  for (int64_t it = 0; it < iterations; ++it) {
+    us = solve_rows(c, vm, c->Vhat.as<double>(), c->U, r);
+    solve_rows(c, vt, c->U.as<double>(), c->Vhat, r);
+  }
+  us = solve_rows(c, vm, c->Vhat.as<double>(), c->U, r);
+  c->Vhat_n = n;
+  c->Vhat_r = r;
+  c->U_m = m;
+  c->U_r = r;
+  c->oriented_T = false;
+  rep->underdetermined_rows = us.flagged;
+  rep->e = std::sqrt(us.ss) / std::sqrt((double)c->known);  // masked_residual_norm, core.cpp:35-39
+  if (Uout) ck(cudaMemcpyAsync(Uout, c->U.p, sizeof(double) * m * r, cudaMemcpyDeviceToHost, c->stream), "D2H U");
+  if (Vout) ck(cudaMemcpyAsync(Vout, c->Vhat.p, sizeof(double) * n * r, cudaMemcpyDeviceToHost, c->stream), "D2H V");
+  ck(cudaStreamSynchronize(c->stream), "als");
   rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
@@ -1010,6 +1063,22 @@ int rsm_ctx_solver_stats(rsm_ctx* c, double* out, int cap) {
 // ---- one-shot, reference-shaped calls ----
 rsm_status rsm_make_trial_params(const rsm_config* cfg, int64_t m, int64_t n, rsm_trial_params* out) {
   return guard(nullptr, [&] { *out = trial_params_impl(cfg, m, n); });
+}
+
+rsm_status rsm_ctx_als(rsm_ctx* c, int64_t r, int64_t iterations, uint64_t seed, double* U, double* V,
+                       rsm_report* rep) {
+  return guard(c, [&] { als_impl(c, r, iterations, seed, U, V, rep); });
+}
+
+rsm_status rsm_als(const double* values, const uint8_t* mask, int64_t m, int64_t n, int64_t r, int64_t iterations,
+                   uint64_t seed, double* U, double* V, rsm_report* rep) {
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  st = rsm_ctx_load(c, values, mask, m, n);
+  if (!st) st = rsm_ctx_als(c, r, iterations, seed, U, V, rep);
+  if (st) g_err = c->err;
+  return st;
 }
 
 rsm_status rsm_decompose(const double* values, const uint8_t* mask, int64_t m, int64_t n, const rsm_config* cfg,

@@ -13,35 +13,10 @@
 #include <vector>
 
 #include "../../include/rsm_b200.h"
+#include "host_rng.h"
 
 namespace {
-
-inline uint64_t mix(uint64_t z) {
-  z ^= z >> 30;
-  z *= 0xbf58476d1ce4e5b9ull;
-  z ^= z >> 27;
-  z *= 0x94d049bb133111ebull;
-  z ^= z >> 31;
-  return z;
-}
-struct Rng {
-  uint64_t s;
-  Rng(uint64_t seed, uint64_t tag, uint64_t index) {
-    s = mix(seed + 0x9e3779b97f4a7c15ull * tag);
-    s = mix(s + 0xbf58476d1ce4e5b9ull * index);
-  }
-  uint64_t next_u64() {
-    s += 0x9e3779b97f4a7c15ull;
-    return mix(s);
-  }
-  double next_unit() { return (static_cast<double>(next_u64() >> 11) + 0.5) * 0x1.0p-53; }
-  double next_normal() {
-    const double u1 = next_unit();
-    const double u2 = next_unit();
-    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2);
-  }
-};
-
+using rsmh::Rng;
 }  // namespace
 
 extern "C" rsm_status rsm_generate(int64_t m, int64_t n, int64_t r, double rho, double sigma,

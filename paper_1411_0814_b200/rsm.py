@@ -90,6 +90,7 @@ def lib():
         "rsm_ctx_load": (i32, [_P, _P, _P, i64, i64]),
         "rsm_ctx_load_device": (i32, [_P, _P, _P, i64, i64]),
         "rsm_ctx_decompose": (i32, [_P, C.POINTER(_Config), _P, _P, C.POINTER(_Report)]),
+        "rsm_ctx_als": (i32, [_P, i64, i64, u64, _P, _P, C.POINTER(_Report)]),
         "rsm_ctx_fetch_factors": (i32, [_P, _P, _P]),
         "rsm_ctx_select": (i32, [_P, C.POINTER(_TrialParams), u64, _P, _P, C.POINTER(u64), C.POINTER(u64)]),
         "rsm_ctx_harvest_gram": (i32, [_P, C.POINTER(_TrialParams), u64, _P, C.POINTER(u64), C.POINTER(u64),
@@ -102,6 +103,7 @@ def lib():
         "rsm_ctx_solver_stats": (C.c_int, [_P, _P, C.c_int]),
         "rsm_make_trial_params": (i32, [C.POINTER(_Config), i64, i64, C.POINTER(_TrialParams)]),
         "rsm_decompose": (i32, [_P, _P, i64, i64, C.POINTER(_Config), _P, _P, C.POINTER(_Report)]),
+        "rsm_als": (i32, [_P, _P, i64, i64, i64, i64, u64, _P, _P, C.POINTER(_Report)]),
         "rsm_harvest_gram": (i32, [_P, _P, i64, i64, C.POINTER(_TrialParams), u64, _P, C.POINTER(u64),
                                    C.POINTER(u64), C.POINTER(u64)]),
         "rsm_solve_v": (i32, [_P, i64, i64, dbl, _P, C.POINTER(i64), C.POINTER(i32)]),
@@ -123,9 +125,9 @@ def lib():
 def exported_symbols():
     """Names the C-ABI header declares (used by the CPU symbol test)."""
     return ["rsm_config_default", "rsm_last_error", "rsm_ctx_create", "rsm_ctx_destroy", "rsm_nccl_unique_id",
-            "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_decompose", "rsm_ctx_fetch_factors",
+            "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_decompose", "rsm_ctx_fetch_factors", "rsm_ctx_als",
             "rsm_ctx_select", "rsm_ctx_harvest_gram", "rsm_ctx_solve_v", "rsm_ctx_solve_u", "rsm_ctx_stage_ms",
-            "rsm_ctx_launch_count", "rsm_ctx_last_load_h2d_bytes", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_harvest_gram", "rsm_solve_v",
+            "rsm_ctx_launch_count", "rsm_ctx_last_load_h2d_bytes", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_als", "rsm_harvest_gram", "rsm_solve_v",
             "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_fp64_peak_tflops",
             "rsm_dmma_peak_tflops", "rsm_shard_range"]
 
@@ -327,6 +329,15 @@ class Context:
         F = Factorization(self.m, self.n, r, U, V) if fetch else None
         return F, _report(rep)
 
+    def als(self, r: int, iterations: int, seed: int, fetch: bool = True):
+        """baseline_als on the loaded matrix (als.cpp:11-44) -> (Factorization, DecompositionReport)."""
+        U = np.empty((self.m, max(r, 1))) if fetch else None
+        V = np.empty((self.n, max(r, 1))) if fetch else None
+        rep = _Report()
+        _check(lib().rsm_ctx_als(self.h, r, iterations, seed, _ptr(U), _ptr(V), C.byref(rep)), self.h)
+        F = Factorization(self.m, self.n, r, U, V) if fetch else None
+        return F, _report(rep)
+
     def fetch_factors(self, r: int):
         U = np.empty((self.m, r))
         V = np.empty((self.n, r))
@@ -439,6 +450,17 @@ def decompose(M: MaskedMatrix, cfg: RsmConfig):
     c = cfg._c()
     _check(lib().rsm_decompose(_ptr(M.values), _ptr(M.mask), M.m, M.n, C.byref(c), _ptr(U), _ptr(V),
                                C.byref(rep)))
+    return Factorization(M.m, M.n, r, U, V), _report(rep)
+
+
+def baseline_als(M: MaskedMatrix, r: int, iterations: int, seed: int, workers: int = 0):
+    """rsm::baseline_als (solver.hpp:79-81, als.cpp:11-44) -> (Factorization, DecompositionReport).
+    `workers` is accepted for signature parity; the device decides its own parallelism."""
+    U = np.empty((M.m, max(r, 1)))
+    V = np.empty((M.n, max(r, 1)))
+    rep = _Report()
+    _check(lib().rsm_als(_ptr(M.values), _ptr(M.mask), M.m, M.n, r, iterations, seed, _ptr(U), _ptr(V),
+                         C.byref(rep)))
     return Factorization(M.m, M.n, r, U, V), _report(rep)
 
 

@@ -326,3 +326,28 @@ def test_host_packed_mask_matches_device_load():
         F2, r2 = c2.decompose(cfg)
         assert np.array_equal(F1.u, F2.u) and np.array_equal(F1.v, F2.v)
         assert r1.e == r2.e and r1.z == r2.z and r1.trials_accepted == r2.trials_accepted
+
+
+@pytest.mark.parametrize("case", [(2000, 200, 3, 0.8, 5, 0), (400, 900, 4, 0.6, 4, 9)])
+def test_baseline_als_matches_oracle(case):
+    # baseline_als on the device (stage-5 kernel on M and on its transpose)
+    # against the C restatement of als.cpp:11-44
+    m, n, r, rho, its, seed = case
+    M = gen(m, n, r, rho, 1e-3, seed)
+    F, rep = rsm.baseline_als(M, r, its, seed)
+    U_o, V_o, fl_o, e_o = O.als(M.values, M.mask, r, its, seed)
+    assert rep.underdetermined_rows == fl_o
+    assert rel_fro(F.u @ F.v.T, U_o @ V_o.T) <= UV_TOL
+    assert abs(rep.e - e_o) <= 1e-9 * e_o + 1e-12
+
+
+def test_baseline_als_validation():
+    M = gen(50, 20, 2, 0.7, 0.0, 1)
+    for r, its in [(0, 3), (20, 3), (2, 0)]:
+        with pytest.raises(rsm.Error) as ei:
+            rsm.baseline_als(M, r, its, 1)
+        assert ei.value.code == rsm.errc.invalid_config
+    M0 = rsm.MaskedMatrix(10, 5)
+    with pytest.raises(rsm.Error) as ei:
+        rsm.baseline_als(M0, 2, 3, 1)
+    assert ei.value.code == rsm.errc.insufficient_coverage

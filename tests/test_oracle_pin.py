@@ -205,6 +205,20 @@ def test_solve_u_vs_reference():
     assert np.abs(U - Ur).max() <= 1e-10
 
 
+@needs_ref
+@pytest.mark.parametrize("case", [(80, 20, 3, 0.7, 5, 11), (50, 70, 2, 0.5, 3, 4)])
+def test_als_vs_reference(case):
+    # baseline_als (als.cpp:11-44): seeded init, alternating row solves on M and M^T
+    m, n, r, rho, its, seed = case
+    from oracle.oracle import generate
+    Y, W = generate(m, n, r, rho, 1e-2, seed)
+    U, V, fl, e = O.als(Y, W, r, its, seed)
+    Ur, Vr, flr, er = R.als(Y, W, r, its, seed)
+    assert fl == flr
+    assert rel_fro(U @ V.T, Ur @ Vr.T) <= 1e-10
+    assert abs(e - er) <= 1e-10 * er
+
+
 def test_solve_u_reference_cases_on_oracle():
     # tests/test_solver.cpp:161-172 minimum norm (1, 1)
     u = np.zeros(2)
