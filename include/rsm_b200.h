@@ -17,6 +17,10 @@
  *   rsm_solve_u           <- rsm::solve_u              include/rsm/solver.hpp:74-75, src/solver.cpp:64-89
  *   rsm_masked_residual_norm <- rsm::masked_residual_norm include/rsm/core.hpp:94, src/core.cpp:35-39
  *   rsm_generate          <- rsm::generate (observed matrix only) include/rsm/synth.hpp:29, src/synth.cpp:12-57
+ *   rsm_ctx_als / rsm_als <- rsm::baseline_als         include/rsm/solver.hpp:79-81, src/als.cpp:11-44
+ *   rsm_load_matrix_csv   <- rsm::load_matrix          include/rsm/io.hpp:14, src/io.cpp:56-99
+ *   rsm_save_matrix_csv   <- rsm::save_matrix          include/rsm/io.hpp:18, src/io.cpp:101-116
+ *   rsm_dataset_checksum  <- rsm::dataset_checksum     include/rsm/io.hpp:22, src/io.cpp:140-154
  *
  * Host buffers are caller-owned; device memory is owned by the context.
  * Calls are synchronous on return, one host thread per context. Matrices
@@ -185,6 +189,29 @@ rsm_status rsm_dmma_peak_tflops(int device, double* tflops);
  * rows [row0, row0+rows) of an m x n instance; multithreaded. */
 rsm_status rsm_generate(int64_t m, int64_t n, int64_t r, double rho, double sigma, uint64_t seed,
                         int64_t row0, int64_t rows, double* values, uint8_t* mask);
+
+/* Structured-missingness generator (BASELINE config 5; no reference
+ * counterpart): affine-camera tracks, points x (2 frames)
+ * columns, rank 4, each point visible over one contiguous frame window of
+ * length uniform in [wmin, wmax]; rows [row0, row0+rows). The streams are
+ * documented in src synth.cpp and DESIGN.md. */
+rsm_status rsm_generate_tracks(int64_t points, int64_t frames, int64_t wmin, int64_t wmax, double sigma,
+                               uint64_t seed, int64_t row0, int64_t rows, double* values, uint8_t* mask);
+
+/* ------------------------------------------------------------- loader */
+/* NaN-CSV masked matrix (rsm::load_matrix, io.cpp:56-99): one row per line,
+ * empty or "nan" (any case) cells hidden. *values (m x n, NaN at hidden
+ * cells) and *mask (m x n) are malloc'd by the library; release them with
+ * rsm_free. Parse failures return RSM_ERR_PARSE_IO with the reference's
+ * messages. */
+rsm_status rsm_load_matrix_csv(const char* path, double** values, uint8_t** mask, int64_t* m, int64_t* n);
+/* rsm::save_matrix (io.cpp:101-116): hidden cells as NaN, %.17g values. */
+rsm_status rsm_save_matrix_csv(const char* path, const double* values, const uint8_t* mask, int64_t m,
+                               int64_t n);
+/* rsm::dataset_checksum (io.cpp:140-154): FNV-1a over dims, mask, values. */
+rsm_status rsm_dataset_checksum(const double* values, const uint8_t* mask, int64_t m, int64_t n,
+                                uint64_t* out);
+void rsm_free(void* p);
 
 #ifdef __cplusplus
 }

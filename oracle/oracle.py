@@ -75,6 +75,7 @@ def lib():
         L.orc_decompose.restype = C.c_int
         L.orc_decompose.argtypes = [P, P, i64, i64, C.POINTER(Config), P, P, C.POINTER(Report)]
         L.orc_generate_rows.argtypes = [i64, i64, i64, d, d, u64, i64, i64, P, P]
+        L.orc_generate_tracks.argtypes = [i64, i64, i64, i64, d, u64, P, P]
         L.orc_als.restype = C.c_int
         L.orc_als.argtypes = [P, P, i64, i64, i64, i64, u64, P, P, C.POINTER(i64), C.POINTER(d)]
         _lib = L
@@ -168,6 +169,13 @@ def solve_u(Y, mask, V, r):
     _chk(lib().orc_solve_u(_p(np.ascontiguousarray(Y)), _p(np.ascontiguousarray(mask, np.uint8)), m, n,
                            _p(np.ascontiguousarray(V, np.float64)), r, _p(U), C.byref(fl)))
     return U, fl.value
+
+
+def generate_tracks(points, frames, wmin, wmax, sigma, seed):
+    Y = np.zeros((points, 2 * frames))
+    W = np.zeros((points, 2 * frames), np.uint8)
+    lib().orc_generate_tracks(points, frames, wmin, wmax, sigma, seed, _p(Y), _p(W))
+    return Y, W
 
 
 def als(Y, mask, r, iterations, seed):

@@ -761,3 +761,35 @@ void orc_generate_rows(int64_t m, int64_t n, int64_t r, double rho, double sigma
   free(a);
   free(B);
 }
+
+
+void orc_generate_tracks(int64_t points, int64_t frames, int64_t wmin, int64_t wmax, double sigma,
+                         uint64_t seed, double* Y, uint8_t* W) {
+  const int64_t n = 2 * frames;
+  for (int64_t i = 0; i < points; ++i) {
+    uint64_t sp = orc_rng_state(seed, 16 /* TRACK_POINT */, (uint64_t)i);
+    const double X[4] = {2.0 * orc_next_unit(&sp) - 1.0, 2.0 * orc_next_unit(&sp) - 1.0,
+                         2.0 * orc_next_unit(&sp) - 1.0, 1.0};
+    uint64_t sw = orc_rng_state(seed, 18 /* TRACK_WINDOW */, (uint64_t)i);
+    const int64_t L = wmin + (int64_t)orc_next_below(&sw, (uint64_t)(wmax - wmin + 1));
+    const int64_t f0 = (int64_t)orc_next_below(&sw, (uint64_t)(frames - L + 1));
+    uint64_t sn = orc_rng_state(seed, 19 /* TRACK_NOISE */, (uint64_t)i);
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t f = j / 2;
+      if (f < f0 || f >= f0 + L) {
+        Y[i * n + j] = NAN;
+        W[i * n + j] = 0;
+        continue;
+      }
+      /* camera row (j % 2) of frame f: entries 4*(j%2) .. +3 of the frame's stream */
+      uint64_t sc = orc_rng_state(seed, 17 /* TRACK_CAMERA */, (uint64_t)f);
+      double P[8];
+      for (int q = 0; q < 8; ++q) P[q] = orc_next_normal(&sc);
+      double s = 0.0;
+      for (int q = 0; q < 4; ++q) s += P[(j % 2) * 4 + q] * X[q];
+      if (sigma > 0.0) s += sigma * orc_next_normal(&sn);
+      Y[i * n + j] = s;
+      W[i * n + j] = 1;
+    }
+  }
+}

@@ -131,6 +131,11 @@ int orc_decompose(const double* Y, const uint8_t* mask, int64_t m, int64_t n,
 /* synth.cpp:12-71 restricted to the observed matrix (Y and mask), for a row
  * block [row0, row0+rows). Y hidden cells are NaN. A is m x r, B r x n are
  * generated by the callee from the per-row streams. */
+/* config-5 track generator restated from its specification (this library's
+ * rsm_generate_tracks; the reference has no counterpart). */
+void orc_generate_tracks(int64_t points, int64_t frames, int64_t wmin, int64_t wmax, double sigma,
+                         uint64_t seed, double* Y, uint8_t* W);
+
 void orc_generate_rows(int64_t m, int64_t n, int64_t r, double rho, double sigma, uint64_t seed,
                        int64_t row0, int64_t rows, double* Y, uint8_t* mask);
 

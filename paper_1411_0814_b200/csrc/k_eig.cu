@@ -22,6 +22,7 @@
 // fixed order, so the result is bitwise reproducible. When n <= 16 the block
 // is the whole space and a single Rayleigh-Ritz step is the exact
 // eigendecomposition.
+#include <algorithm>
 #include <cooperative_groups.h>
 
 #include "rsm_internal.h"
@@ -369,6 +370,16 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   int buf = 0;
   int matvecs = 0;
   const bool full = (b >= n);  // block = whole space
+  if (a.zero_rows && *a.zero_rows > r) {
+    // more than r exact zero eigenvalues: the rank gate fails (solver.cpp:34-39)
+    if (blockIdx.x == 0 && tid == 0) {
+      a.istat[0] = 3;
+      a.istat[3] = 0;
+      a.istat[4] = 0;
+      for (int i = 0; i < 16; ++i) a.dstat[i] = 0.0;
+    }
+    return;
+  }
   // dynamic shared memory: [own rows of X, Y, Z][G rows when resident][iterate chunk]
   const int nr = row_hi - row_lo;
   const int own = ((a.rows_per_cta * ld) + 1) & ~1;
@@ -605,6 +616,17 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     // resolved against the rank-gate thresholds: either converged too, or
     // clearly above 10 tol lambda_max (eigenvalues that small are amplified by
     // the filter exactly like the wanted ones, so they would be in the block)
+    // Coverage certificate: Ritz values bound the eigenvalues from above
+    // (lambda_k <= theta_k, Rayleigh-Ritz interlacing), and the power-column
+    // estimate bounds lambda_max from below, so theta_{r+1} <= tol * lmax
+    // proves at least r+1 eigenvalues at or below the reference's threshold:
+    // the rank gate of solver.cpp:34-39 fails, whatever the rest of the
+    // spectrum (e.g. columns no trial covered give exact zero eigenvalues).
+    if (!full && r < b && lmax > 0.0 && sh.theta[r] <= a.tol * lmax) {
+      status = 3;
+      ++outer;
+      break;
+    }
     maxres = 0.0;
     for (int j = 0; j < r && j < b; ++j) maxres = fmax(maxres, sqrt(sh.red[j]));
     bool sep = true;
@@ -626,7 +648,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     if (!(acut < 0.999 * ub)) acut = 0.999 * ub;
     if (acut <= 0.0) acut = 1e-6 * ub;
   }
-  if (status != 0 && maxres <= 1e-9 * ub) status = 0;  // converged to a looser bound
+  if (status == 1 && maxres <= 1e-9 * ub) status = 0;  // converged to a looser bound
   // ---- outputs ----
   for (int q = tid; q < nr * r; q += ET) {
     const int lr = q / r, j = q % r;
@@ -647,6 +669,27 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     a.dstat[12] = (double)sync_cyc;
   }
 #undef EIG_T
+}
+
+// Exactly-zero rows of G (columns no trial covered: count 0 when G is our
+// harvest, else rows whose n entries are all 0.0) are exact zero eigenvalues;
+// more than r of them fail the reference's rank gate outright.
+__global__ void k_zero_rows(const double* __restrict__ G, int64_t n, const int* __restrict__ cnt,
+                            int* __restrict__ out) {
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int nw = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+  int z = 0;
+  for (int64_t i = warp; i < n; i += nw) {
+    bool zero;
+    if (cnt) zero = cnt[i] == 0;
+    else {
+      bool nz = false;
+      for (int64_t k = lane; k < n; k += 32) nz |= G[i * n + k] != 0.0;
+      zero = !__any_sync(0xffffffffu, nz);
+    }
+    z += zero ? 1 : 0;
+  }
+  if (lane == 0 && z) atomicAdd(out, z);
 }
 
 // sign fix (solver.cpp:47-60): the largest-magnitude entry of each column is
@@ -708,6 +751,12 @@ cudaError_t launch_eig(const EigArgs& a0, int grid, cudaStream_t s) {
   }
   cudaFuncSetAttribute(k_eig<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_BYTES);
   return cudaLaunchCooperativeKernel((void*)k_eig<17>, dim3(grid), dim3(ET), args, dyn, s);
+}
+
+void launch_zero_rows(const double* G, int64_t n, const int* cnt, int* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(int), s);
+  int blocks = (int)std::min<int64_t>(148 * 4, (n + 7) / 8);
+  k_zero_rows<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(G, n, cnt, out);
 }
 
 void launch_sign_fix(double* V, int64_t n, int r, cudaStream_t s) {

@@ -561,6 +561,9 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   a.dstat = c->eD.as<double>();
   a.max_outer = 60;
   a.cnt = c->G_harvest ? c->colcnt.as<int>() : nullptr;
+  a.zero_rows = c->eI.as<int>() + 7;
+  rsmk::launch_zero_rows(a.G, n, a.cnt, c->eI.as<int>() + 7, c->stream);
+  ++c->launches;
   ck(rsmk::launch_eig(a, grid, c->stream), "cooperative eig launch");
   rsmk::launch_sign_fix(c->Vhat.as<double>(), n, (int)r, c->stream);
   c->launches += 2;
@@ -584,6 +587,9 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   c->solver_stats[14] = dstat[10];  // and their cycles
   c->solver_stats[15] = dstat[11];  // filter matvec cycles (CTA 0)
   for (int i = 0; i < 8; ++i) c->solver_stats[16 + i] = dstat[16 + i];  // CholQR sub-phase cycles
+  if (istat[0] == 3)  // certified: more than r eigenvalues at or below tol * lambda_max
+    fail(RSM_ERR_INSUFFICIENT_COVERAGE,
+         "rank gate failed: constraint coverage below n-r; raise the trial count or epsilon");
   if (istat[0] != 0) fail(RSM_ERR_INTERNAL, "symmetric eigensolver failed to converge");
   c->Vhat_n = n;
   c->Vhat_r = r;
@@ -846,6 +852,14 @@ void rsm_config_default(rsm_config* cfg) {
 }
 
 const char* rsm_last_error(const rsm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+}  // extern "C"
+
+namespace rsmk {
+void set_host_error(const std::string& msg) { g_err = msg; }
+}  // namespace rsmk
+
+extern "C" {
 
 rsm_status rsm_ctx_create(rsm_ctx** out, int device, int world, int rank, const void* nccl_id) {
   return guard(nullptr, [&] {

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 namespace rsmk {
@@ -61,6 +62,7 @@ struct EigArgs {
   int rpw;          // rows per warp
   int gres;         // set by launch_eig: G rows resident in shared memory
   int kc;           // set by launch_eig: iterate rows staged per bulk copy
+  const int* zero_rows;  // exactly-zero rows of G (k_zero_rows), or null
   double* X;        // n x ld  (3 buffers)
   double* Y;
   double* Z;
@@ -84,6 +86,9 @@ struct SolveUArgs {
   int* flagged;     // count (integer atomics)
   int r;
 };
+
+// rsm_ctx.cu: message for rsm_last_error(NULL) from host-only entry points
+void set_host_error(const std::string& msg);
 
 // k_prep.cu
 void launch_pack_rows(const uint8_t* mask, int64_t m, int64_t n, uint32_t* bits, int64_t nwp,
@@ -119,6 +124,7 @@ int eig_part_width(int b);
 cudaError_t launch_eig(const EigArgs& a, int grid, cudaStream_t s);
 int eig_max_grid();
 void launch_sign_fix(double* V, int64_t n, int r, cudaStream_t s);
+void launch_zero_rows(const double* G, int64_t n, const int* cnt, int* out, cudaStream_t s);
 // k_solve_u.cu
 void launch_solve_u(const SolveUArgs& a, cudaStream_t s);
 void launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s);

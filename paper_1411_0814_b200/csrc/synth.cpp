@@ -67,3 +67,67 @@ extern "C" rsm_status rsm_generate(int64_t m, int64_t n, int64_t r, double rho, 
   for (auto& x : th) x.join();
   return RSM_OK;
 }
+
+// Structured-missingness generator for BASELINE config 5 (SURVEY.md section
+// 8(f) row 1; the reference has none, SPEC.md:448 lists it as a non-goal).
+// An affine-camera track matrix: point i is X_i = (x, y, z, 1) with x, y, z
+// uniform in [-1, 1] (Rng(seed, TRACK_POINT, i).next_unit), frame f has a
+// 2 x 4 camera P_f with N(0,1) entries (Rng(seed, TRACK_CAMERA, f), row-major),
+// so the noiseless matrix Y[i][2f + c] = P_f[c] . X_i has rank 4. Point i is
+// visible over one contiguous window of frames: length L uniform in
+// [wmin, wmax] and start uniform in [0, frames - L] (Rng(seed, TRACK_WINDOW,
+// i).next_below, length first). Visible cells get sigma * N(0,1) noise from
+// Rng(seed, TRACK_NOISE, i), drawn in column order; hidden cells hold NaN.
+extern "C" rsm_status rsm_generate_tracks(int64_t points, int64_t frames, int64_t wmin, int64_t wmax,
+                                          double sigma, uint64_t seed, int64_t row0, int64_t rows,
+                                          double* values, uint8_t* mask) {
+  if (points < 1 || frames < 1 || wmin < 1 || wmax < wmin || wmax > frames || row0 < 0 || rows < 0 ||
+      row0 + rows > points)
+    return RSM_ERR_INVALID_CONFIG;
+  const int64_t n = 2 * frames;
+  std::vector<double> P((size_t)(frames * 8));
+  for (int64_t f = 0; f < frames; ++f) {
+    rsmh::Rng rc(seed, rsmh::stream::TRACK_CAMERA, (uint64_t)f);
+    for (int q = 0; q < 8; ++q) P[(size_t)(f * 8 + q)] = rc.next_normal();
+  }
+  unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (rows * n < (int64_t)1 << 20) nt = 1;
+  auto work = [&](int64_t lo, int64_t hi) {
+    for (int64_t t = lo; t < hi; ++t) {
+      const int64_t i = row0 + t;
+      double* y = values + t * n;
+      uint8_t* w = mask + t * n;
+      rsmh::Rng rp(seed, rsmh::stream::TRACK_POINT, (uint64_t)i);
+      double X[4];
+      for (int q = 0; q < 3; ++q) X[q] = 2.0 * rp.next_unit() - 1.0;
+      X[3] = 1.0;
+      rsmh::Rng rw(seed, rsmh::stream::TRACK_WINDOW, (uint64_t)i);
+      const int64_t L = wmin + (int64_t)rw.next_below((uint64_t)(wmax - wmin + 1));
+      const int64_t f0 = (int64_t)rw.next_below((uint64_t)(frames - L + 1));
+      rsmh::Rng rn(seed, rsmh::stream::TRACK_NOISE, (uint64_t)i);
+      for (int64_t j = 0; j < n; ++j) {
+        const int64_t f = j >> 1;
+        if (f < f0 || f >= f0 + L) {
+          y[j] = std::nan("");
+          w[j] = 0;
+          continue;
+        }
+        const double* pr = P.data() + f * 8 + (j & 1) * 4;
+        double s = 0.0;
+        for (int q = 0; q < 4; ++q) s += pr[q] * X[q];
+        if (sigma > 0.0) s += sigma * rn.next_normal();
+        y[j] = s;
+        w[j] = 1;
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  const int64_t per = (rows + nt - 1) / nt;
+  for (unsigned t = 0; t < nt; ++t) {
+    const int64_t lo = t * per, hi = std::min<int64_t>(rows, lo + per);
+    if (lo >= hi) break;
+    th.emplace_back(work, lo, hi);
+  }
+  for (auto& x : th) x.join();
+  return RSM_OK;
+}

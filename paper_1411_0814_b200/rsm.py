@@ -110,6 +110,11 @@ def lib():
         "rsm_solve_u": (i32, [_P, _P, i64, i64, _P, i64, _P, C.POINTER(i64)]),
         "rsm_masked_residual_norm": (i32, [_P, _P, i64, i64, _P, _P, i64, C.POINTER(dbl)]),
         "rsm_generate": (i32, [i64, i64, i64, dbl, dbl, u64, i64, i64, _P, _P]),
+        "rsm_generate_tracks": (i32, [i64, i64, i64, i64, dbl, u64, i64, i64, _P, _P]),
+        "rsm_load_matrix_csv": (i32, [C.c_char_p, C.POINTER(_P), C.POINTER(_P), C.POINTER(i64), C.POINTER(i64)]),
+        "rsm_save_matrix_csv": (i32, [C.c_char_p, _P, _P, i64, i64]),
+        "rsm_dataset_checksum": (i32, [_P, _P, i64, i64, C.POINTER(u64)]),
+        "rsm_free": (None, [_P]),
         "rsm_fp64_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
         "rsm_dmma_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
         "rsm_shard_range": (None, [i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]),
@@ -128,7 +133,8 @@ def exported_symbols():
             "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_decompose", "rsm_ctx_fetch_factors", "rsm_ctx_als",
             "rsm_ctx_select", "rsm_ctx_harvest_gram", "rsm_ctx_solve_v", "rsm_ctx_solve_u", "rsm_ctx_stage_ms",
             "rsm_ctx_launch_count", "rsm_ctx_last_load_h2d_bytes", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_als", "rsm_harvest_gram", "rsm_solve_v",
-            "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_fp64_peak_tflops",
+            "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_generate_tracks", "rsm_load_matrix_csv",
+            "rsm_save_matrix_csv", "rsm_dataset_checksum", "rsm_free", "rsm_fp64_peak_tflops",
             "rsm_dmma_peak_tflops", "rsm_shard_range"]
 
 
@@ -507,3 +513,50 @@ def generate(m: int, n: int, r: int, rho: float, sigma: float, seed: int, row0: 
     if st:
         raise Error(st, "synthetic spec out of range")
     return MaskedMatrix(rows, n, Y, W)
+
+
+def generate_tracks(points: int, frames: int, wmin: int, wmax: int, sigma: float, seed: int, row0: int = 0,
+                    rows: int | None = None) -> MaskedMatrix:
+    """Structured-missingness instance of BASELINE config 5 (affine-camera
+    tracks, rank 4, one contiguous visibility window per point; the streams
+    are documented at rsm_generate_tracks in synth.cpp), rows [row0, row0+rows)."""
+    rows = points - row0 if rows is None else rows
+    Y = np.empty((rows, 2 * frames))
+    W = np.empty((rows, 2 * frames), np.uint8)
+    st = lib().rsm_generate_tracks(points, frames, wmin, wmax, sigma, seed, row0, rows, _ptr(Y), _ptr(W))
+    if st:
+        raise Error(st, "track spec out of range")
+    return MaskedMatrix(rows, 2 * frames, Y, W)
+
+
+def load_matrix(path: str) -> MaskedMatrix:
+    """rsm::load_matrix (io.cpp:56-99): NaN-CSV -> MaskedMatrix."""
+    pv, pm = C.c_void_p(), C.c_void_p()
+    m, n = C.c_int64(), C.c_int64()
+    st = lib().rsm_load_matrix_csv(os.fsencode(path), C.byref(pv), C.byref(pm), C.byref(m), C.byref(n))
+    if st:
+        raise Error(st, lib().rsm_last_error(None).decode())
+    try:
+        cnt = m.value * n.value
+        Y = np.ctypeslib.as_array(C.cast(pv, C.POINTER(C.c_double)), (cnt,)).copy().reshape(m.value, n.value)
+        W = np.ctypeslib.as_array(C.cast(pm, C.POINTER(C.c_uint8)), (cnt,)).copy().reshape(m.value, n.value)
+    finally:
+        lib().rsm_free(pv)
+        lib().rsm_free(pm)
+    return MaskedMatrix(m.value, n.value, Y, W)
+
+
+def save_matrix(M: MaskedMatrix, path: str) -> None:
+    """rsm::save_matrix (io.cpp:101-116): hidden cells as NaN, %.17g values."""
+    st = lib().rsm_save_matrix_csv(os.fsencode(path), _ptr(M.values), _ptr(M.mask), M.m, M.n)
+    if st:
+        raise Error(st, lib().rsm_last_error(None).decode())
+
+
+def dataset_checksum(M: MaskedMatrix) -> int:
+    """rsm::dataset_checksum (io.cpp:140-154)."""
+    out = C.c_uint64()
+    st = lib().rsm_dataset_checksum(_ptr(M.values), _ptr(M.mask), M.m, M.n, C.byref(out))
+    if st:
+        raise Error(st, lib().rsm_last_error(None).decode())
+    return int(out.value)

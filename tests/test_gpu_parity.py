@@ -351,3 +351,44 @@ def test_baseline_als_validation():
     with pytest.raises(rsm.Error) as ei:
         rsm.baseline_als(M0, 2, 3, 1)
     assert ei.value.code == rsm.errc.insufficient_coverage
+
+
+# ------------------------------------------- config 5: structured missingness
+
+def test_config5_tracks_coverage_failure_matches_oracle():
+    # BASELINE config 5 shape at reduced size: edge frames are seen by too few
+    # points for any 5-point probe to cover them, so G has exact zero rows and
+    # the rank gate (solver.cpp:34-39) fails with insufficient_coverage, on the
+    # device exactly as in the oracle (dsyev on the oracle's G)
+    M = rsm.generate_tracks(2048, 256, 32, 128, 1e-3, 0)
+    cfg = rsm.RsmConfig(rank=4, mode=rsm.Mode.M2, block=5, plan=rsm.TrialPlan(2048), seed=0)
+    with pytest.raises(O.OracleError) as eo:
+        O.decompose(M.values, M.mask, 4, 2048, mode=1, block=5, seed=0)
+    with pytest.raises(rsm.Error) as ed:
+        rsm.decompose(M, cfg)
+    assert eo.value.code == ed.value.code == rsm.errc.insufficient_coverage
+    assert "rank gate failed" in str(ed.value)
+
+
+def test_config5_tracks_covered_matches_oracle():
+    # wide windows cover every frame: the gate passes and the decomposition of
+    # the structured instance matches the oracle
+    M = rsm.generate_tracks(1500, 48, 40, 48, 1e-3, 3)
+    cfg = rsm.RsmConfig(rank=4, mode=rsm.Mode.M2, block=5, plan=rsm.TrialPlan(1500), seed=3)
+    F, rep = _e2e(M, cfg)
+    assert rep.gram_rank >= 96 - 4
+
+
+def test_solve_v_zero_rows_fail_the_gate():
+    # a caller-supplied accumulator with more than r all-zero rows
+    rng = np.random.default_rng(8)
+    A = rng.standard_normal((40, 40))
+    G = A @ A.T
+    for j in (3, 9, 17, 22, 31, 38):
+        G[j, :] = 0.0
+        G[:, j] = 0.0
+    with pytest.raises(O.OracleError) as eo:
+        O.solve_v(G, 4)
+    with pytest.raises(rsm.Error) as ed:
+        rsm.solve_v(G, 4, 1e-9)
+    assert eo.value.code == ed.value.code == rsm.errc.insufficient_coverage
