@@ -284,4 +284,47 @@ inline double masked_residual_norm(const MaskedMatrix& M, const Factorization& F
   return e;
 }
 
+// baseline_als (include/rsm/solver.hpp:79-81): the device ALS baseline
+inline std::pair<Factorization, DecompositionReport> baseline_als(const MaskedMatrix& M, index_t r,
+                                                                  index_t iterations, std::uint64_t seed,
+                                                                  int workers = 0) {
+  (void)workers;
+  const index_t rr = r > 0 ? r : 1;
+  std::vector<double> U(static_cast<std::size_t>(M.m * rr)), V(static_cast<std::size_t>(M.n * rr));
+  rsm_report rep;
+  detail::check(rsm_als(M.values.data(), M.mask.data(), M.m, M.n, r, iterations, seed, U.data(), V.data(), &rep));
+  Factorization F(M.m, M.n, r);
+  F.u = std::move(U);
+  F.v = std::move(V);
+  DecompositionReport d;
+  d.e = rep.e;
+  d.underdetermined_rows = rep.underdetermined_rows;
+  d.wall_time = rep.wall_time;
+  return {std::move(F), d};
+}
+
+// load_matrix / save_matrix / dataset_checksum (include/rsm/io.hpp:14-22)
+inline MaskedMatrix load_matrix(const std::string& path) {
+  double* v = nullptr;
+  std::uint8_t* w = nullptr;
+  std::int64_t m = 0, n = 0;
+  detail::check(rsm_load_matrix_csv(path.c_str(), &v, &w, &m, &n));
+  MaskedMatrix M(m, n);
+  std::copy(v, v + m * n, M.values.begin());
+  std::copy(w, w + m * n, M.mask.begin());
+  rsm_free(v);
+  rsm_free(w);
+  return M;
+}
+
+inline void save_matrix(const MaskedMatrix& M, const std::string& path) {
+  detail::check(rsm_save_matrix_csv(path.c_str(), M.values.data(), M.mask.data(), M.m, M.n));
+}
+
+inline std::uint64_t dataset_checksum(const MaskedMatrix& M) {
+  std::uint64_t h = 0;
+  detail::check(rsm_dataset_checksum(M.values.data(), M.mask.data(), M.m, M.n, &h));
+  return h;
+}
+
 }  // namespace rsm

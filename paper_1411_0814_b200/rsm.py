@@ -187,8 +187,12 @@ class MaskedMatrix:
 
 @dataclass
 class TrialPlan:
+    """rsm::TrialPlan (include/rsm/planner.hpp:12-16); the device path runs
+    explicit counts, `source` is recorded in the run report."""
+
     trials: int = 0
     epsilon: float = 0.99
+    source: str = "explicit"
 
 
 @dataclass

@@ -4,6 +4,7 @@
 // underneath. Exit code 0 = all checks passed.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "rsm_gpu/rsm.hpp"
@@ -138,6 +139,17 @@ int main() {
     cfg.workers = 3;
     const auto [F2, r2] = decompose(M, cfg);
     CHECK(F1.u == F2.u && F1.v == F2.v && r1.e == r2.e && r1.z == r2.z);
+  }
+  {  // baseline_als (als.cpp:11-44) and the loader path (io.hpp:14-22)
+    const MaskedMatrix M = synth(200, 40, 3, 0.7, 1e-3, 21);
+    const auto [F, rep] = baseline_als(M, 3, 5, 21);
+    CHECK(F.u.size() == 200 * 3 && std::fabs(rep.e - masked_residual_norm(M, F)) <= 1e-12 * rep.e + 1e-15);
+    CHECK_THROWS_CODE(baseline_als(M, 0, 5, 1), errc::invalid_config);
+    save_matrix(M, "dropin_io.csv");
+    const MaskedMatrix R = load_matrix("dropin_io.csv");
+    CHECK(R.m == M.m && R.n == M.n && R.mask == M.mask && dataset_checksum(R) == dataset_checksum(M));
+    std::remove("dropin_io.csv");
+    CHECK_THROWS_CODE(load_matrix("no_such_file_anywhere.csv"), errc::parse_io);
   }
   std::printf("dropin: %d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;

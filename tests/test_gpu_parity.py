@@ -392,3 +392,24 @@ def test_solve_v_zero_rows_fail_the_gate():
     with pytest.raises(rsm.Error) as ed:
         rsm.solve_v(G, 4, 1e-9)
     assert eo.value.code == ed.value.code == rsm.errc.insufficient_coverage
+
+
+def test_run_report_reproducible(tmp_path):
+    # tests/test_cli.cpp:78-105 of the reference, through the library: the
+    # instance saved to CSV and loaded back decomposes to the same artifacts
+    # and reports (wall_time aside) on every run
+    from paper_1411_0814_b200 import report as RP
+    M = gen(60, 20, 2, 0.7, 0.2, 9)
+    p = str(tmp_path / "d.csv")
+    rsm.save_matrix(M, p)
+    L = rsm.load_matrix(p)
+    cfg = rsm.RsmConfig(rank=2, mode=rsm.Mode.M2, plan=rsm.TrialPlan(300), seed=4)
+    reps = []
+    for _ in range(2):
+        F, rep = rsm.decompose(L, cfg)
+        rep.wall_time = 0.0
+        reps.append((F, RP.serialize_report(RP.make_report(cfg, rep, rsm.dataset_checksum(L)))))
+    assert np.array_equal(reps[0][0].u, reps[1][0].u) and np.array_equal(reps[0][0].v, reps[1][0].v)
+    assert reps[0][1] == reps[1][1]
+    r = RP.parse_report(reps[0][1])
+    assert r.checksum == rsm.dataset_checksum(M) and r.trials == 300 and r.trial_source == "explicit"
