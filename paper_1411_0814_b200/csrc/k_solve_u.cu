@@ -106,16 +106,23 @@ __host__ __device__ constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 *
 
 }  // namespace
 
-// One warp per row (rows strided over the grid's warps), two row buffers per
-// warp in shared memory. With BULK (even n) the next row's values and mask
-// words arrive by two 1-D bulk copies (TMA) on the buffer's mbarrier, issued
-// by one lane; otherwise by per-lane cp.async. V-hat sits in shared memory as
-// ceil(R/2) planes of (v_2p, v_2p+1) pairs (VSMEM) or is read from global.
-template <int R, bool VSMEM, bool BULK>
-__global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u(SolveUArgs a) {
-  constexpr int NP = (R + 1) / 2;           // V planes
-  constexpr int NA = R * (R + 1) / 2;       // packed normal matrix
-  constexpr int NV = pow2_at_least(NA + R + 1);  // reduced values (A, b, count, pad)
+// One warp per row (rows strided over the grid's warps). STAGE 1: two row
+// buffers per warp in shared memory, the next row's values and mask words
+// arriving by two 1-D bulk copies (TMA) on the buffer's mbarrier, issued by
+// one lane; STAGE 2: the same with per-lane cp.async (odd n); STAGE 0: no row
+// buffers, the warp reads its row straight from global memory (the second
+// pass re-reads it from L2) -- the layout when V-hat is too large to share
+// shared memory with row buffers (config 4: n = 2048, r = 8). V-hat sits in
+// shared memory as ceil(R/2) planes of (v_2p, v_2p+1) pairs (VSMEM) or is
+// read from global.
+template <int R, bool VSMEM, int STAGE>
+__global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUArgs a) {
+  constexpr bool BULK = STAGE == 1;
+  constexpr int NP = (R + 1) / 2;      // V planes
+  constexpr int NA = R * (R + 1) / 2;  // packed normal matrix
+  // reduced values (A, b, count): padded to a power of two for the halving
+  // reduction when small; reduced value by value for larger r
+  constexpr int NV = R <= 4 ? pow2_at_least(NA + R + 1) : NA + R + 1;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
@@ -186,12 +193,13 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u(SolveUArgs a) {
   unsigned phase = 0u;  // bit b: parity of buffer b's next completion
   int cur = 0;
   int64_t row = a.row_lo + gw;
-  if (row < a.row_hi) issue(row, 0);
+  if (STAGE && row < a.row_hi) issue(row, 0);
   const int nfull = (int)(n >> 5);
   for (; row < a.row_hi; row += nw) {
     const int64_t nxt = row + nw;
-    if (nxt < a.row_hi) issue(nxt, cur ^ 1);
-    if (BULK) {
+    if (STAGE && nxt < a.row_hi) issue(nxt, cur ^ 1);
+    if (STAGE == 0) {
+    } else if (BULK) {
       const unsigned bar = smem_u32(bars + 2 * warp + cur);
       unsigned done = 0;
       do {
@@ -207,8 +215,8 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u(SolveUArgs a) {
       else asm volatile("cp.async.wait_group 0;\n" ::);
       __syncwarp();
     }
-    const double* y = ybuf(cur);
-    const uint32_t* wd = reinterpret_cast<const uint32_t*>(y + npd);
+    const double* y = STAGE ? ybuf(cur) : a.Y + row * n;
+    const uint32_t* wd = STAGE ? reinterpret_cast<const uint32_t*>(y + npd) : a.bitsR + row * a.nwp;
     // normal equations over the observed cells; hidden cells are skipped by
     // predication (their NaN never enters arithmetic)
     double acc[NV];
@@ -245,13 +253,22 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u(SolveUArgs a) {
       for (int64_t w = lane; w < a.nwp; w += 32) cnt += __popc(wd[w]);
       acc[NA + R] = (double)cnt;
     }
-    warp_reduce_halving<NV>(acc, lane);
+    if (R <= 4) {
+      warp_reduce_halving<NV>(acc, lane);
+    } else {
+#pragma unroll
+      for (int p = 0; p < NV; ++p) acc[p] = warp_sum(acc[p]);
+    }
+    auto total = [&](int p) {
+      if constexpr (R <= 4) return warp_total<NV>(acc, p);
+      else return acc[p];
+    };
     double A[NA], bv[R];
 #pragma unroll
-    for (int p = 0; p < NA; ++p) A[p] = warp_total<NV>(acc, p);
+    for (int p = 0; p < NA; ++p) A[p] = total(p);
 #pragma unroll
-    for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, NA + i);
-    const int nj = (int)warp_total<NV>(acc, NA + R);
+    for (int i = 0; i < R; ++i) bv[i] = total(NA + i);
+    const int nj = (int)total(NA + R);
 
     double u[R];
     bool flagged = false;
@@ -376,19 +393,20 @@ void launch_residual(const double* Y, const uint32_t* bitsR, int64_t m, int64_t 
   k_residual<<<(unsigned)blocks, 256, 0, s>>>(Y, bitsR, m, n, nwp, U, V, r, rowres);
 }
 
-template <int R, bool VSMEM, bool BULK>
+template <int R, bool VSMEM, int STAGE>
 static void launch_solve_u_k(const SolveUArgs& a, size_t fixed, size_t per_warp, int sms, cudaStream_t s) {
-  // one CTA per SM with as many warps as the row buffers allow: V-hat is
-  // staged once per SM and every warp keeps two rows in flight
-  const size_t cap = 227 * 1024;
-  int w = (int)std::min<size_t>(SU_MAXW, (cap - fixed) / per_warp);
+  // one CTA per SM with as many warps as shared memory (row buffers) and the
+  // register budget allow: V-hat is staged once per SM
+  const size_t cap = 227 * 1024 - 2048;  // static shared memory of the kernel
+  const int wmax = R <= 4 ? SU_MAXW : 12;
+  int w = per_warp ? (int)std::min<size_t>(wmax, (cap - fixed) / per_warp) : wmax;
   if (w < 1) w = 1;
   const size_t smem = fixed + (size_t)w * per_warp;
-  cudaFuncSetAttribute(k_solve_u<R, VSMEM, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_solve_u<R, VSMEM, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t rows = a.row_hi - a.row_lo;
   int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
   if (blocks < 1) blocks = 1;
-  k_solve_u<R, VSMEM, BULK><<<(unsigned)blocks, w * 32, smem, s>>>(a);
+  k_solve_u<R, VSMEM, STAGE><<<(unsigned)blocks, w * 32, smem, s>>>(a);
 }
 
 template <int R>
@@ -401,16 +419,18 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
   const size_t vbytes = sizeof(double) * 2 * NP * (size_t)a.n;
   const size_t bufb = sizeof(double) * (size_t)(((a.n + 1) & ~int64_t(1)) + a.nwp / 2);
   const size_t per_warp = 2 * bufb;
-  // V-hat in shared memory when it leaves room for at least 8 warps
-  const bool vsm = head + vbytes + 8 * per_warp <= 227 * 1024;
+  const size_t cap = 227 * 1024 - 2048;
   const bool bulk = (a.n % 2) == 0;
-  const size_t fixed = head + (vsm ? vbytes : 0);
-  if (vsm) {
-    if (bulk) launch_solve_u_k<R, true, true>(a, fixed, per_warp, sms, s);
-    else launch_solve_u_k<R, true, false>(a, fixed, per_warp, sms, s);
+  if (head + vbytes + 8 * per_warp <= cap) {
+    // V-hat and >= 8 warps of staged rows
+    if (bulk) launch_solve_u_k<R, true, 1>(a, head + vbytes, per_warp, sms, s);
+    else launch_solve_u_k<R, true, 2>(a, head + vbytes, per_warp, sms, s);
+  } else if (head + vbytes <= cap) {
+    // V-hat alone fills shared memory: rows are read from global
+    launch_solve_u_k<R, true, 0>(a, head + vbytes, 0, sms, s);
   } else {
-    if (bulk) launch_solve_u_k<R, false, true>(a, fixed, per_warp, sms, s);
-    else launch_solve_u_k<R, false, false>(a, fixed, per_warp, sms, s);
+    if (bulk) launch_solve_u_k<R, false, 1>(a, head, per_warp, sms, s);
+    else launch_solve_u_k<R, false, 2>(a, head, per_warp, sms, s);
   }
 }
 
