@@ -146,6 +146,40 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     }
   }
   __syncthreads();
+  // A_all = V^T V (packed upper) for the dense-row complement (r > 4),
+  // summed in a fixed order: per-thread strided partials, then a fixed tree
+  __shared__ double Aall[NA];
+  if constexpr (R > 4) {
+    __shared__ double Ared[SU_MAXW][NA];
+    double part[NA];
+#pragma unroll
+    for (int p = 0; p < NA; ++p) part[p] = 0.0;
+    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+      double v[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) v[k] = a.V[c * R + k];
+      int p = 0;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = i; j < R; ++j) {
+          part[p] = fma(v[i], v[j], part[p]);
+          ++p;
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < NA; ++p) {
+      const double t = warp_sum(part[p]);
+      if (lane == 0) Ared[warp][p] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < NA) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t += Ared[w][threadIdx.x];
+      Aall[threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
   auto vload = [&](int64_t c, double* v) {
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -222,6 +256,13 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     double acc[NV];
 #pragma unroll
     for (int p = 0; p < NV; ++p) acc[p] = 0.0;
+    int cnt = 0;  // observed cells (mask words are zero beyond n)
+    for (int64_t w = lane; w < a.nwp; w += 32) cnt += __popc(wd[w]);
+    // r > 4 and at least half observed: V_O^T V_O = V^T V minus the hidden
+    // cells' outer products (walking only the hidden bits), which saves most
+    // of the r(r+1)/2 FMAs per cell
+    bool dense = false;
+    if constexpr (R > 4) dense = 2 * (int64_t)warp_sum_int(cnt) >= n;
     // branchless (so the loads of consecutive columns pipeline): a hidden
     // cell's basis row is scaled by 0 and its value selected away, so the NaN
     // stored there never enters arithmetic
@@ -229,17 +270,19 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
       double v[R];
       vload(c, v);
       const double yc = k ? y[c] : 0.0;
-      const double kf = k ? 1.0 : 0.0;
-      double t[R];
+      if (!dense) {
+        const double kf = k ? 1.0 : 0.0;
+        double t[R];
 #pragma unroll
-      for (int i = 0; i < R; ++i) t[i] = kf * v[i];
-      int p = 0;
+        for (int i = 0; i < R; ++i) t[i] = kf * v[i];
+        int p = 0;
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
+        for (int i = 0; i < R; ++i) {
 #pragma unroll
-        for (int j = i; j < R; ++j) {
-          acc[p] = fma(t[i], v[j], acc[p]);
-          ++p;
+          for (int j = i; j < R; ++j) {
+            acc[p] = fma(t[i], v[j], acc[p]);
+            ++p;
+          }
         }
       }
 #pragma unroll
@@ -248,11 +291,29 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
 #pragma unroll 2
     for (int w = 0; w < nfull; ++w) add(w * 32 + lane, (wd[w] >> lane) & 1u);
     if ((int64_t)nfull * 32 + lane < n) add(nfull * 32 + lane, (wd[nfull] >> lane) & 1u);
-    {
-      int cnt = 0;  // observed cells (mask words are zero beyond n)
-      for (int64_t w = lane; w < a.nwp; w += 32) cnt += __popc(wd[w]);
-      acc[NA + R] = (double)cnt;
+    if (dense) {
+      const int nwn = (int)((n + 31) >> 5);
+      for (int w = lane; w < nwn; w += 32) {
+        const int rem = (int)(n - (int64_t)w * 32);
+        const unsigned valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+        unsigned miss = ~wd[w] & valid;
+        while (miss) {
+          const int bpos = __ffs(miss) - 1;
+          miss &= miss - 1u;
+          double v[R];
+          vload((int64_t)w * 32 + bpos, v);
+          int p = 0;
+#pragma unroll
+          for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int j = i; j < R; ++j) {
+              acc[p] = fma(v[i], v[j], acc[p]);
+              ++p;
+            }
+        }
+      }
     }
+    acc[NA + R] = (double)cnt;
     if (R <= 4) {
       warp_reduce_halving<NV>(acc, lane);
     } else {
@@ -265,7 +326,7 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     };
     double A[NA], bv[R];
 #pragma unroll
-    for (int p = 0; p < NA; ++p) A[p] = total(p);
+    for (int p = 0; p < NA; ++p) A[p] = dense ? Aall[p] - total(p) : total(p);
 #pragma unroll
     for (int i = 0; i < R; ++i) bv[i] = total(NA + i);
     const int nj = (int)total(NA + R);
