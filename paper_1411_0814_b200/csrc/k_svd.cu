@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
           }
         }
         big = __any_sync(0xffffffffu, big);
-        const bool stop = !big || it >= 6;
+        const bool stop = !big || it >= a.max_outer;
         if (stop) {
           if (lane < K) sig[lane] = sqrt(fmax(gram[lane * KMAX + lane], 0.0));
         } else {
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
             ++p;
           }
       }
-      if (!big || it >= 6) break;  // warp-uniform
+      if (!big || it >= a.max_outer) break;  // warp-uniform
       {
         int p = 0;
 #pragma unroll

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -478,6 +479,11 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
       }
       a.Lpad = Lpad;
       a.use_smem = use_smem ? 1 : 0;
+      static const int svd_maxit = [] {
+        const char* e = getenv("RSM_SVD_MAXIT");
+        return e ? atoi(e) : 6;
+      }();
+      a.max_outer = svd_maxit;
       // row branch with k <= 9: warp-per-trial kernel; otherwise CTA per trial
       if (!(m2 && rsmk::launch_svd_warp(a, c->sms, c->stream))) rsmk::launch_svd(a, m2, (int)grid, smem, c->stream);
       ++c->launches;

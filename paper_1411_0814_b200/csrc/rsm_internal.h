@@ -37,6 +37,7 @@ struct SvdArgs {
   uint32_t* scratch_u32; // per-CTA 2*mwp words (column branch)
   int64_t Lpad;
   int use_smem;
+  int max_outer;         // one-sided Jacobi rotations per trial (at most)
 };
 
 struct GramArgs {
