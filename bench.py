@@ -179,6 +179,13 @@ def cpu_reference_sample(Y, W, c, G=None, trials_prefix=64, rows_sample=16384):
                 est_decompose_s=est)
 
 
+def arm_config(c, world):
+    """The `config` object both arms print (same workload, same keys)."""
+    return {"workload": c["workload"], "m": c["m"], "n": c["n"], "r": c["r"], "rho": c["rho"], "sigma": c["sigma"],
+            "k": c["k"], "trials": c["T"], "seed": c["seed"], "parallelism": f"trials+rows x{world}",
+            "l2": f"flushed (256 MiB write) between timed steps; Y ({c['m'] * c['n'] * 8 / 2**30:.2f} GiB) vs 126 MB L2"}
+
+
 def run_reference_arm(args, c):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -198,11 +205,11 @@ def run_reference_arm(args, c):
             vals.append(res)
     v = statistics.median([x["value"] for x in vals])
     est = statistics.median([x["est_decompose_s"] for x in vals])
-    line = {"metric": "submatrices/s (full RSM decompose)", "value": v, "unit": "submatrices/s", "n_gpus": 0,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": c["workload"], "m": m, "n": n, "r": c["r"], "rho": c["rho"], "k": c["k"],
-                       "trials": c["T"], "seed": c["seed"]},
+    line = {"metric": "submatrices/s (full RSM decompose)", "value": v, "unit": "submatrices/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator streams, seed 0)",
+            "config": arm_config(c, args.gpus),
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "submatrices/s", "cores": vals[0]["cores"], "kind": "reference",
                              "sample": vals[0]["sample"]},
@@ -361,9 +368,7 @@ def main():
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (reference generator streams, seed 0)",
-                "config": {"workload": c["workload"], "m": m, "n": n, "r": r, "rho": c["rho"], "sigma": c["sigma"],
-                           "k": c["k"], "trials": T, "seed": c["seed"], "parallelism": f"trials+rows x{world}",
-                           "l2": "flushed (256 MiB write) between timed steps; Y (1 GiB) exceeds L2"},
+                "config": arm_config(c, world),
                 "e2e": {"value": T / (e2e_ms / 1e3), "unit": "submatrices/s", "ms_per_step": e2e_ms,
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "roofline": roof, "stages": stage_info, "cpu_baseline": cpu, "clocks": clk,
