@@ -433,7 +433,11 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   // expanded vectors fit the buffer budget; stage 3 accumulates across chunks.
   const int64_t rp = (rex + 1) & ~1;
   const int64_t tbytes = npad * rp * (int64_t)sizeof(double);
-  const int64_t budget = (int64_t)6 << 30;
+  // RSM_CHUNK_BYTES overrides the budget (tests exercise the multi-chunk path)
+  static const int64_t budget = [] {
+    const char* e = getenv("RSM_CHUNK_BYTES");
+    return e ? std::max<int64_t>(1, atoll(e)) : ((int64_t)6 << 30);
+  }();
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(Tl, budget / tbytes));
   const int cpl = rsmk::gram_cols_per_lane(rex);
   build_tiles(c, npad, cpl);
