@@ -324,7 +324,12 @@ def main():
     stage_info["select"].update(alg_bytes=alg["s1_bytes"], gbs=alg["s1_bytes"] / (med[0] * 1e-3) / 1e9)
     stage_info["svd"].update(alg_flops=alg["s2_flops"], tflops=alg["s2_flops"] / (med[1] * 1e-3) / 1e12,
                              alg_bytes=alg["s2_bytes"], gbs=alg["s2_bytes"] / (med[1] * 1e-3) / 1e9)
-    stage_info["gram"].update(alg_flops=alg["s3_flops"], tflops=alg["s3_flops"] / (med[2] * 1e-3) / 1e12)
+    # SURVEY.md 8(d) S3 count, 2 r q^2 per trial (the roofline figure); the
+    # unique-entry count r q (q + 1) of the symmetric update is reported beside it
+    stage_info["gram"].update(alg_flops=alg["s3_flops_survey"],
+                              tflops=alg["s3_flops_survey"] / (med[2] * 1e-3) / 1e12,
+                              alg_flops_unique=alg["s3_flops"],
+                              tflops_unique=alg["s3_flops"] / (med[2] * 1e-3) / 1e12)
     stage_info["solve_v"].update(alg_bytes=alg["s4_bytes"])
     stage_info["solve_u"].update(alg_bytes=alg["s5_bytes"], gbs=alg["s5_bytes"] / (med[5] * 1e-3) / 1e9)
     dom = names[int(np.argmax(med[:6]))]
@@ -373,6 +378,8 @@ def main():
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "roofline": roof, "stages": stage_info, "cpu_baseline": cpu, "clocks": clk,
                 "gpu_launches": launches,
+                "harvest": {"value": T / (float(np.sum(med[:4])) * 1e-3), "unit": "submatrices/s",
+                            "note": "T / device time of stages 1-3 (selection, SVD, Gram), SURVEY.md 8(d)"},
                 "report": {"e": rep.e, "attempted": rep.trials_attempted, "accepted": rep.trials_accepted,
                            "z": rep.z, "gram_rank": rep.gram_rank, "underdetermined_rows": rep.underdetermined_rows}}
         print(json.dumps(line))

@@ -432,7 +432,9 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
       }
       __syncwarp();
     }
-    // descending norms (stable), then the top rows, normalised
+    // descending norms (stable), then the top rows, normalised. The sort is a
+    // compile-time bubble network on (sigma, row) pairs, so both stay in
+    // registers (no dynamically indexed local arrays).
     double sig[K];
     int ord[K];
 #pragma unroll
@@ -441,33 +443,43 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
       ord[i] = i;
     }
     // stable bubble sort on K <= 9 entries (ties keep the lower index first)
-    for (int pass = 0; pass < K - 1; ++pass)
-      for (int j = 0; j < K - 1 - pass; ++j)
-        if (sig[ord[j]] < sig[ord[j + 1]]) {
-          const int tmp = ord[j];
-          ord[j] = ord[j + 1];
-          ord[j + 1] = tmp;
-        }
-    double inv[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) inv[i] = sig[ord[i]] > 0.0 ? 1.0 / sig[ord[i]] : 0.0;
+    for (int pass = 0; pass < K - 1; ++pass)
+#pragma unroll
+      for (int j = 0; j < K - 1 - pass; ++j)
+        if (sig[j] < sig[j + 1]) {
+          const double ts = sig[j];
+          sig[j] = sig[j + 1];
+          sig[j + 1] = ts;
+          const int ti = ord[j];
+          ord[j] = ord[j + 1];
+          ord[j + 1] = ti;
+        }
+    // row i of the output: S row ord[i] scaled by 1/sigma_i (0 when excluded)
+    constexpr int RPX = (K + 1) & ~1;
+    double scl[RPX];
+    const double* srow[RPX];
+#pragma unroll
+    for (int i = 0; i < RPX; ++i) {
+      const bool use = i < K && i < rex && sig[i < K ? i : 0] > 0.0;
+      scl[i] = use ? 1.0 / sig[i < K ? i : 0] : 0.0;
+      srow[i] = S + (int64_t)(i < K ? ord[i] : 0) * Lp;
+    }
     // expanded layout (see k_svd): rp/2 planes of npad pairs, zero outside
-    // the support; same rounding as the CTA kernel: rotated row / sigma
+    // the support
     double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
+    const int lmax = L > 0 ? L - 1 : 0;
     for (int64_t j = lane; j < a.npad; j += 32) {
       const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
       const bool in = (word & bit) != 0;
-      const int c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
+      int c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
+      c = c < lmax ? c : lmax;
 #pragma unroll
-      for (int p = 0; p < (K + 1) / 2; ++p) {
+      for (int p = 0; p < RPX / 2; ++p) {
         if (p >= rp / 2) break;
-        double v[2] = {0.0, 0.0};
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = 2 * p + h;
-          if (i < K && in && i < rex && inv[i] > 0.0) v[h] = S[ord[i] * Lp + c] / sig[ord[i]];
-        }
-        vout[p * a.npad + j] = make_double2(v[0], v[1]);
+        const double v0 = in ? srow[2 * p][c] * scl[2 * p] : 0.0;
+        const double v1 = in ? srow[2 * p + 1][c] * scl[2 * p + 1] : 0.0;
+        vout[p * a.npad + j] = make_double2(v0, v1);
       }
     }
     __syncwarp();
