@@ -114,6 +114,17 @@ rsm_status rsm_ctx_load(rsm_ctx* ctx, const double* values, const uint8_t* mask,
 rsm_status rsm_ctx_load_device(rsm_ctx* ctx, const double* d_values, const uint8_t* d_mask,
                                int64_t m, int64_t n);
 
+/* Generate the reference's synthetic instance (rsm::generate, src/synth.cpp:12-57;
+ * same streams as rsm_generate below) directly on the device and load it into
+ * the context (no host buffers, no H2D). The mask is bit-exact with
+ * rsm_generate; values agree to a few ulps (device log/cos in Box-Muller). */
+rsm_status rsm_ctx_generate(rsm_ctx* ctx, int64_t m, int64_t n, int64_t r, double rho, double sigma,
+                            uint64_t seed);
+/* Copy the loaded matrix back: values (m x n FP64, NaN where hidden) and the
+ * bit-packed row mask (m x nwp u32, bit j%32 of word j/32; nwp written to
+ * *nwp); either buffer may be NULL. */
+rsm_status rsm_ctx_fetch_matrix(rsm_ctx* ctx, double* values, uint32_t* words, int64_t* nwp);
+
 /* decompose on the loaded matrix. U (m x r) and V (n x r) row-major host
  * buffers may be NULL to leave the factors on the device
  * (rsm_ctx_fetch_factors copies them later). */

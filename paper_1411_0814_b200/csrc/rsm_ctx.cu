@@ -975,6 +975,39 @@ rsm_status rsm_ctx_load_device(rsm_ctx* c, const double* d_values, const uint8_t
   });
 }
 
+rsm_status rsm_ctx_generate(rsm_ctx* c, int64_t m, int64_t n, int64_t r, double rho, double sigma, uint64_t seed) {
+  return guard(c, [&] {
+    if (m < 1 || n < 1 || r < 1 || r > 32) fail(RSM_ERR_INVALID_CONFIG, "generate: need m, n >= 1 and 1 <= r <= 32");
+    if (!(rho > 0.0 && rho <= 1.0) || !(sigma >= 0.0)) fail(RSM_ERR_INVALID_CONFIG, "generate: need 0 < rho <= 1, sigma >= 0");
+    const int64_t nwp = ceil_div(n, 128) * 4;
+    c->Y.ensure(sizeof(double) * m * n + 16);  // stage 5 may read 8 bytes past the end
+    c->bitsR.ensure(sizeof(uint32_t) * m * nwp);
+    DevBuf B;
+    B.ensure(sizeof(double) * r * n);
+    rsmk::launch_generate(m, n, r, rho, sigma, seed, B.as<double>(), nwp, c->Y.as<double>(), c->bitsR.as<uint32_t>(),
+                          c->sms, c->stream);
+    c->launches += 2;
+    ck(cudaGetLastError(), "generate kernels");
+    c->last_h2d = 0;
+    load_common(c, m, n, true);
+    B.release();
+  });
+}
+
+rsm_status rsm_ctx_fetch_matrix(rsm_ctx* c, double* values, uint32_t* words, int64_t* nwp_out) {
+  return guard(c, [&] {
+    if (!c->loaded) fail(RSM_ERR_INVALID_CONFIG, "no matrix loaded");
+    const int64_t nwp = ceil_div(c->n, 128) * 4;
+    if (nwp_out) *nwp_out = nwp;
+    if (values)
+      ck(cudaMemcpyAsync(values, c->Y.p, sizeof(double) * c->m * c->n, cudaMemcpyDeviceToHost, c->stream), "D2H Y");
+    if (words)
+      ck(cudaMemcpyAsync(words, c->bitsR.p, sizeof(uint32_t) * c->m * nwp, cudaMemcpyDeviceToHost, c->stream),
+         "D2H mask words");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
 rsm_status rsm_ctx_decompose(rsm_ctx* c, const rsm_config* cfg, double* U, double* V, rsm_report* rep) {
   return guard(c, [&] { decompose_impl(c, cfg, U, V, rep); });
 }

@@ -102,6 +102,9 @@ void launch_transpose(const double* Y, const uint8_t* M, int64_t m, int64_t n, d
                       uint8_t* Mt, cudaStream_t s);
 void launch_count_bits(const uint32_t* bits, int64_t nwords, unsigned long long* out,
                        cudaStream_t s);
+// k_synth.cu: device generator (B is r x n scratch)
+void launch_generate(int64_t m, int64_t n, int64_t r, double rho, double sigma, uint64_t seed, double* B,
+                     int64_t nwp, double* Y, uint32_t* bits, int sms, cudaStream_t s);
 // k_select.cu
 void launch_select(const uint32_t* bits, int64_t stride, int64_t nwords, int64_t pool, int block,
                    uint64_t seed, uint64_t a0, int64_t count, int32_t* idx_out, int32_t* q_out,

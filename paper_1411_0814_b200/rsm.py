@@ -89,6 +89,8 @@ def lib():
         "rsm_ctx_stream": (_P, [_P]),
         "rsm_ctx_load": (i32, [_P, _P, _P, i64, i64]),
         "rsm_ctx_load_device": (i32, [_P, _P, _P, i64, i64]),
+        "rsm_ctx_generate": (i32, [_P, i64, i64, i64, dbl, dbl, u64]),
+        "rsm_ctx_fetch_matrix": (i32, [_P, _P, _P, C.POINTER(i64)]),
         "rsm_ctx_decompose": (i32, [_P, C.POINTER(_Config), _P, _P, C.POINTER(_Report)]),
         "rsm_ctx_als": (i32, [_P, i64, i64, u64, _P, _P, C.POINTER(_Report)]),
         "rsm_ctx_fetch_factors": (i32, [_P, _P, _P]),
@@ -130,7 +132,7 @@ def lib():
 def exported_symbols():
     """Names the C-ABI header declares (used by the CPU symbol test)."""
     return ["rsm_config_default", "rsm_last_error", "rsm_ctx_create", "rsm_ctx_destroy", "rsm_nccl_unique_id",
-            "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_decompose", "rsm_ctx_fetch_factors", "rsm_ctx_als",
+            "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_generate", "rsm_ctx_fetch_matrix", "rsm_ctx_decompose", "rsm_ctx_fetch_factors", "rsm_ctx_als",
             "rsm_ctx_select", "rsm_ctx_harvest_gram", "rsm_ctx_solve_v", "rsm_ctx_solve_u", "rsm_ctx_stage_ms",
             "rsm_ctx_launch_count", "rsm_ctx_last_load_h2d_bytes", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_als", "rsm_harvest_gram", "rsm_solve_v",
             "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_generate_tracks", "rsm_load_matrix_csv",
@@ -328,6 +330,22 @@ class Context:
     def load_device(self, values_ptr: int, mask_ptr: int, m: int, n: int):
         _check(lib().rsm_ctx_load_device(self.h, values_ptr, mask_ptr, m, n), self.h)
         self.m, self.n = m, n
+
+    def generate(self, m: int, n: int, r: int, rho: float, sigma: float, seed: int):
+        """Device-side rsm::generate straight into this context (SURVEY.md 8(f) row 3)."""
+        _check(lib().rsm_ctx_generate(self.h, m, n, r, rho, sigma, seed), self.h)
+        self.m, self.n = m, n
+
+    def fetch_matrix(self) -> "MaskedMatrix":
+        """The loaded matrix back on the host (values + byte mask unpacked from the device words)."""
+        m, n = self.m, self.n
+        nwp = C.c_int64(0)
+        _check(lib().rsm_ctx_fetch_matrix(self.h, None, None, C.byref(nwp)), self.h)
+        values = np.empty((m, n), dtype=np.float64)
+        words = np.empty((m, nwp.value), dtype=np.uint32)
+        _check(lib().rsm_ctx_fetch_matrix(self.h, _ptr(values), _ptr(words), None), self.h)
+        bits = np.unpackbits(words.view(np.uint8).reshape(m, -1), axis=1, bitorder="little")[:, :n]
+        return MaskedMatrix.from_arrays(values, bits.astype(np.uint8))
 
     def decompose(self, cfg: RsmConfig, fetch: bool = True):
         r = cfg.rank
