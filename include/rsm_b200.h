@@ -17,6 +17,7 @@
  *   rsm_solve_u           <- rsm::solve_u              include/rsm/solver.hpp:74-75, src/solver.cpp:64-89
  *   rsm_masked_residual_norm <- rsm::masked_residual_norm include/rsm/core.hpp:94, src/core.cpp:35-39
  *   rsm_generate          <- rsm::generate (observed matrix only) include/rsm/synth.hpp:29, src/synth.cpp:12-57
+ *   rsm_ctx_generate      <- rsm::generate on the device (same streams; mask bit-exact, values to a few ulps)
  *   rsm_ctx_als / rsm_als <- rsm::baseline_als         include/rsm/solver.hpp:79-81, src/als.cpp:11-44
  *   rsm_load_matrix_csv   <- rsm::load_matrix          include/rsm/io.hpp:14, src/io.cpp:56-99
  *   rsm_save_matrix_csv   <- rsm::save_matrix          include/rsm/io.hpp:18, src/io.cpp:101-116
