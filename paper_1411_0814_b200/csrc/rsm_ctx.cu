@@ -114,6 +114,7 @@ struct rsm_ctx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   NcclComm comm = nullptr;
+  bool coll = false;  // collectives on (world > 1, or forced for a one-rank check)
   std::string err;
 
   // the loaded matrix as given
@@ -513,7 +514,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   record(c, 3);
   rsmk::launch_gram_reduce(c->P.as<double>(), nslices, npad, n, c->colcnt.as<int>(), c->G.as<double>(), c->stream);
   ++c->launches;
-  if (c->world > 1) {
+  if (c->coll) {
     if (g_nccl.allReduce(c->G.p, c->G.p, (size_t)(n * n), kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
       fail(RSM_ERR_INTERNAL, "ncclAllReduce failed");
   }
@@ -663,7 +664,7 @@ SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& out
   }
   double ss = 0.0;
   int fl = 0;
-  if (c->world > 1) {
+  if (c->coll) {
     // row shards: gather U, sum the scalars
     double* tmp = nullptr;
     ck(cudaMallocAsync((void**)&tmp, sizeof(double) * 2, c->stream), "malloc");
@@ -889,12 +890,18 @@ rsm_status rsm_ctx_create(rsm_ctx** out, int device, int world, int rank, const 
     c->sms = prop.multiProcessorCount;
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
-    if (world > 1) {
+    // RSM_FORCE_COLLECTIVES=1 with world == 1 and an id: a one-rank NCCL
+    // communicator and the multi-rank code path (allreduce / allgather run as
+    // identities), so the collectives are exercised on a single GPU
+    const char* fc = getenv("RSM_FORCE_COLLECTIVES");
+    const bool force = world == 1 && nccl_id && fc && atoi(fc) == 1;
+    if (world > 1 || force) {
       if (!nccl_id) fail(RSM_ERR_INVALID_CONFIG, "world > 1 needs an NCCL unique id");
       if (!g_nccl.load()) fail(RSM_ERR_INTERNAL, "libnccl.so.2 not loadable");
       NcclId id;
       std::memcpy(&id, nccl_id, sizeof(id));
       if (g_nccl.commInitRank(&c->comm, world, id, rank) != 0) fail(RSM_ERR_INTERNAL, "ncclCommInitRank failed");
+      c->coll = true;
     }
     *out = c;
   });
