@@ -50,6 +50,44 @@ __global__ void dmma_tp(double* out, int iters) {
   if (s == 12345.0) out[0] = s;
 }
 
+
+// half the warps issue DFMA chains, half issue DMMA chains: does the SM run
+// the two FP64 paths concurrently?
+template <int CH>
+__global__ void mixed_tp(double* out, int iters) {
+  const int warp = threadIdx.x >> 5;
+  if (warp & 1) {
+    double a = out[threadIdx.x & 31], b = out[(threadIdx.x + 1) & 31];
+    double c[CH][2];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) c[k][0] = c[k][1] = 0.0;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[k][0]), "+d"(c[k][1])
+                     : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < CH; ++k) s += c[k][0] + c[k][1];
+    if (s == 12345.0) out[0] = s;
+  } else {
+    double acc[16];
+    const double a = out[0], b = out[1];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = out[2 + k];
+    for (int i = 0; i < iters * 2; ++i) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[k] = fma(a, acc[k], b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += acc[k];
+    if (s == 12345.0) out[0] = s;
+  }
+}
+
 int main() {
   double* d;
   long long* cyc;
@@ -86,5 +124,20 @@ int main() {
   run("DMMA 4 chains x 256 thr", dmma_tp<4>, 256, 4 * 512.0 / 32, 5000);
   run("DMMA 8 chains x 256 thr", dmma_tp<8>, 256, 8 * 512.0 / 32, 2500);
   run("DMMA 2 chains x 128 thr", dmma_tp<2>, 128, 2 * 512.0 / 32, 10000);
+  // mixed: per DMMA warp-iteration 4*512/32 flops per thread; per DFMA warp-iteration 16*16*2 flops per thread
+  {
+    const int iters = 20000, threads = 256;
+    mixed_tp<4><<<sms * 4, threads>>>(d, iters);
+    cudaEventRecord(e0);
+    mixed_tp<4><<<sms * 4, threads>>>(d, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fl_dmma = 4 * 512.0 / 32 * (threads / 2) * (double)sms * 4 * iters;
+    const double fl_dfma = 2 * 16 * 2.0 * (threads / 2) * (double)sms * 4 * iters;
+    printf("mixed DMMA+DFMA warps: %.2f TFLOP/s total (%.2f ms; DMMA share of flops %.2f)\n",
+           (fl_dmma + fl_dfma) / ms / 1e9, ms, fl_dmma / (fl_dmma + fl_dfma));
+  }
   return 0;
 }
