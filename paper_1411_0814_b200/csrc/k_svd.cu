@@ -59,8 +59,13 @@ __device__ void warp0_popc_scan(const uint32_t* words, uint32_t* pre, int64_t nw
 
 }  // namespace
 
+// threads per CTA: the column branch spreads a trial's ~q = m rho^l rows over
+// 16 warps (one trial per SM: the K x q vectors fill shared memory)
 template <bool M2>
-__global__ void __launch_bounds__(128) k_svd(SvdArgs a) {
+constexpr int svd_cta_threads() { return M2 ? 128 : 512; }
+
+template <bool M2>
+__global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nth = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
@@ -522,10 +527,10 @@ size_t svd_smem_fixed(int64_t cmw) {
 void launch_svd(const SvdArgs& a, bool m2, int grid, size_t smem, cudaStream_t s) {
   if (m2) {
     cudaFuncSetAttribute(k_svd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_svd<true><<<grid, 128, smem, s>>>(a);
+    k_svd<true><<<grid, svd_cta_threads<true>(), smem, s>>>(a);
   } else {
     cudaFuncSetAttribute(k_svd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_svd<false><<<grid, 128, smem, s>>>(a);
+    k_svd<false><<<grid, svd_cta_threads<false>(), smem, s>>>(a);
   }
 }
 
@@ -533,10 +538,10 @@ int svd_occupancy(bool m2, size_t smem) {
   int nb = 0;
   if (m2) {
     cudaFuncSetAttribute(k_svd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_svd<true>, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_svd<true>, svd_cta_threads<true>(), smem);
   } else {
     cudaFuncSetAttribute(k_svd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_svd<false>, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_svd<false>, svd_cta_threads<false>(), smem);
   }
   return nb;
 }
