@@ -59,6 +59,55 @@ __device__ void warp0_popc_scan(const uint32_t* words, uint32_t* pre, int64_t nw
 
 }  // namespace
 
+constexpr int SVD_GRED = 16 * 36;  // 16 warps x K(K+1)/2 (K <= 8) Gram partials
+
+// Gram of the K vectors (K x L, leading dimension Lp) in one pass: each
+// thread accumulates all K(K+1)/2 products over its columns, warps reduce by
+// recursive halving, lane-holders publish per-warp partials, and threads
+// p < K(K+1)/2 sum them in warp order (deterministic). Writes the full
+// symmetric K x K into gram (leading dimension KMAX).
+template <int K>
+__device__ void cta_gram_1pass(const double* vec, int64_t Lp, int64_t L, double* gram, double* gred) {
+  constexpr int P = K * (K + 1) / 2;
+  constexpr int NV = P <= 4 ? 4 : (P <= 8 ? 8 : (P <= 16 ? 16 : (P <= 32 ? 32 : 64)));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  double g[NV];
+#pragma unroll
+  for (int p = 0; p < NV; ++p) g[p] = 0.0;
+  for (int64_t c = tid; c < L; c += blockDim.x) {
+    double x[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) x[i] = vec[i * Lp + c];
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = i; j < K; ++j) {
+        g[p] = fma(x[i], x[j], g[p]);
+        ++p;
+      }
+  }
+  warp_reduce_halving<NV>(g, lane);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const double t = warp_total<NV>(g, p);
+    if (lane == 0) gred[warp * P + p] = t;
+  }
+  __syncthreads();
+  if (tid < P) {
+    double t = 0.0;
+    for (int w = 0; w < nwarps; ++w) t += gred[w * P + tid];
+    int i = 0, rem = tid;
+    while (rem >= K - i) {
+      rem -= K - i;
+      ++i;
+    }
+    const int j = i + rem;
+    gram[i * KMAX + j] = t;
+    gram[j * KMAX + i] = t;
+  }
+}
+
 // threads per CTA: the column branch spreads a trial's ~q = m rho^l rows over
 // 16 warps (one trial per SM: the K x q vectors fill shared memory)
 template <bool M2>
@@ -77,7 +126,8 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
   double* W = gram + KMAX * KMAX;                       // KMAX*KMAX
   double* Vacc = W + KMAX * KMAX;                       // KMAX*KMAX (column branch)
   double* Tmp = Vacc + KMAX * KMAX;                     // KMAX*KMAX
-  double* cs = Tmp + KMAX * KMAX;                       // 64
+  double* gred = Tmp + KMAX * KMAX;                     // SVD_GRED (per-warp Gram partials)
+  double* cs = gred + SVD_GRED;                         // 64
   double* sig = cs + 64;                                // KMAX
   int* pairs = reinterpret_cast<int*>(sig + KMAX);      // 64
   int* ord = pairs + 64;                                // KMAX
@@ -167,6 +217,19 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
     // the top-rex subspace (what stage 3 consumes) by ~tol * g_ii / (g_ii - g_jj)
     const double tol_ortho = 1e-14;
     for (int it = 0;; ++it) {
+      if (K >= 2 && K <= 8) {
+        // one pass over the vectors: every thread accumulates all K(K+1)/2
+        // products of its columns, warps reduce, partials summed in fixed order
+        switch (K) {
+          case 2: cta_gram_1pass<2>(vec, Lp, L, gram, gred); break;
+          case 3: cta_gram_1pass<3>(vec, Lp, L, gram, gred); break;
+          case 4: cta_gram_1pass<4>(vec, Lp, L, gram, gred); break;
+          case 5: cta_gram_1pass<5>(vec, Lp, L, gram, gred); break;
+          case 6: cta_gram_1pass<6>(vec, Lp, L, gram, gred); break;
+          case 7: cta_gram_1pass<7>(vec, Lp, L, gram, gred); break;
+          default: cta_gram_1pass<8>(vec, Lp, L, gram, gred); break;
+        }
+      } else
       for (int p = warp; p < P; p += nwarps) {
         // unrank p -> (i, j), i <= j
         int i = 0, rem = p;
@@ -519,7 +582,7 @@ bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s) {
 }
 
 size_t svd_smem_fixed(int64_t cmw) {
-  size_t s = sizeof(double) * (4 * KMAX * KMAX + 64 + KMAX) + sizeof(int) * (64 + 3 * KMAX + 4) +
+  size_t s = sizeof(double) * (4 * KMAX * KMAX + SVD_GRED + 64 + KMAX) + sizeof(int) * (64 + 3 * KMAX + 4) +
              sizeof(uint32_t) * 2 * (size_t)cmw;
   return (s + 15) & ~(size_t)15;
 }
