@@ -67,7 +67,7 @@ constexpr int SVD_GRED = 16 * 36;  // 16 warps x K(K+1)/2 (K <= 8) Gram partials
 // p < K(K+1)/2 sum them in warp order (deterministic). Writes the full
 // symmetric K x K into gram (leading dimension KMAX).
 template <int K>
-__device__ void cta_gram_1pass(const double* vec, int64_t Lp, int64_t L, double* gram, double* gred) {
+__device__ __noinline__ void cta_gram_1pass(const double* vec, int64_t Lp, int64_t L, double* gram, double* gred) {
   constexpr int P = K * (K + 1) / 2;
   constexpr int NV = P <= 4 ? 4 : (P <= 8 ? 8 : (P <= 16 ? 16 : (P <= 32 ? 32 : 64)));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -105,6 +105,23 @@ __device__ void cta_gram_1pass(const double* vec, int64_t Lp, int64_t L, double*
     const int j = i + rem;
     gram[i * KMAX + j] = t;
     gram[j * KMAX + i] = t;
+  }
+}
+
+// vectors <- W^T vectors (W is K x K, leading dimension KMAX), thread per column
+template <int K>
+__device__ __noinline__ void cta_rotate(double* vec, int64_t Lp, int64_t L, const double* W) {
+  for (int64_t c = threadIdx.x; c < L; c += blockDim.x) {
+    double x[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) x[i] = vec[i * Lp + c];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double y = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) y += W[i * KMAX + j] * x[i];
+      vec[j * Lp + c] = y;
+    }
   }
 }
 
@@ -267,7 +284,18 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
       }
       __syncthreads();
       if (flags[2]) break;
-      // vectors <- W^T vectors
+      // vectors <- W^T vectors (compile-time K up to 8: register arrays)
+      if (K >= 2 && K <= 8) {
+        switch (K) {
+          case 2: cta_rotate<2>(vec, Lp, L, W); break;
+          case 3: cta_rotate<3>(vec, Lp, L, W); break;
+          case 4: cta_rotate<4>(vec, Lp, L, W); break;
+          case 5: cta_rotate<5>(vec, Lp, L, W); break;
+          case 6: cta_rotate<6>(vec, Lp, L, W); break;
+          case 7: cta_rotate<7>(vec, Lp, L, W); break;
+          default: cta_rotate<8>(vec, Lp, L, W); break;
+        }
+      } else
       for (int64_t c = tid; c < L; c += nth) {
         double x[KMAX];
 #pragma unroll

@@ -8,12 +8,14 @@ from paper_1411_0814_b200 import rsm  # noqa: E402
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c3"
 shapes = {"c3": (131072, 1024, 4, 0.8, 1e-3, 5, 16384), "c1": (2000, 200, 3, 0.8, 1e-3, 4, 2000),
-          "c4": (1048576, 2048, 8, 0.9, 1e-3, 9, 65536)}
+          "c4": (1048576, 2048, 8, 0.9, 1e-3, 9, 65536), "c2": (20000, 500, 5, 0.7, 1e-2, 6, 4096)}
 m, n, r, rho, sigma, k, T = shapes[cfgname]
-M = rsm.generate(m, n, r, rho, sigma, 0)
+seed = 1 if cfgname == "c2" else 0
+mode = rsm.Mode.M1 if cfgname == "c2" else rsm.Mode.M2
+M = rsm.generate(m, n, r, rho, sigma, seed)
 ctx = rsm.Context(0)
 ctx.load(M)
-cfg = rsm.RsmConfig(rank=r, mode=rsm.Mode.M2, block=k, plan=rsm.TrialPlan(T), seed=0)
+cfg = rsm.RsmConfig(rank=r, mode=mode, block=k, plan=rsm.TrialPlan(T), seed=seed)
 for i in range(int(os.environ.get("REPS", "2"))):
     t0 = time.time()
     _, rep = ctx.decompose(cfg, fetch=False)
