@@ -266,10 +266,10 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     // branchless (so the loads of consecutive columns pipeline): a hidden
     // cell's basis row is scaled by 0 and its value selected away, so the NaN
     // stored there never enters arithmetic
-    auto add = [&](int64_t c, bool k) {
+    auto add_y = [&](int64_t c, bool k, double yraw) {
       double v[R];
       vload(c, v);
-      const double yc = k ? y[c] : 0.0;
+      const double yc = k ? yraw : 0.0;
       if (!dense) {
         const double kf = k ? 1.0 : 0.0;
         double t[R];
@@ -288,8 +288,28 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
 #pragma unroll
       for (int i = 0; i < R; ++i) acc[NA + i] = fma(yc, v[i], acc[NA + i]);
     };
+    auto add = [&](int64_t c, bool k) { add_y(c, k, k ? y[c] : 0.0); };
+    if constexpr (STAGE == 0) {
+      // rows straight from global memory: UB words' mask words and values
+      // are loaded before any is used, so UB loads per lane are in flight
+      // (the hidden cells' NaN is loaded but selected away)
+      constexpr int UB = 8;
+      int w = 0;
+      for (; w + UB <= nfull; w += UB) {
+        unsigned bw[UB];
+        double yv[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) bw[u] = __ldg(wd + w + u);
+#pragma unroll
+        for (int u = 0; u < UB; ++u) yv[u] = __ldcs(y + (int64_t)(w + u) * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < UB; ++u) add_y((w + u) * 32 + lane, (bw[u] >> lane) & 1u, yv[u]);
+      }
+      for (; w < nfull; ++w) add(w * 32 + lane, (wd[w] >> lane) & 1u);
+    } else {
 #pragma unroll 2
-    for (int w = 0; w < nfull; ++w) add(w * 32 + lane, (wd[w] >> lane) & 1u);
+      for (int w = 0; w < nfull; ++w) add(w * 32 + lane, (wd[w] >> lane) & 1u);
+    }
     if ((int64_t)nfull * 32 + lane < n) add(nfull * 32 + lane, (wd[nfull] >> lane) & 1u);
     if (dense) {
       const int nwn = (int)((n + 31) >> 5);
@@ -381,17 +401,34 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     }
     // second pass over the row still in shared memory: direct residual
     double ss = 0.0;
-    auto res = [&](int64_t c, bool k) {
+    auto res_y = [&](int64_t c, bool k, double yraw) {
       double v[R];
       vload(c, v);
       double p = 0.0;
 #pragma unroll
       for (int q = 0; q < R; ++q) p = fma(u[q], v[q], p);
-      const double d = k ? y[c] - p : 0.0;
+      const double d = k ? yraw - p : 0.0;
       ss = fma(d, d, ss);
     };
+    auto res = [&](int64_t c, bool k) { res_y(c, k, k ? y[c] : 0.0); };
+    if constexpr (STAGE == 0) {
+      constexpr int UB = 8;
+      int w = 0;
+      for (; w + UB <= nfull; w += UB) {
+        unsigned bw[UB];
+        double yv[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) bw[u] = __ldg(wd + w + u);
+#pragma unroll
+        for (int u = 0; u < UB; ++u) yv[u] = __ldg(y + (int64_t)(w + u) * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < UB; ++u) res_y((w + u) * 32 + lane, (bw[u] >> lane) & 1u, yv[u]);
+      }
+      for (; w < nfull; ++w) res(w * 32 + lane, (wd[w] >> lane) & 1u);
+    } else {
 #pragma unroll 2
-    for (int w = 0; w < nfull; ++w) res(w * 32 + lane, (wd[w] >> lane) & 1u);
+      for (int w = 0; w < nfull; ++w) res(w * 32 + lane, (wd[w] >> lane) & 1u);
+    }
     if ((int64_t)nfull * 32 + lane < n) res(nfull * 32 + lane, (wd[nfull] >> lane) & 1u);
     ss = warp_sum(ss);
     if (lane < R) {

@@ -59,7 +59,8 @@ __device__ void warp0_popc_scan(const uint32_t* words, uint32_t* pre, int64_t nw
 
 }  // namespace
 
-constexpr int SVD_GRED = 16 * 36;  // 16 warps x K(K+1)/2 (K <= 8) Gram partials
+constexpr int SVD_GRED_PER_WARP = 36;  // K(K+1)/2 Gram partials per warp (K <= 8)
+static_assert(4 * SVD_GRED_PER_WARP <= KMAX * KMAX, "row-branch partials fit in Tmp");
 
 // Gram of the K vectors (K x L, leading dimension Lp) in one pass: each
 // thread accumulates all K(K+1)/2 products over its columns, warps reduce by
@@ -143,8 +144,10 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
   double* W = gram + KMAX * KMAX;                       // KMAX*KMAX
   double* Vacc = W + KMAX * KMAX;                       // KMAX*KMAX (column branch)
   double* Tmp = Vacc + KMAX * KMAX;                     // KMAX*KMAX
-  double* gred = Tmp + KMAX * KMAX;                     // SVD_GRED (per-warp Gram partials)
-  double* cs = gred + SVD_GRED;                         // 64
+  // per-warp Gram partials (warps x 36): the row branch's 4 warps alias Tmp
+  // (free during the Gram); the column branch's 16 warps get their own region
+  double* gred = M2 ? Tmp : Tmp + KMAX * KMAX;
+  double* cs = Tmp + KMAX * KMAX + (M2 ? 0 : (svd_cta_threads<M2>() / 32) * SVD_GRED_PER_WARP);  // 64
   double* sig = cs + 64;                                // KMAX
   int* pairs = reinterpret_cast<int*>(sig + KMAX);      // 64
   int* ord = pairs + 64;                                // KMAX
@@ -609,8 +612,9 @@ bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s) {
 #undef RSM_SVDW
 }
 
-size_t svd_smem_fixed(int64_t cmw) {
-  size_t s = sizeof(double) * (4 * KMAX * KMAX + SVD_GRED + 64 + KMAX) + sizeof(int) * (64 + 3 * KMAX + 4) +
+size_t svd_smem_fixed(int64_t cmw, bool m2) {
+  const int gred = m2 ? 0 : svd_cta_threads<false>() / 32 * SVD_GRED_PER_WARP;
+  size_t s = sizeof(double) * (4 * KMAX * KMAX + gred + 64 + KMAX) + sizeof(int) * (64 + 3 * KMAX + 4) +
              sizeof(uint32_t) * 2 * (size_t)cmw;
   return (s + 15) & ~(size_t)15;
 }

@@ -454,7 +454,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     int64_t Lmax = m2 ? out.sel.qmax : 0;
     if (!m2) for (int64_t t = t_lo; t < t_hi; ++t) Lmax = std::max<int64_t>(Lmax, hq[t]);
     const int64_t Lpad = std::max<int64_t>(2, (Lmax + 1) & ~int64_t(1));
-    const size_t fixed = rsmk::svd_smem_fixed(cmw);
+    const size_t fixed = rsmk::svd_smem_fixed(cmw, m2);
     const size_t vecb = sizeof(double) * (size_t)K * Lpad;
     const bool use_smem = fixed + vecb <= 200 * 1024;
     const size_t smem = fixed + (use_smem ? vecb : 0);

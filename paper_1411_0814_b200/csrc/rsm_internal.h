@@ -113,7 +113,7 @@ void launch_accept(const int32_t* q, const int32_t* idx, int64_t count, int32_t 
                    int block, uint64_t a0, int32_t* blockcnt, SelState* st, uint64_t T,
                    uint64_t* t_attempt, int32_t* t_q, int32_t* t_idx, cudaStream_t s);
 // k_svd.cu
-size_t svd_smem_fixed(int64_t cmw);
+size_t svd_smem_fixed(int64_t cmw, bool m2);
 void launch_svd(const SvdArgs& a, bool m2, int grid, size_t smem, cudaStream_t s);
 int svd_occupancy(bool m2, size_t smem);
 bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s);  // row branch, k <= 9
