@@ -88,3 +88,24 @@ np.save(sys.argv[1], np.concatenate([F.u.ravel(), F.v.ravel(), [rep.e, rep.z]]))
     # the slices' partial sums are added chunk by chunk: identical up to reassociation
     assert np.max(np.abs(a[:-2] - b[:-2])) <= 1e-9 * np.max(np.abs(a[:-2]))
     assert abs(a[-2] - b[-2]) <= 1e-9 * a[-2]
+
+
+@pytest.mark.parametrize("m,n,r", [(500, 1600, 8), (500, 1601, 7), (300, 4000, 8), (400, 3000, 4), (400, 2001, 3)])
+def test_solve_u_wide_rows(m, n, r):
+    # the stage-5 layouts the BASELINE bench shape does not reach: V-hat filling
+    # shared memory with rows read from global memory (config 4's n = 2048,
+    # r = 8 layout), V-hat read from global memory (n = 4000, r = 8), odd
+    # widths; rows above and below half observed (the r > 4 complement path
+    # and the direct path); U, flags and the residual sum against the oracle
+    M = rsm.generate(m, n, r, 0.55, 1e-2, n + r)
+    rng = np.random.default_rng(n)
+    V, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    ctx = rsm.Context(0)
+    ctx.load(M)
+    res, ss = ctx.solve_u(V, r)
+    U_o, fl_o = O.solve_u(M.values, M.mask, V, r)
+    assert res.underdetermined_rows == fl_o
+    assert rel_fro(res.u, U_o) <= 1e-12
+    R = np.where(M.mask != 0, np.nan_to_num(M.values) - U_o @ V.T, 0.0)
+    ss_o = float(np.sum(R * R))
+    assert abs(ss - ss_o) <= 1e-10 * ss_o
