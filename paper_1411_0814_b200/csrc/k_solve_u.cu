@@ -21,6 +21,7 @@
 // sum (y - u.v)^2 from the row still in shared memory, never by the
 // cancelling ||y||^2 - u^T b shortcut.
 #include <algorithm>
+#include <cstdlib>
 
 #include "rsm_internal.h"
 #include "rsm_dev.cuh"
@@ -447,6 +448,278 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
   }
 }
 
+// Normal-equation solve of one row (packed upper A, b, observed count nj):
+// Cholesky in registers; rows with nj < R or a pivot <= 1e-10 max diag take the
+// eigendecomposition pseudo-inverse. Returns true when the row is flagged
+// (detail/row_solve.hpp:26-35: fewer than r observations or rank < r). Same
+// arithmetic as the solve inside k_solve_u.
+template <int R>
+__device__ __forceinline__ bool row_solve(const double* A, const double* bv, int nj, double* u) {
+  constexpr int NA = R * (R + 1) / 2;
+  bool slow = nj < R;
+  if (!slow) {
+    double L[NA];
+    double dmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) dmax = fmax(dmax, A[i * R - i * (i - 1) / 2]);
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        double v = A[j * R - j * (j - 1) / 2 + (i - j)];
+#pragma unroll
+        for (int k = 0; k < j; ++k) v -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
+        if (i == j) {
+          if (!(v > 1e-10 * dmax)) slow = true;
+          L[q] = sqrt(fmax(v, 0.0));
+        } else {
+          L[q] = v / L[j * (j + 1) / 2 + j];
+        }
+        ++q;
+      }
+    }
+    if (!slow) {
+      double z[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        double v = bv[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) v -= L[i * (i + 1) / 2 + k] * z[k];
+        z[i] = v / L[i * (i + 1) / 2 + i];
+      }
+#pragma unroll
+      for (int i = R - 1; i >= 0; --i) {
+        double v = z[i];
+#pragma unroll
+        for (int k = i + 1; k < R; ++k) v -= L[k * (k + 1) / 2 + i] * u[k];
+        u[i] = v / L[i * (i + 1) / 2 + i];
+      }
+    }
+  }
+  if (slow) {
+    const int rank = pinv_solve<R>(A, bv, u);
+    return (nj < R) || (rank < R);
+  }
+  return false;
+}
+
+// Fused-pass row solver (r <= 4, V-hat in shared memory, rows staged by TMA):
+// as k_solve_u<R, true, 1>, but the residual pass of a warp's row k runs in
+// the same column loop as the accumulation pass of its next row k+1, so every
+// shared-memory read of V-hat (the dominant shared-memory traffic) serves both
+// passes. Row k stays in its buffer until that loop ends; the buffer is then
+// refilled with row k+2 while row k+1 is solved.
+template <int R>
+__global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
+  constexpr int NP = (R + 1) / 2;
+  constexpr int NA = R * (R + 1) / 2;
+  constexpr int NV = pow2_at_least(NA + R + 1);
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t npd = (n + 1) & ~int64_t(1);
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);  // [SU_MAXW][2]
+  double2* Vp = reinterpret_cast<double2*>(sm + 2 * SU_MAXW);
+  double* wb = sm + 2 * SU_MAXW + 2 * NP * n;
+  const int64_t bufd = npd + a.nwp / 2;
+  auto ybuf = [&](int b) { return wb + (2 * warp + b) * bufd; };
+  if (threadIdx.x < 2 * nwarps)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + threadIdx.x)), "r"(1));
+  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  for (int64_t e = threadIdx.x; e < NP * n; e += blockDim.x) {
+    const int64_t p = e / n, c = e % n;
+    const double x0 = a.V[c * R + 2 * p];
+    const double x1 = (2 * p + 1 < R) ? a.V[c * R + 2 * p + 1] : 0.0;
+    Vp[e] = make_double2(x0, x1);
+  }
+  __syncthreads();
+  auto vload = [&](int64_t c, double* v) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double2 t = Vp[p * n + c];
+      v[2 * p] = t.x;
+      if (2 * p + 1 < R) v[2 * p + 1] = t.y;
+    }
+  };
+  const uint32_t ybytes = (uint32_t)(n * 8), wbytes = (uint32_t)(a.nwp * 4);
+  auto issue = [&](int64_t row, int b) {
+    if (lane == 0) {
+      double* yb = ybuf(b);
+      const unsigned bar = smem_u32(bars + 2 * warp + b);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(ybytes + wbytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              smem_u32(yb)),
+          "l"(a.Y + row * n), "r"(ybytes), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              smem_u32(yb + npd)),
+          "l"(a.bitsR + row * a.nwp), "r"(wbytes), "r"(bar)
+          : "memory");
+    }
+  };
+  unsigned phase = 0u;
+  auto wait_buf = [&](int b) {
+    const unsigned bar = smem_u32(bars + 2 * warp + b);
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar), "r"((phase >> b) & 1u)
+          : "memory");
+    } while (!done);
+    phase ^= 1u << b;
+  };
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t nw = (int64_t)gridDim.x * nwarps;
+  const int64_t r0 = a.row_lo + gw;
+  if (r0 >= a.row_hi) return;
+  const int64_t nrows = (a.row_hi - r0 + nw - 1) / nw;  // this warp's rows: r0 + k nw
+  const int nfull = (int)(n >> 5);
+  const bool tail = (int64_t)nfull * 32 + lane < n;
+  issue(r0, 0);
+  if (nrows > 1) issue(r0 + nw, 1);
+  // accumulation terms of column c of a row (hidden cells selected away)
+  auto accum = [&](double* acc, const double* v, double yraw, bool k) {
+    const double kf = k ? 1.0 : 0.0;
+    const double yc = k ? yraw : 0.0;
+    double t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) t[i] = kf * v[i];
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int j = i; j < R; ++j) {
+        acc[p] = fma(t[i], v[j], acc[p]);
+        ++p;
+      }
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[NA + i] = fma(yc, v[i], acc[NA + i]);
+  };
+  auto resid = [&](double& ss, const double* v, const double* u, double yraw, bool k) {
+    double p = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) p = fma(u[q], v[q], p);
+    const double d = k ? yraw - p : 0.0;
+    ss = fma(d, d, ss);
+  };
+  // reduce a row's accumulators and solve it
+  auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u) -> bool {
+    int cnt = 0;
+    for (int64_t w = lane; w < a.nwp; w += 32) cnt += __popc(wd[w]);
+    acc[NA + R] = (double)cnt;
+    warp_reduce_halving<NV>(acc, lane);
+    double A[NA], bv[R];
+#pragma unroll
+    for (int p = 0; p < NA; ++p) A[p] = warp_total<NV>(acc, p);
+#pragma unroll
+    for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, NA + i);
+    const int nj = (int)warp_total<NV>(acc, NA + R);
+    return row_solve<R>(A, bv, nj, u);
+  };
+  // row 0: accumulation pass alone
+  double u[R];
+  bool flagged;
+  {
+    wait_buf(0);
+    const double* y = ybuf(0);
+    const uint32_t* wd = reinterpret_cast<const uint32_t*>(y + npd);
+    double acc[NV];
+#pragma unroll
+    for (int p = 0; p < NV; ++p) acc[p] = 0.0;
+#pragma unroll 2
+    for (int w = 0; w < nfull; ++w) {
+      const int64_t c = w * 32 + lane;
+      double v[R];
+      vload(c, v);
+      const bool k = (wd[w] >> lane) & 1u;
+      accum(acc, v, k ? y[c] : 0.0, k);
+    }
+    if (tail) {
+      const int64_t c = (int64_t)nfull * 32 + lane;
+      double v[R];
+      vload(c, v);
+      const bool k = (wd[nfull] >> lane) & 1u;
+      accum(acc, v, k ? y[c] : 0.0, k);
+    }
+    flagged = finish(acc, wd, u);
+  }
+  for (int64_t k = 0; k < nrows; ++k) {
+    const int64_t row = r0 + k * nw;
+    const int b = (int)(k & 1);
+    const double* y = ybuf(b);
+    const uint32_t* wd = reinterpret_cast<const uint32_t*>(y + npd);
+    const bool has_next = k + 1 < nrows;
+    double ss = 0.0;
+    double acc[NV];
+#pragma unroll
+    for (int p = 0; p < NV; ++p) acc[p] = 0.0;
+    const double* yn = ybuf(b ^ 1);
+    const uint32_t* wn = reinterpret_cast<const uint32_t*>(yn + npd);
+    if (has_next) {
+      wait_buf(b ^ 1);
+      // residual of row k and accumulation of row k+1 share the V-hat reads
+#pragma unroll 2
+      for (int w = 0; w < nfull; ++w) {
+        const int64_t c = w * 32 + lane;
+        double v[R];
+        vload(c, v);
+        const bool k0 = (wd[w] >> lane) & 1u;
+        const bool k1 = (wn[w] >> lane) & 1u;
+        resid(ss, v, u, k0 ? y[c] : 0.0, k0);
+        accum(acc, v, k1 ? yn[c] : 0.0, k1);
+      }
+      if (tail) {
+        const int64_t c = (int64_t)nfull * 32 + lane;
+        double v[R];
+        vload(c, v);
+        const bool k0 = (wd[nfull] >> lane) & 1u;
+        const bool k1 = (wn[nfull] >> lane) & 1u;
+        resid(ss, v, u, k0 ? y[c] : 0.0, k0);
+        accum(acc, v, k1 ? yn[c] : 0.0, k1);
+      }
+    } else {
+#pragma unroll 2
+      for (int w = 0; w < nfull; ++w) {
+        const int64_t c = w * 32 + lane;
+        double v[R];
+        vload(c, v);
+        const bool k0 = (wd[w] >> lane) & 1u;
+        resid(ss, v, u, k0 ? y[c] : 0.0, k0);
+      }
+      if (tail) {
+        const int64_t c = (int64_t)nfull * 32 + lane;
+        double v[R];
+        vload(c, v);
+        const bool k0 = (wd[nfull] >> lane) & 1u;
+        resid(ss, v, u, k0 ? y[c] : 0.0, k0);
+      }
+    }
+    ss = warp_sum(ss);
+    if (lane < R) {
+      double uk = 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == lane) uk = u[q];
+      a.U[row * R + lane] = uk;
+    }
+    if (lane == 0) {
+      a.rowres[row] = ss;
+      if (flagged) atomicAdd(a.flagged, 1);
+    }
+    __syncwarp();  // row k's buffer is free: refill it with row k+2
+    if (k + 2 < nrows) issue(r0 + (k + 2) * nw, b);
+    if (has_next) flagged = finish(acc, wn, u);
+  }
+}
+
 // deterministic single-CTA sum of n doubles (fixed strided order + tree)
 __global__ void k_sum_rows(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
   __shared__ double part[1024];
@@ -519,8 +792,26 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
   const size_t per_warp = 2 * bufb;
   const size_t cap = 227 * 1024 - 2048;
   const bool bulk = (a.n % 2) == 0;
+  static const bool fused_off = [] {
+    const char* e = getenv("RSM_SOLVE_U_FUSED");
+    return e && atoi(e) == 0;
+  }();
   if (head + vbytes + 8 * per_warp <= cap) {
     // V-hat and >= 8 warps of staged rows
+    if constexpr (R <= 4) {
+      if (bulk && !fused_off) {
+        const size_t capw = 227 * 1024 - 2048;
+        int w = (int)std::min<size_t>(SU_MAXW, (capw - head - vbytes) / per_warp);
+        if (w < 1) w = 1;
+        const size_t smem = head + vbytes + (size_t)w * per_warp;
+        cudaFuncSetAttribute(k_solve_u_fused<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t rows = a.row_hi - a.row_lo;
+        int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
+        if (blocks < 1) blocks = 1;
+        k_solve_u_fused<R><<<(unsigned)blocks, w * 32, smem, s>>>(a);
+        return;
+      }
+    }
     if (bulk) launch_solve_u_k<R, true, 1>(a, head + vbytes, per_warp, sms, s);
     else launch_solve_u_k<R, true, 2>(a, head + vbytes, per_warp, sms, s);
   } else if (head + vbytes <= cap) {
