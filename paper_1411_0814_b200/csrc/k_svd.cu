@@ -465,24 +465,25 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
       }
     }
     __syncwarp();
-    // one-sided Jacobi, Gram-accelerated
+    // one-sided Jacobi, Gram-accelerated. The Gram of the rotated vectors is
+    // accumulated in the rotation pass itself (one read of S per iteration).
     double g[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) g[p] = 0.0;
+    for (int c = lane; c < L; c += 32) {
+      double x[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
+      int p = 0;
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = i; j < K; ++j) {
+          g[p] = fma(x[i], x[j], g[p]);
+          ++p;
+        }
+    }
     for (int it = 0;; ++it) {
-#pragma unroll
-      for (int p = 0; p < P; ++p) g[p] = 0.0;
-      for (int c = lane; c < L; c += 32) {
-        double x[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
-        int p = 0;
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-#pragma unroll
-          for (int j = i; j < K; ++j) {
-            g[p] = fma(x[i], x[j], g[p]);
-            ++p;
-          }
-      }
 #pragma unroll
       for (int p = 0; p < P; ++p) g[p] = warp_sum(g[p]);
       bool big = false;
@@ -517,17 +518,28 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
       __syncwarp();
       warp_jacobi_reg<K, true>(Gs, K, Ws, K, 40);
       __syncwarp();
+#pragma unroll
+      for (int p = 0; p < P; ++p) g[p] = 0.0;
       for (int c = lane; c < L; c += 32) {
-        double x[K];
+        double x[K], y[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-          double y = 0.0;
+          double t = 0.0;
 #pragma unroll
-          for (int i = 0; i < K; ++i) y = fma(Ws[i * K + j], x[i], y);
-          S[j * Lp + c] = y;
+          for (int i = 0; i < K; ++i) t = fma(Ws[i * K + j], x[i], t);
+          y[j] = t;
+          S[j * Lp + c] = t;
         }
+        int p = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int j = i; j < K; ++j) {
+            g[p] = fma(y[i], y[j], g[p]);
+            ++p;
+          }
       }
       __syncwarp();
     }
