@@ -60,7 +60,7 @@ __device__ void warp0_popc_scan(const uint32_t* words, uint32_t* pre, int64_t nw
 }  // namespace
 
 constexpr int SVD_GRED_PER_WARP = 36;  // K(K+1)/2 Gram partials per warp (K <= 8)
-static_assert(4 * SVD_GRED_PER_WARP <= KMAX * KMAX, "row-branch partials fit in Tmp");
+static_assert(4 * 45 <= KMAX * KMAX, "row-branch partials (4 warps, K <= 9) fit in Tmp");
 
 // Gram of the K vectors (K x L, leading dimension Lp) in one pass: each
 // thread accumulates all K(K+1)/2 products over its columns, warps reduce by
@@ -237,9 +237,10 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
     // the top-rex subspace (what stage 3 consumes) by ~tol * g_ii / (g_ii - g_jj)
     const double tol_ortho = 1e-14;
     for (int it = 0;; ++it) {
-      if (K >= 2 && K <= 8) {
+      if (K >= 2 && K <= (M2 ? 9 : 8)) {
         // one pass over the vectors: every thread accumulates all K(K+1)/2
         // products of its columns, warps reduce, partials summed in fixed order
+        // (K = 9 only in the 4-warp row branch: its partials fit in Tmp)
         switch (K) {
           case 2: cta_gram_1pass<2>(vec, Lp, L, gram, gred); break;
           case 3: cta_gram_1pass<3>(vec, Lp, L, gram, gred); break;
@@ -247,7 +248,10 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
           case 5: cta_gram_1pass<5>(vec, Lp, L, gram, gred); break;
           case 6: cta_gram_1pass<6>(vec, Lp, L, gram, gred); break;
           case 7: cta_gram_1pass<7>(vec, Lp, L, gram, gred); break;
-          default: cta_gram_1pass<8>(vec, Lp, L, gram, gred); break;
+          case 8: cta_gram_1pass<8>(vec, Lp, L, gram, gred); break;
+          default:
+            if constexpr (M2) cta_gram_1pass<9>(vec, Lp, L, gram, gred);
+            break;
         }
       } else
       for (int p = warp; p < P; p += nwarps) {
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
       __syncthreads();
       if (flags[2]) break;
       // vectors <- W^T vectors (compile-time K up to 8: register arrays)
-      if (K >= 2 && K <= 8) {
+      if (K >= 2 && K <= 9) {
         switch (K) {
           case 2: cta_rotate<2>(vec, Lp, L, W); break;
           case 3: cta_rotate<3>(vec, Lp, L, W); break;
@@ -296,7 +300,8 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
           case 5: cta_rotate<5>(vec, Lp, L, W); break;
           case 6: cta_rotate<6>(vec, Lp, L, W); break;
           case 7: cta_rotate<7>(vec, Lp, L, W); break;
-          default: cta_rotate<8>(vec, Lp, L, W); break;
+          case 8: cta_rotate<8>(vec, Lp, L, W); break;
+          default: cta_rotate<9>(vec, Lp, L, W); break;
         }
       } else
       for (int64_t c = tid; c < L; c += nth) {

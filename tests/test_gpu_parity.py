@@ -413,3 +413,11 @@ def test_run_report_reproducible(tmp_path):
     assert reps[0][1] == reps[1][1]
     r = RP.parse_report(reps[0][1])
     assert r.checksum == rsm.dataset_checksum(M) and r.trials == 300 and r.trial_source == "explicit"
+
+
+def test_harvest_gram_wide_k9_cta_kernel():
+    # k = 9 with ~760 survivors: the per-warp submatrices exceed the warp kernel's
+    # shared-memory budget, so stage 2 runs the CTA-per-trial kernel with the
+    # compile-time K = 9 Gram and rotation (config 4's path at a small m and T)
+    M = gen(600, 1200, 8, 0.95, 1e-3, 4)
+    _gram_check(M, 1, 8, 12, 4, block=9)
