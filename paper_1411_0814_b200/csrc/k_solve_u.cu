@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
 #pragma unroll
         for (int u = 0; u < UB; ++u) bw[u] = __ldg(wd + w + u);
 #pragma unroll
-        for (int u = 0; u < UB; ++u) yv[u] = __ldcs(y + (int64_t)(w + u) * 32 + lane);
+        for (int u = 0; u < UB; ++u) yv[u] = __ldg(y + (int64_t)(w + u) * 32 + lane);
 #pragma unroll
         for (int u = 0; u < UB; ++u) add_y((w + u) * 32 + lane, (bw[u] >> lane) & 1u, yv[u]);
       }
