@@ -390,6 +390,147 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
 // leaves the full Gram in every lane, the convergence test is evaluated
 // redundantly (warp-uniform), and only the K x K eigensolve goes through
 // shared memory.
+// Top-(K-1) right-singular subspace of a K x (q) submatrix S from its K x K
+// Gram G = S S^T (packed upper g), for the case r = K - 1 the row branch's
+// default k = r + 1 gives. Stage 3 consumes only the projector V_r V_r^T, so
+// any orthonormal basis of span(V_r) serves: the smallest eigenvector u of G
+// by inverse iteration (Cholesky of G, at most 5 steps, converged when
+// successive iterates agree to 1e-14), a Householder reflection H with
+// H u = -+e_K whose first K-1 columns Q span u-perp = span(U_r), M = Q^T G Q
+// and its Cholesky M = L L^T; then V = S^T C with C = Q L^{-T} is orthonormal
+// (V^T V = L^{-1} M L^{-T} = I) and spans the top-r right singular vectors.
+// Run by one lane into C (K x (K-1), smem); returns false (the caller falls
+// back to the one-sided Jacobi) when G is not clearly separated -- inverse
+// iteration not converged or M not safely positive definite.
+template <int K>
+__device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C) {
+  constexpr int R = K - 1;
+  constexpr int P = K * (K + 1) / 2;
+  auto gat = [&](int i, int j) {  // packed upper G (shared memory)
+    const int lo = i < j ? i : j, hi = i < j ? j : i;
+    return Gsm[lo * K - lo * (lo - 1) / 2 + (hi - lo)];
+  };
+  double tr = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) tr += gat(i, i);
+  if (!(tr > 0.0)) return false;
+  // Cholesky of G (packed lower) with a floor on the pivots (G may be
+  // singular: the floor only regularises the inverse iteration)
+  double L[P];
+  auto li = [](int i, int j) { return i * (i + 1) / 2 + j; };
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double d = gat(j, j);
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= L[li(j, k)] * L[li(j, k)];
+    d = fmax(d, 1e-30 * tr);
+    L[li(j, j)] = sqrt(d);
+#pragma unroll
+    for (int i = j + 1; i < K; ++i) {
+      double v = gat(i, j);
+#pragma unroll
+      for (int k = 0; k < j; ++k) v -= L[li(i, k)] * L[li(j, k)];
+      L[li(i, j)] = v / L[li(j, j)];
+    }
+  }
+  double x[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) x[i] = 1.0 + 0.25 * i;
+  bool conv = false;
+  for (int it = 0; it < 5 && !conv; ++it) {
+    double z[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double v = x[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) v -= L[li(i, k)] * z[k];
+      z[i] = v / L[li(i, i)];
+    }
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+      double v = z[i];
+#pragma unroll
+      for (int k = i + 1; k < K; ++k) v -= L[li(k, i)] * z[k];
+      z[i] = v / L[li(i, i)];
+    }
+    double nz = 0.0, dot = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) nz += z[i] * z[i];
+    nz = rsqrt(nz);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      z[i] *= nz;
+      dot += z[i] * x[i];
+    }
+    double diff = 0.0;
+    const double sg = dot >= 0.0 ? 1.0 : -1.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) diff = fmax(diff, fabs(z[i] - sg * x[i]));
+    if (it > 0 && diff <= 1e-14) conv = true;
+#pragma unroll
+    for (int i = 0; i < K; ++i) x[i] = z[i];
+  }
+  if (!conv) return false;
+  // Householder v = x + s e_K, H = I - beta v v^T (H x = -s e_K); the first R
+  // columns of H are Q. M = Q^T G Q = (H G H)[0:R, 0:R] with w = G v,
+  // gamma = v^T w: (HGH)_ij = G_ij - beta (v_i w_j + w_i v_j) + beta^2 gamma v_i v_j
+  const double sgn = x[K - 1] >= 0.0 ? 1.0 : -1.0;
+  double v[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = x[i];
+  v[K - 1] += sgn;
+  double vv = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) vv += v[i] * v[i];
+  const double beta = 2.0 / vv;
+  double w[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) t += gat(i, k) * v[k];
+    w[i] = t;
+  }
+  double gam = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) gam += v[i] * w[i];
+  // Cholesky of M (packed lower, reusing L), pivots well above zero
+  double dmax = 0.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    dmax = fmax(dmax, gat(i, i) - 2.0 * beta * v[i] * w[i] + beta * beta * gam * v[i] * v[i]);
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    double d = gat(j, j) - 2.0 * beta * v[j] * w[j] + beta * beta * gam * v[j] * v[j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= L[li(j, k)] * L[li(j, k)];
+    if (!(d > 1e-8 * dmax)) return false;
+    L[li(j, j)] = sqrt(d);
+#pragma unroll
+    for (int i = j + 1; i < R; ++i) {
+      double t = gat(i, j) - beta * (v[i] * w[j] + w[i] * v[j]) + beta * beta * gam * v[i] * v[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t -= L[li(i, k)] * L[li(j, k)];
+      L[li(i, j)] = t / L[li(j, j)];
+    }
+  }
+  // C = Q L^{-T}: row i of C solves L c = q_i, q_ij = delta_ij - beta v_i v_j
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double c[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      double t = (i == j ? 1.0 : 0.0) - beta * v[i] * v[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t -= L[li(j, k)] * c[k];
+      c[j] = t / L[li(j, j)];
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) C[i * R + j] = c[j];
+  }
+  return true;
+}
+
 constexpr int SVDW_WARPS = 4;
 
 template <int K>
@@ -488,9 +629,25 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
           ++p;
         }
     }
+    bool fast = false;
     for (int it = 0;; ++it) {
 #pragma unroll
       for (int p = 0; p < P; ++p) g[p] = warp_sum(g[p]);
+      if constexpr (K <= 6) {
+        if (it == 0 && rex == K - 1 && a.fast_basis) {
+          // r = k - 1: an orthonormal basis of the top-r subspace straight
+          // from the Gram (see topr_basis_small), no Jacobi rotations
+          if (lane == 0) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) Gs[p] = g[p];
+            Gs[K * K - 1] = topr_basis_small<K>(Gs, Ws) ? 1.0 : 0.0;
+          }
+          __syncwarp();
+          fast = Gs[K * K - 1] != 0.0;
+          __syncwarp();
+          if (fast) break;
+        }
+      }
       bool big = false;
       {
         int p = 0;
@@ -547,6 +704,41 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
           }
       }
       __syncwarp();
+    }
+    if constexpr (K <= 6) {
+      if (fast) {
+        // V = S^T C (K x r coefficients in Ws), expanded layout
+        constexpr int R1 = K - 1;
+        constexpr int RPX1 = (R1 + 1) & ~1;
+        double cf[K][RPX1];
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int j = 0; j < RPX1; ++j) cf[i][j] = j < R1 ? Ws[i * R1 + j] : 0.0;
+        double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
+        const int lmax = L > 0 ? L - 1 : 0;
+        for (int64_t j = lane; j < a.npad; j += 32) {
+          const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
+          const bool in = (word & bit) != 0;
+          int c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
+          c = c < lmax ? c : lmax;
+          double x[K];
+#pragma unroll
+          for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
+#pragma unroll
+          for (int p = 0; p < RPX1 / 2; ++p) {
+            double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+              v0 = fma(x[i], cf[i][2 * p], v0);
+              v1 = fma(x[i], cf[i][2 * p + 1], v1);
+            }
+            vout[p * a.npad + j] = make_double2(in ? v0 : 0.0, in ? v1 : 0.0);
+          }
+        }
+        __syncwarp();
+        continue;
+      }
     }
     // descending norms (stable), then the top rows, normalised. The sort is a
     // compile-time bubble network on (sigma, row) pairs, so both stay in

@@ -489,6 +489,11 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
         return e ? atoi(e) : 6;
       }();
       a.max_outer = svd_maxit;
+      static const int fast_basis = [] {
+        const char* e = getenv("RSM_SVD_FAST_BASIS");
+        return e ? atoi(e) : 1;
+      }();
+      a.fast_basis = fast_basis;
       // row branch with k <= 9: warp-per-trial kernel; otherwise CTA per trial
       if (!(m2 && rsmk::launch_svd_warp(a, c->sms, c->stream))) rsmk::launch_svd(a, m2, (int)grid, smem, c->stream);
       ++c->launches;

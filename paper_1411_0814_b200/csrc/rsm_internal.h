@@ -38,6 +38,7 @@ struct SvdArgs {
   int64_t Lpad;
   int use_smem;
   int max_outer;         // one-sided Jacobi rotations per trial (at most)
+  int fast_basis;        // row branch, r = k - 1: top-r basis from the Gram (no Jacobi)
 };
 
 struct GramArgs {
