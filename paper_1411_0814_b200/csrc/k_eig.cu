@@ -9,7 +9,9 @@
 //   * ub = ||G||_inf bounds the spectrum from above;
 //   * a block of b >= r+2 vectors is filtered with a degree-d Chebyshev
 //     polynomial damping [a, ub] (a = largest Ritz value of the block,
-//     d chosen so the amplification stays below 1e6 to keep CholQR stable),
+//     d chosen so the amplification stays below EigArgs::amp = 1e10: CholQR2
+//     with its shifted retry keeps such blocks orthonormal, and the larger
+//     degree saves an outer round at configs 1, 3 and 4),
 //     re-orthonormalised by CholQR2 and Rayleigh-Ritz projected;
 //   * it stops when the residuals of the r+1 lowest Ritz pairs fall below
 //     1e-12 ub, which makes the r+1 lowest Ritz values the eigenvalues the
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       const double e = 0.5 * (ub - acut), c = 0.5 * (ub + acut);
       const double x0 = fabs(c / e);
       const double growth = x0 + sqrt(x0 * x0 - 1.0);
-      int d = (int)floor(log(2e6) / log(growth));
+      int d = (int)floor(log(a.amp) / log(growth));
       d = d < 2 ? 2 : (d > 24 ? 24 : d);
       double sigma = e / (0.0 - c);
       const double tau = 2.0 / sigma;

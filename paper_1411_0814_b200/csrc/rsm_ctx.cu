@@ -576,6 +576,11 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   a.istat = c->eI.as<int>();
   a.dstat = c->eD.as<double>();
   a.max_outer = 60;
+  static const double amp = [] {
+    const char* e = getenv("RSM_EIG_AMP");
+    return e ? atof(e) : 1e10;
+  }();
+  a.amp = amp;
   a.cnt = c->G_harvest ? c->colcnt.as<int>() : nullptr;
   a.zero_rows = c->eI.as<int>() + 7;
   rsmk::launch_zero_rows(a.G, n, a.cnt, c->eI.as<int>() + 7, c->stream);

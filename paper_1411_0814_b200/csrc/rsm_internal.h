@@ -75,6 +75,7 @@ struct EigArgs {
   double* dstat;    // [0] lambda_max, [1] ub, [2] max residual
   int max_outer;
   const int* cnt;   // per-column trial counts when G = diag(cnt) - PSD (else null)
+  double amp;       // Chebyshev filter amplification cap (degree choice)
 };
 
 struct SolveUArgs {
