@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       const double x0 = fabs(c / e);
       const double growth = x0 + sqrt(x0 * x0 - 1.0);
       int d = (int)floor(log(a.amp) / log(growth));
-      d = d < 2 ? 2 : (d > 24 ? 24 : d);
+      d = d < 2 ? 2 : (d > a.dmax ? a.dmax : d);
       double sigma = e / (0.0 - c);
       const double tau = 2.0 / sigma;
       grid.sync();  // X complete

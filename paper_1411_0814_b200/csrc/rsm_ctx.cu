@@ -581,6 +581,11 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
     return e ? atof(e) : 1e10;
   }();
   a.amp = amp;
+  static const int dmax = [] {
+    const char* e = getenv("RSM_EIG_DMAX");
+    return e ? atoi(e) : 40;
+  }();
+  a.dmax = dmax;
   a.cnt = c->G_harvest ? c->colcnt.as<int>() : nullptr;
   a.zero_rows = c->eI.as<int>() + 7;
   rsmk::launch_zero_rows(a.G, n, a.cnt, c->eI.as<int>() + 7, c->stream);

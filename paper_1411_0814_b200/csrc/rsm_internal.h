@@ -76,6 +76,7 @@ struct EigArgs {
   int max_outer;
   const int* cnt;   // per-column trial counts when G = diag(cnt) - PSD (else null)
   double amp;       // Chebyshev filter amplification cap (degree choice)
+  int dmax;         // and degree cap
 };
 
 struct SolveUArgs {
