@@ -126,6 +126,49 @@ __device__ __noinline__ void cta_rotate(double* vec, int64_t Lp, int64_t L, cons
   }
 }
 
+// Column branch gather: vector j of S^T is column idx[j] over the surviving
+// rows. Each thread walks its mask words' set bits four rows at a time and
+// issues the 4 K loads of a batch before storing any, so a batch costs one
+// memory round trip instead of four (the rows are random: every load is its
+// own sector).
+template <int K>
+__device__ __noinline__ void cta_gather_cols(const double* __restrict__ Y, int64_t n, int64_t mwp, const int* idx,
+                                             const uint32_t* rw, const uint32_t* rp, double* vec, int64_t Lp) {
+  constexpr int B = 4;
+  int col[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) col[j] = idx[j];
+  for (int64_t w = threadIdx.x; w < mwp; w += blockDim.x) {
+    uint32_t word = rw[w];
+    int64_t c = rp[w];
+    while (word) {
+      int64_t rows[B];
+      int nb = 0;
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        rows[q] = -1;
+        if (word) {
+          rows[q] = w * 32 + (__ffs(word) - 1);
+          word &= word - 1;
+          nb = q + 1;
+        }
+      }
+      double x[B][K];
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[q][j] = rows[q] >= 0 ? __ldg(Y + rows[q] * n + col[j]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (q < nb) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) vec[j * Lp + c + q] = x[q][j];
+        }
+      c += nb;
+    }
+  }
+}
+
 // threads per CTA: the column branch spreads a trial's ~q = m rho^l rows over
 // 16 warps (one trial per SM: the K x q vectors fill shared memory)
 template <bool M2>
@@ -216,6 +259,17 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
       __syncthreads();
       L = flags[0];
       // gather S^T (K x L): vector j = column idx[j] over surviving rows
+      if (K >= 2 && K <= 8) {
+        switch (K) {
+          case 2: cta_gather_cols<2>(a.Y, a.n, a.mwp, idx, rw, rp, vec, Lp); break;
+          case 3: cta_gather_cols<3>(a.Y, a.n, a.mwp, idx, rw, rp, vec, Lp); break;
+          case 4: cta_gather_cols<4>(a.Y, a.n, a.mwp, idx, rw, rp, vec, Lp); break;
+          case 5: cta_gather_cols<5>(a.Y, a.n, a.mwp, idx, rw, rp, vec, Lp); break;
+          case 6: cta_gather_cols<6>(a.Y, a.n, a.mwp, idx, rw, rp, vec, Lp); break;
+          case 7: cta_gather_cols<7>(a.Y, a.n, a.mwp, idx, rw, rp, vec, Lp); break;
+          default: cta_gather_cols<8>(a.Y, a.n, a.mwp, idx, rw, rp, vec, Lp); break;
+        }
+      } else
       for (int64_t w = tid; w < a.mwp; w += nth) {
         uint32_t word = rw[w];
         int64_t c = rp[w];
