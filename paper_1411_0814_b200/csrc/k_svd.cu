@@ -126,6 +126,41 @@ __device__ __noinline__ void cta_rotate(double* vec, int64_t Lp, int64_t L, cons
   }
 }
 
+// Row branch gather in the CTA-per-trial kernel: the K drawn rows' values at
+// four support columns per thread are loaded before any is stored (one memory
+// round trip per batch), the column counts are bumped as before.
+template <int K>
+__device__ __noinline__ void cta_gather_rows(const double* __restrict__ Y, int64_t n, const int* idx,
+                                             const uint32_t* cm, const uint32_t* pre, double* vec, int64_t Lp,
+                                             int* colcnt) {
+  constexpr int B = 4;
+  int64_t rowoff[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) rowoff[i] = (int64_t)idx[i] * n;
+  for (int64_t j0 = threadIdx.x; j0 < n; j0 += (int64_t)B * blockDim.x) {
+    double x[B][K];
+    int64_t cpos[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int64_t j = j0 + (int64_t)q * blockDim.x;
+      cpos[q] = -1;
+      if (j < n) {
+        const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
+        if (word & bit) cpos[q] = pre[j >> 5] + __popc(word & (bit - 1u));
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) x[q][i] = cpos[q] >= 0 ? __ldg(Y + rowoff[i] + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q)
+      if (cpos[q] >= 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) vec[i * Lp + cpos[q]] = x[q][i];
+        atomicAdd(colcnt + j0 + (int64_t)q * blockDim.x, 1);
+      }
+  }
+}
+
 // Column branch gather: vector j of S^T is column idx[j] over the surviving
 // rows. Each thread walks its mask words' set bits four rows at a time and
 // issues the 4 K loads of a batch before storing any, so a batch costs one
@@ -229,6 +264,18 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
       L = flags[0];
       for (int64_t w = tid; w < a.cmw; w += nth) a.t_cm[tl * a.cmw + w] = cm[w];
       // gather S (K x L) row-major into vec (sampler.cpp:80-84)
+      if (K >= 2 && K <= 9) {
+        switch (K) {
+          case 2: cta_gather_rows<2>(a.Y, a.n, idx, cm, pre, vec, Lp, a.colcnt); break;
+          case 3: cta_gather_rows<3>(a.Y, a.n, idx, cm, pre, vec, Lp, a.colcnt); break;
+          case 4: cta_gather_rows<4>(a.Y, a.n, idx, cm, pre, vec, Lp, a.colcnt); break;
+          case 5: cta_gather_rows<5>(a.Y, a.n, idx, cm, pre, vec, Lp, a.colcnt); break;
+          case 6: cta_gather_rows<6>(a.Y, a.n, idx, cm, pre, vec, Lp, a.colcnt); break;
+          case 7: cta_gather_rows<7>(a.Y, a.n, idx, cm, pre, vec, Lp, a.colcnt); break;
+          case 8: cta_gather_rows<8>(a.Y, a.n, idx, cm, pre, vec, Lp, a.colcnt); break;
+          default: cta_gather_rows<9>(a.Y, a.n, idx, cm, pre, vec, Lp, a.colcnt); break;
+        }
+      } else
       for (int64_t j = tid; j < a.n; j += nth) {
         const uint32_t word = cm[j >> 5];
         const uint32_t bit = 1u << (j & 31);
