@@ -210,7 +210,7 @@ template <bool M2>
 constexpr int svd_cta_threads() { return M2 ? 128 : 512; }
 
 template <bool M2>
-__global__ void __launch_bounds__(svd_cta_threads<M2>()) k_svd(SvdArgs a) {
+__global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nth = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
