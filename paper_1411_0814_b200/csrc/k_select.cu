@@ -25,14 +25,14 @@ __global__ void __launch_bounds__(256) k_select(const uint32_t* __restrict__ bit
                                                 int64_t nwords, int64_t pool, int block,
                                                 uint64_t seed, uint64_t a0, int64_t count,
                                                 int32_t* __restrict__ idx_out,
-                                                int32_t* __restrict__ q_out) {
+                                                int32_t* __restrict__ q_out, int apw) {
   extern __shared__ int32_t sidx[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
-  const int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32;
-  int32_t* my = sidx + (size_t)warp * 32 * block;
+  const int64_t base = ((int64_t)blockIdx.x * warps + warp) * apw;
+  int32_t* my = sidx + (size_t)warp * apw * block;
   const int64_t a = base + lane;
-  if (a < count) {
+  if (lane < apw && a < count) {
     uint64_t st = rng_state(seed, 5 /* stream::TRIAL */, a0 + (uint64_t)a);
     int32_t key[2 * KMAX], val[2 * KMAX];
     int nmap = 0;
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_select(const uint32_t* __restrict__ bit
     for (int t = 0; t < block; ++t) idx_out[a * block + t] = out[t];
   }
   __syncwarp();
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < apw; ++i) {
     const int64_t ai = base + i;
     if (ai >= count) break;
     const int32_t* rows = my + i * block;
@@ -165,12 +165,16 @@ __global__ void k_acc_emit(const int32_t* __restrict__ q, const int32_t* __restr
 void launch_select(const uint32_t* bits, int64_t stride, int64_t nwords, int64_t pool, int block,
                    uint64_t seed, uint64_t a0, int64_t count, int32_t* idx_out, int32_t* q_out,
                    cudaStream_t s) {
+  // attempts per warp: 32 (one draw per lane) when an attempt's scan is a
+  // few words; 4 when it is long (the column branch scans m/32 words per drawn
+  // column), so that enough warps share the scans
+  const int apw = nwords > 64 ? 4 : 32;
   const int threads = 256, warps = threads / 32;
-  const int64_t per_block = (int64_t)warps * 32;
+  const int64_t per_block = (int64_t)warps * apw;
   const int64_t blocks = (count + per_block - 1) / per_block;
-  const size_t smem = (size_t)warps * 32 * block * sizeof(int32_t);
+  const size_t smem = (size_t)warps * apw * block * sizeof(int32_t);
   k_select<<<(unsigned)blocks, threads, smem, s>>>(bits, stride, nwords, pool, block, seed, a0,
-                                                   count, idx_out, q_out);
+                                                   count, idx_out, q_out, apw);
 }
 
 void launch_accept(const int32_t* q, const int32_t* idx, int64_t count, int32_t min_count,
