@@ -421,3 +421,13 @@ def test_harvest_gram_wide_k9_cta_kernel():
     # compile-time K = 9 Gram and rotation (config 4's path at a small m and T)
     M = gen(600, 1200, 8, 0.95, 1e-3, 4)
     _gram_check(M, 1, 8, 12, 4, block=9)
+
+
+@pytest.mark.parametrize("k", [4, 5, 6])
+def test_harvest_gram_pure_noise_small_gaps(k):
+    # no low-rank structure: the k x k Grams have no clear gap below the top
+    # r = k - 1, which exercises the top-r basis path's convergence test and
+    # its one-sided Jacobi fallback
+    vals, mask = random_masked(400, 60, 0.9, 40 + k)
+    M = rsm.MaskedMatrix(400, 60, vals, mask)
+    _gram_check(M, 1, k - 1, 300, k, block=k)
