@@ -134,8 +134,10 @@ struct rsm_ctx {
   // workspace
   DevBuf sel_idx, sel_q, blockcnt, selstate, t_attempt, t_q, t_idx, t_cm, Vtrial,
       colcnt, svd_scr, svd_scr32, P, tiles, G, eX, eY, eZ, ePart, eW, eI, eD, Vhat, U, rowres,
-      flagged, dsum, cnt64;
+      flagged, dsum, cnt64, Wq, tiles8;
   int64_t tiles_n = -1;
+  int64_t tiles8_n = -1;  // tcgen05 stage-3 tile list valid for this npad
+  int ntiles8 = 0;
   int tiles_cpl = 0;
   int64_t G_n = 0;      // accumulator on device valid for this n
   bool G_harvest = false;  // G = diag(colcnt) - PSD (from our harvest, single rank)
@@ -147,6 +149,10 @@ struct rsm_ctx {
   double stage_ms[8] = {};
   double solver_stats[24] = {};  // eig: outer its, matvecs, lambda_max, ub, max residual, block, grid
   int64_t launches = 0;
+  // held by the one-shot calls (rsm_decompose, rsm_solve_u, ...) from the load
+  // through the last device->host copy: those share one context per device, and
+  // the reference's functions are reentrant (SPEC concurrency model)
+  std::mutex oneshot;
 
   void set_err(const std::string& s) { err = s; }
 };
@@ -382,6 +388,23 @@ void build_tiles(rsm_ctx* c, int64_t npad, int cpl) {
   c->tiles_cpl = cpl;
 }
 
+void build_tiles8(rsm_ctx* c, int64_t npad) {
+  if (c->tiles8_n == npad) return;
+  std::vector<int2> t;
+  rsmk::gram_i8_tiles(npad, t);
+  c->tiles8.ensure(sizeof(int2) * t.size());
+  ck(cudaMemcpy(c->tiles8.p, t.data(), sizeof(int2) * t.size(), cudaMemcpyHostToDevice), "H2D tiles");
+  c->tiles8_n = npad;
+  c->ntiles8 = (int)t.size();
+}
+
+// stage 3 on the tensor cores (k_gram_i8.cu) unless RSM_GRAM=dfma selects the
+// FP64 register-tile kernel (k_gram.cu), kept as the exact-FP64 comparison
+bool gram_on_tensor_cores() {
+  const char* e = getenv("RSM_GRAM");
+  return !(e && std::string(e) == "dfma");
+}
+
 int64_t ntiles_for(int64_t npad, int cpl) {
   const int64_t TR = 64, TC = 32 * cpl;
   int64_t k = 0;
@@ -440,17 +463,41 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     return e ? std::max<int64_t>(1, atoll(e)) : ((int64_t)6 << 30);
   }();
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(Tl, budget / tbytes));
+  const bool i8 = gram_on_tensor_cores();
   const int cpl = rsmk::gram_cols_per_lane(rex);
-  build_tiles(c, npad, cpl);
-  const int64_t ntiles = ntiles_for(npad, cpl);
+  int64_t ntiles = 0;
+  if (i8) {
+    build_tiles8(c, npad);
+    ntiles = c->ntiles8;
+  } else {
+    build_tiles(c, npad, cpl);
+    ntiles = ntiles_for(npad, cpl);
+  }
+  // tensor-core path: K = trials * rex rows of int8 slices per trial chunk,
+  // split into nk K-chunks (P slices) so the work units fill the SMs and each
+  // chunk's int32 sums stay exact (k_gram_i8.cu)
+  const int S8 = rsmk::gram_i8_slices();
+  const int64_t Kpad0 = ceil_div(std::max<int64_t>(chunk, 1) * rex, 32) * 32;
+  int nk = 1;
+  if (i8) {
+    int64_t k = std::max(ceil_div(Kpad0, rsmk::gram_i8_kmax()), ceil_div(c->sms, ntiles));
+    k = std::min<int64_t>(k, std::max<int64_t>(ceil_div(Kpad0, rsmk::gram_i8_kmax()), Kpad0 / 512));
+    nk = (int)std::max<int64_t>(1, k);
+    if (const char* e = getenv("RSM_I8_NK")) nk = (int)std::max<int64_t>(ceil_div(Kpad0, rsmk::gram_i8_kmax()), atoll(e));
+  }
   int nslices = 1;
   if (Tl > 0) {
-    // at most one wave of the 2-CTA/SM kernel: floor(2*SMs / tiles) slices
-    nslices = (int)std::max<int64_t>(1, ((int64_t)rsmk::gram_ctas_per_sm(rex) * c->sms) / ntiles);
-    nslices = (int)std::min<int64_t>(nslices, std::max<int64_t>(1, chunk / 16));
+    if (i8) {
+      nslices = nk;
+    } else {
+      // at most one wave of the 2-CTA/SM kernel: floor(2*SMs / tiles) slices
+      nslices = (int)std::max<int64_t>(1, ((int64_t)rsmk::gram_ctas_per_sm(rex) * c->sms) / ntiles);
+      nslices = (int)std::min<int64_t>(nslices, std::max<int64_t>(1, chunk / 16));
+    }
     c->P.ensure(sizeof(double) * (size_t)nslices * npad * npad);
     c->t_cm.ensure(sizeof(uint32_t) * chunk * cmw);
     c->Vtrial.ensure((size_t)tbytes * chunk);
+    if (i8) c->Wq.ensure((size_t)S8 * Kpad0 * npad);
     int64_t Lmax = m2 ? out.sel.qmax : 0;
     if (!m2) for (int64_t t = t_lo; t < t_hi; ++t) Lmax = std::max<int64_t>(Lmax, hq[t]);
     const int64_t Lpad = std::max<int64_t>(2, (Lmax + 1) & ~int64_t(1));
@@ -500,16 +547,35 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
       ck(cudaGetLastError(), "svd launch");
       if (c0 == t_lo) record(c, 2);  // with several chunks, later stage-2 work counts as stage 3
       // stage 3
-      rsmk::GramArgs g{};
-      g.t_cm = c->t_cm.as<uint32_t>();
-      g.V = c->Vtrial.as<double>();
-      g.T = c1 - c0; g.cmw = cmw; g.npad = npad; g.R = rex; g.nslices = nslices;
-      g.accumulate = c0 > t_lo ? 1 : 0;
-      g.tiles = c->tiles.as<int2>();
-      g.P = c->P.as<double>();
-      rsmk::launch_gram(g, (int)ntiles, c->stream);
-      ++c->launches;
-      ck(cudaGetLastError(), "gram launch");
+      if (i8) {
+        const int64_t Kpad = ceil_div((c1 - c0) * rex, 32) * 32;
+        rsmk::launch_slice_planes(c->Vtrial.as<double>(), c1 - c0, rex, npad, Kpad, c->Wq.as<int8_t>(), c->stream);
+        rsmk::GramI8Args g{};
+        g.W = c->Wq.as<int8_t>();
+        g.npad = npad;
+        g.Kpad = Kpad;
+        g.nk = nk;
+        g.Kc = ceil_div(ceil_div(Kpad, nk), 32) * 32;
+        g.ntiles = (int)ntiles;
+        g.tiles = c->tiles8.as<int2>();
+        g.P = c->P.as<double>();
+        g.accumulate = c0 > t_lo ? 1 : 0;
+        const char* dg = getenv("RSM_I8_DIAG");
+        g.diag = dg ? atoi(dg) : 0;
+        ck(rsmk::launch_gram_i8(g, c->sms, c->stream), "gram (tcgen05) launch");
+        c->launches += 2;
+      } else {
+        rsmk::GramArgs g{};
+        g.t_cm = c->t_cm.as<uint32_t>();
+        g.V = c->Vtrial.as<double>();
+        g.T = c1 - c0; g.cmw = cmw; g.npad = npad; g.R = rex; g.nslices = nslices;
+        g.accumulate = c0 > t_lo ? 1 : 0;
+        g.tiles = c->tiles.as<int2>();
+        g.P = c->P.as<double>();
+        rsmk::launch_gram(g, (int)ntiles, c->stream);
+        ++c->launches;
+        ck(cudaGetLastError(), "gram launch");
+      }
     }
   } else {
     record(c, 2);
@@ -931,7 +997,7 @@ rsm_status rsm_ctx_destroy(rsm_ctx* c) {
                     &c->t_idx, &c->t_cm, &c->Vtrial, &c->colcnt, &c->svd_scr,
                     &c->svd_scr32, &c->P, &c->tiles, &c->G, &c->eX, &c->eY, &c->eZ, &c->ePart,
                     &c->eW, &c->eI, &c->eD, &c->Vhat, &c->U, &c->rowres, &c->flagged, &c->dsum,
-                    &c->cnt64};
+                    &c->cnt64, &c->Wq, &c->tiles8};
   for (DevBuf* b : bufs) b->release();
   if (c->hstage) cudaFreeHost(c->hstage);
   for (auto& e : c->ev) cudaEventDestroy(e);
@@ -1077,6 +1143,11 @@ rsm_status rsm_ctx_harvest_gram(rsm_ctx* c, const rsm_trial_params* p, uint64_t 
     HarvestOut h = harvest_impl(c, v, p, trials);
     if (G) ck(cudaMemcpyAsync(G, c->G.p, sizeof(double) * v.n * v.n, cudaMemcpyDeviceToHost, c->stream), "D2H G");
     ck(cudaStreamSynchronize(c->stream), "sync");
+    float ms = 0.f;  // stages 1-3 split (events 0..4), as decompose reports it
+    for (int i = 0; i < 4; ++i) {
+      ck(cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]), "event");
+      c->stage_ms[i] = ms;
+    }
     *attempted = h.sel.attempted;
     *accepted = h.sel.accepted;
     *z = h.z;
@@ -1154,6 +1225,7 @@ rsm_status rsm_als(const double* values, const uint8_t* mask, int64_t m, int64_t
   rsm_ctx* c = nullptr;
   rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
   if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
   st = rsm_ctx_load(c, values, mask, m, n);
   if (!st) st = rsm_ctx_als(c, r, iterations, seed, U, V, rep);
   if (st) g_err = c->err;
@@ -1165,6 +1237,7 @@ rsm_status rsm_decompose(const double* values, const uint8_t* mask, int64_t m, i
   rsm_ctx* c = nullptr;
   rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
   if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
   st = rsm_ctx_load(c, values, mask, m, n);
   if (st) { g_err = c->err; return st; }
   st = rsm_ctx_decompose(c, cfg, U, V, rep);
@@ -1178,6 +1251,7 @@ rsm_status rsm_harvest_gram(const double* values, const uint8_t* mask, int64_t m
   rsm_ctx* c = nullptr;
   rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
   if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
   st = rsm_ctx_load(c, values, mask, m, n);
   if (!st) st = rsm_ctx_harvest_gram(c, p, trials, G, attempted, accepted, z);
   if (st) g_err = c->err;
@@ -1189,6 +1263,7 @@ rsm_status rsm_solve_v(const double* G, int64_t n, int64_t r, double tol, double
   rsm_ctx* c = nullptr;
   rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
   if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
   st = rsm_ctx_solve_v(c, G, n, r, tol, V, gram_rank, borderline, nullptr);
   if (st) g_err = c->err;
   return st;
@@ -1199,6 +1274,7 @@ rsm_status rsm_solve_u(const double* values, const uint8_t* mask, int64_t m, int
   rsm_ctx* c = nullptr;
   rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
   if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
   st = rsm_ctx_load(c, values, mask, m, n);
   if (!st) st = rsm_ctx_solve_u(c, V, r, U, underdetermined_rows, nullptr);
   if (st) g_err = c->err;
@@ -1212,6 +1288,7 @@ rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, i
   rsm_ctx* c = nullptr;
   rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
   if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
   st = rsm_ctx_load(c, values, mask, m, n);
   if (st) { g_err = c->err; return st; }
   return guard(c, [&] {

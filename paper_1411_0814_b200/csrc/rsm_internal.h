@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace rsmk {
@@ -53,6 +54,19 @@ struct GramArgs {
   int accumulate;  // add to P instead of overwriting (trial chunks after the first)
   const int2* tiles;
   double* P;       // nslices x npad x npad partials
+};
+
+// stage 3 on tcgen05 (k_gram_i8.cu): int8 slices Wq[S][Kpad][npad] (MN-major)
+struct GramI8Args {
+  const int8_t* W;
+  int64_t npad, Kpad;
+  int64_t Kc;        // K rows per work unit (multiple of 32, <= gram_i8_kmax())
+  int nk;            // K-chunks (P slices)
+  int ntiles;        // 128 x 64 tiles touching the upper triangle
+  const int2* tiles;
+  double* P;         // nk x npad x npad partials (-W^T W per K-chunk)
+  int accumulate;    // add to P (trial chunks after the first)
+  int diag;          // RSM_I8_DIAG: 0 normal, 1 loads only, 2 MMAs only (timing experiments)
 };
 
 struct EigArgs {
@@ -126,6 +140,13 @@ int gram_ctas_per_sm(int R);
 void launch_gram(const GramArgs& a, int ntiles, cudaStream_t s);
 void launch_gram_reduce(const double* P, int nslices, int64_t npad, int64_t n, const int* cnt,
                         double* G, cudaStream_t s);
+// k_gram_i8.cu
+int gram_i8_slices();
+int64_t gram_i8_kmax();
+void gram_i8_tiles(int64_t npad, std::vector<int2>& t);
+void launch_slice_planes(const double* V, int64_t T, int rex, int64_t npad, int64_t Kpad, int8_t* W,
+                         cudaStream_t s);
+cudaError_t launch_gram_i8(const GramI8Args& a, int sms, cudaStream_t s);
 // k_eig.cu
 int eig_part_width(int b);
 cudaError_t launch_eig(const EigArgs& a, int grid, cudaStream_t s);

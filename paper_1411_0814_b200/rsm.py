@@ -323,6 +323,15 @@ class Context:
         self.m, self.n = M.m, M.n
 
     def load_arrays(self, values: np.ndarray, mask: np.ndarray):
+        """Load row-major FP64 values and a byte (uint8/bool) mask of the same
+        shape. Non-contiguous views are copied (free for contiguous inputs);
+        other dtypes or mismatched shapes raise invalid_config."""
+        if values.ndim != 2 or values.dtype != np.float64:
+            raise Error(errc.invalid_config, "values must be a 2-D float64 array")
+        if mask.shape != values.shape or mask.dtype not in (np.uint8, np.bool_):
+            raise Error(errc.invalid_config, "mask must be uint8/bool with the shape of values")
+        values = np.ascontiguousarray(values)
+        mask = np.ascontiguousarray(mask).view(np.uint8)
         m, n = values.shape
         _check(lib().rsm_ctx_load(self.h, _ptr(values), _ptr(mask), m, n), self.h)
         self.m, self.n = m, n
