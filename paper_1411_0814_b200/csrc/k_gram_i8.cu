@@ -8,17 +8,17 @@
 //     G = diag(count) - W^T W,   W = [E_1 V_1 | E_2 V_2 | ...]^T  (K x n),
 // K = trials * r, every entry of W an entry of an orthonormal basis (|w| <= 1).
 //
-// Exact split. Each w is written as  w = sum_{s<S} a_s 2^(-6-7s) + e,
-// a_s integers in [-64, 64] (a_0 = rint(64 w), then rint(128 * remainder) per
-// slice; every step is exact in FP64), |e| <= 2^(-7S). Then
-//     w_i w_j ~= sum_{d<S} 2^(-12-7d) * sum_{s+t=d} a_s(i) a_t(j),
-// and each inner sum is an INTEGER dot product over K: tcgen05 computes it
-// exactly in int32 (|sum| <= S * 4096 * Kc < 2^31 for a K-chunk Kc <= 65536).
-// Dropped terms (s+t >= S) and the representation error bound the absolute
-// error of one product by ~(S+2) 2^(-7S) (S = 7: 1.6e-14), far below the FP64
-// rounding noise that differs between any two summation orders of the
-// reference's own loop at these sizes; the per-class FP64 combination in the
-// epilogue is exact up to one rounding per class.
+// Exact split. Each w is written in balanced signed base-256 digits,
+//     w = a_0 2^-6 + sum_{1<=s<S} a_s 2^(-6-8s) + e,  a_0 in [-65, 65],
+//     a_s in [-128, 127], |e| <= 2^(-7-8(S-1))       (split_i8 below),
+// so  w_i w_j ~= sum_{d<S} 2^(-12-8d) * sum_{s+t=d} a_s(i) a_t(j)
+// and each inner sum is an INTEGER dot product over K that tcgen05 computes
+// exactly in int32 (|sum| <= S * 2^14 * Kc < 2^31 for K-chunks Kc <= 16384).
+// The dropped classes (s+t >= S) and e bound the absolute error of one
+// product by ~S 2^(2-8S) (S = 6, the default: 8.5e-14; S = 7: 3e-16), below
+// the differences between two FP64 summation orders of the reference's own
+// loop at these sizes; the per-class FP64 combination in the epilogue rounds
+// once per class.
 //
 // Layout. The slices are stored MN-major: Wq[s][k][col] int8, row k = trial-
 // vector, npad columns, so stage 2 writes each trial's vectors as contiguous
@@ -142,23 +142,23 @@ struct I8Cfg {
 
 }  // namespace
 
-// w = sum_{s<S} a[s] 2^(-6-7s) + e with |a[s]| <= 64 and |e| <= 2^(-7S) for
-// |w| <= 1 (+rounding): a[0] = rint(64 w), then rint(128 * remainder). The
-// scalings are by powers of two and y - rint(y) is exact, so every step is
-// exact in FP64.
+// Balanced signed digits: w = a[0] 2^-6 + sum_{1<=s<S} a[s] 2^(-6-8s) + e.
+// X = rint(w 2^(6+8(S-1))) is an exact integer (|X| <= 2^54 for |w| <= 1,
+// S <= 7; |e| <= 2^(-7-8(S-1))); its base-256 digits are taken from the
+// least significant end in two's-complement balanced form (digit in
+// [-128, 127], the carry moved up), so a[1..S-1] fit int8 exactly and the
+// leading digit a[0] = what remains lies in [-65, 65].
 template <int S>
 __device__ __forceinline__ void split_i8(double x, int (&a)[S]) {
-  double y = x * 64.0;
-  double q = rint(y);
-  a[0] = (int)q;
-  double r = y - q;
+  long long X = __double2ll_rn(x * (double)(1ll << (6 + 8 * (S - 1))));
 #pragma unroll
-  for (int s = 1; s < S; ++s) {
-    y = r * 128.0;
-    q = rint(y);
-    a[s] = (int)q;
-    r = y - q;
+  for (int s = S - 1; s >= 1; --s) {
+    int d = (int)(X & 255);
+    d -= (d & 128) << 1;  // 128..255 -> -128..-1
+    a[s] = d;
+    X = (X - d) >> 8;
   }
+  a[0] = (int)X;
 }
 
 template <int S>
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int d = S - 1; d >= 0; --d) {  // small classes first
           int v[32];
           tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * BN + 32 * h), v);
-          const double sc = live ? ldexp(1.0, -12 - 7 * d) : 0.0;
+          const double sc = live ? ldexp(1.0, -12 - 8 * d) : 0.0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) acc[j] = fma((double)v[j], sc, acc[j]);
         }
@@ -396,16 +396,16 @@ cudaError_t launch_i8_t(const GramI8Args& a, int sms, cudaStream_t s) {
 
 }  // namespace
 
+// digits per value (RSM_GRAM_SLICES overrides: 5, 6 or 7)
 int gram_i8_slices() {
-  static const int S = [] {
-    const char* e = getenv("RSM_GRAM_SLICES");
-    const int v = e ? atoi(e) : 7;
-    return v == 6 ? 6 : 7;
-  }();
-  return S;
+  const char* e = getenv("RSM_GRAM_SLICES");
+  const int v = e ? atoi(e) : 6;
+  return v < 5 ? 5 : (v > 7 ? 7 : v);
 }
 
-int64_t gram_i8_kmax() { return 65536; }  // S * 4096 * Kc < 2^31 for S <= 7
+// int32 exactness: a class sums at most S products of |digits| <= 128, so
+// |acc| <= S * 16384 * Kc < 2^31 for Kc <= 16384 and S <= 7
+int64_t gram_i8_kmax() { return 16384; }
 
 void gram_i8_tiles(int64_t npad, std::vector<int2>& t) {
   t.clear();
@@ -418,12 +418,19 @@ void launch_slice_planes(const double* V, int64_t T, int rex, int64_t npad, int6
                          cudaStream_t s) {
   const int64_t n = Kpad * (npad / 16);
   const unsigned grid = (unsigned)((n + 255) / 256);
-  if (gram_i8_slices() == 6) k_slice_planes<6><<<grid, 256, 0, s>>>(V, T, rex, npad, Kpad, W);
-  else k_slice_planes<7><<<grid, 256, 0, s>>>(V, T, rex, npad, Kpad, W);
+  switch (gram_i8_slices()) {
+    case 5: k_slice_planes<5><<<grid, 256, 0, s>>>(V, T, rex, npad, Kpad, W); break;
+    case 6: k_slice_planes<6><<<grid, 256, 0, s>>>(V, T, rex, npad, Kpad, W); break;
+    default: k_slice_planes<7><<<grid, 256, 0, s>>>(V, T, rex, npad, Kpad, W); break;
+  }
 }
 
 cudaError_t launch_gram_i8(const GramI8Args& a, int sms, cudaStream_t s) {
-  return gram_i8_slices() == 6 ? launch_i8_t<6>(a, sms, s) : launch_i8_t<7>(a, sms, s);
+  switch (gram_i8_slices()) {
+    case 5: return launch_i8_t<5>(a, sms, s);
+    case 6: return launch_i8_t<6>(a, sms, s);
+    default: return launch_i8_t<7>(a, sms, s);
+  }
 }
 
 }  // namespace rsmk
