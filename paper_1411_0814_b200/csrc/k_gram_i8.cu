@@ -46,6 +46,7 @@
 #include <vector>
 
 #include "rsm_internal.h"
+#include "rsm_dev.cuh"
 
 namespace rsmk {
 
@@ -141,25 +142,6 @@ struct I8Cfg {
 };
 
 }  // namespace
-
-// Balanced signed digits: w = a[0] 2^-6 + sum_{1<=s<S} a[s] 2^(-6-8s) + e.
-// X = rint(w 2^(6+8(S-1))) is an exact integer (|X| <= 2^54 for |w| <= 1,
-// S <= 7; |e| <= 2^(-7-8(S-1))); its base-256 digits are taken from the
-// least significant end in two's-complement balanced form (digit in
-// [-128, 127], the carry moved up), so a[1..S-1] fit int8 exactly and the
-// leading digit a[0] = what remains lies in [-65, 65].
-template <int S>
-__device__ __forceinline__ void split_i8(double x, int (&a)[S]) {
-  long long X = __double2ll_rn(x * (double)(1ll << (6 + 8 * (S - 1))));
-#pragma unroll
-  for (int s = S - 1; s >= 1; --s) {
-    int d = (int)(X & 255);
-    d -= (d & 128) << 1;  // 128..255 -> -128..-1
-    a[s] = d;
-    X = (X - d) >> 8;
-  }
-  a[0] = (int)X;
-}
 
 template <int S>
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -326,33 +308,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-// Expanded FP64 planes (k_svd.cu layout: per trial rp/2 planes of npad
-// (v_2p, v_2p+1) pairs, zero outside the support) -> S int8 slices, MN-major
-// rows k = t * rex + p; rows past T * rex are zero. Thread = (row, 16 columns).
-template <int S>
-__global__ void k_slice_planes(const double* __restrict__ V, int64_t T, int rex, int64_t npad, int64_t Kpad,
-                               int8_t* __restrict__ W) {
-  const int64_t groups = npad / 16;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= Kpad * groups) return;
-  const int64_t k = gid / groups, j0 = (gid % groups) * 16;
-  const int rp = (rex + 1) & ~1;
-  int8_t out[S][16];
-  const int64_t t = k / rex;
-  const int p = (int)(k % rex);
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const double x = t < T ? V[t * npad * rp + (int64_t)(p >> 1) * npad * 2 + (j0 + j) * 2 + (p & 1)] : 0.0;
-    int sl[S];
-    split_i8<S>(x, sl);
-#pragma unroll
-    for (int s = 0; s < S; ++s) out[s][j] = (int8_t)sl[s];
-  }
-#pragma unroll
-  for (int s = 0; s < S; ++s)
-    *reinterpret_cast<uint4*>(W + ((int64_t)s * Kpad + k) * npad + j0) = *reinterpret_cast<const uint4*>(out[s]);
-}
-
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -396,12 +351,7 @@ cudaError_t launch_i8_t(const GramI8Args& a, int sms, cudaStream_t s) {
 
 }  // namespace
 
-// digits per value (RSM_GRAM_SLICES overrides: 5, 6 or 7)
-int gram_i8_slices() {
-  const char* e = getenv("RSM_GRAM_SLICES");
-  const int v = e ? atoi(e) : 6;
-  return v < 5 ? 5 : (v > 7 ? 7 : v);
-}
+int gram_i8_slices() { return rsmd::kGramSlices; }
 
 // int32 exactness: a class sums at most S products of |digits| <= 128, so
 // |acc| <= S * 16384 * Kc < 2^31 for Kc <= 16384 and S <= 7
@@ -414,23 +364,8 @@ void gram_i8_tiles(int64_t npad, std::vector<int2>& t) {
       if (BN * b + BN - 1 >= BM * a) t.push_back(make_int2((int)a, (int)b));
 }
 
-void launch_slice_planes(const double* V, int64_t T, int rex, int64_t npad, int64_t Kpad, int8_t* W,
-                         cudaStream_t s) {
-  const int64_t n = Kpad * (npad / 16);
-  const unsigned grid = (unsigned)((n + 255) / 256);
-  switch (gram_i8_slices()) {
-    case 5: k_slice_planes<5><<<grid, 256, 0, s>>>(V, T, rex, npad, Kpad, W); break;
-    case 6: k_slice_planes<6><<<grid, 256, 0, s>>>(V, T, rex, npad, Kpad, W); break;
-    default: k_slice_planes<7><<<grid, 256, 0, s>>>(V, T, rex, npad, Kpad, W); break;
-  }
-}
-
 cudaError_t launch_gram_i8(const GramI8Args& a, int sms, cudaStream_t s) {
-  switch (gram_i8_slices()) {
-    case 5: return launch_i8_t<5>(a, sms, s);
-    case 6: return launch_i8_t<6>(a, sms, s);
-    default: return launch_i8_t<7>(a, sms, s);
-  }
+  return launch_i8_t<rsmd::kGramSlices>(a, sms, s);
 }
 
 }  // namespace rsmk

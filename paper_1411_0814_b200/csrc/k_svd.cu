@@ -27,6 +27,8 @@
 #include "rsm_internal.h"
 #include "rsm_dev.cuh"
 
+using rsmd::emit_slices4;
+
 namespace rsmk {
 
 using namespace rsmd;
@@ -448,6 +450,40 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
     // top vectors as rp/2 planes of npad (v_{2p}, v_{2p+1}) pairs, zero
     // outside the column support; rp = rex rounded up to even
     const int rex = a.rex, rp = (a.rex + 1) & ~1;
+    if (a.Wq) {
+      // int8 digit slices for the tensor-core stage 3 (k_gram_i8.cu): rows
+      // tl * rex + i, zero outside the support, four columns per thread
+      for (int64_t j0 = 4 * (int64_t)tid; j0 < a.npad; j0 += 4 * (int64_t)nth) {
+        int cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t j = j0 + u;
+          int c = -1;
+          if (M2) {
+            const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
+            if (word & bit) c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
+          } else {
+            for (int q = 0; q < K; ++q)
+              if (idx[q] == j) c = q;
+          }
+          cc[u] = c;
+        }
+        for (int i = 0; i < rex; ++i) {
+          const int o = ord[i];
+          const double sg = M2 ? sig[o] : 0.0;
+          const double inv = sg > 0.0 ? 1.0 / sg : 0.0;
+          double v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            v[u] = 0.0;
+            if (cc[u] >= 0) v[u] = M2 ? vec[o * Lp + cc[u]] * inv : Vacc[cc[u] * KMAX + o];
+          }
+          emit_slices4(a.Wq, a.Kpad, a.npad, tl * rex + i, j0, v[0], v[1], v[2], v[3]);
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
     for (int64_t j = tid; j < a.npad; j += nth) {
       int c = -1;  // support position of column j
@@ -816,8 +852,37 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
         for (int i = 0; i < K; ++i)
 #pragma unroll
           for (int j = 0; j < RPX1; ++j) cf[i][j] = j < R1 ? Ws[i * R1 + j] : 0.0;
-        double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
         const int lmax = L > 0 ? L - 1 : 0;
+        if (a.Wq) {
+          // int8 digit slices (k_gram_i8.cu): lane = 4 consecutive columns
+          for (int64_t j0 = 4 * lane; j0 < a.npad; j0 += 128) {
+            double v[4][R1];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int64_t j = j0 + u;
+              const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
+              const bool in = (word & bit) != 0;
+              int c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
+              c = c < lmax ? c : lmax;
+              double x[K];
+#pragma unroll
+              for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
+#pragma unroll
+              for (int p = 0; p < R1; ++p) {
+                double t = 0.0;
+#pragma unroll
+                for (int i = 0; i < K; ++i) t = fma(x[i], cf[i][p], t);
+                v[u][p] = in ? t : 0.0;
+              }
+            }
+#pragma unroll
+            for (int p = 0; p < R1; ++p)
+              emit_slices4(a.Wq, a.Kpad, a.npad, tl * rex + p, j0, v[0][p], v[1][p], v[2][p], v[3][p]);
+          }
+          __syncwarp();
+          continue;
+        }
+        double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
         for (int64_t j = lane; j < a.npad; j += 32) {
           const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
           const bool in = (word & bit) != 0;
@@ -876,8 +941,33 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     }
     // expanded layout (see k_svd): rp/2 planes of npad pairs, zero outside
     // the support
-    double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
     const int lmax = L > 0 ? L - 1 : 0;
+    if (a.Wq) {
+      // int8 digit slices (k_gram_i8.cu): lane = 4 consecutive columns
+      for (int64_t j0 = 4 * lane; j0 < a.npad; j0 += 128) {
+        int cidx[4];
+        bool in[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t j = j0 + u;
+          const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
+          in[u] = (word & bit) != 0;
+          const int c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
+          cidx[u] = c < lmax ? c : lmax;
+        }
+#pragma unroll
+        for (int p = 0; p < RPX; ++p) {
+          if (p >= rex) break;
+          double v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = in[u] ? srow[p][cidx[u]] * scl[p] : 0.0;
+          emit_slices4(a.Wq, a.Kpad, a.npad, tl * rex + p, j0, v[0], v[1], v[2], v[3]);
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    double2* vout = reinterpret_cast<double2*>(a.Vout + tl * a.npad * rp);
     for (int64_t j = lane; j < a.npad; j += 32) {
       const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
       const bool in = (word & bit) != 0;

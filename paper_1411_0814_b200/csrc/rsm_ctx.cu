@@ -451,19 +451,21 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   c->G.ensure(sizeof(double) * n * n);
   c->colcnt.ensure(sizeof(int) * npad);
   ck(cudaMemsetAsync(c->colcnt.p, 0, sizeof(int) * npad, c->stream), "memset");
-  // stage 2 writes each trial's top vectors expanded (rp/2 planes of npad
-  // pairs, zero outside the support; k_svd.cu) so stage 3 streams fixed
-  // 16-byte-aligned runs. Trials go through stages 2-3 in chunks whose
-  // expanded vectors fit the buffer budget; stage 3 accumulates across chunks.
+  // stage 2 hands stage 3 each trial's top vectors zero outside the support:
+  // as int8 digit slices (rows t*rex + p of S x Kpad x npad, k_gram_i8.cu)
+  // for the tensor-core path, or expanded FP64 planes (rp/2 planes of npad
+  // pairs) for the FP64 kernel. Trials go through stages 2-3 in chunks whose
+  // hand-off buffer fits the budget; stage 3 accumulates across chunks.
+  const bool i8 = gram_on_tensor_cores();
+  const int S8 = rsmk::gram_i8_slices();
   const int64_t rp = (rex + 1) & ~1;
-  const int64_t tbytes = npad * rp * (int64_t)sizeof(double);
+  const int64_t tbytes = i8 ? (int64_t)S8 * rex * npad : npad * rp * (int64_t)sizeof(double);
   // RSM_CHUNK_BYTES overrides the budget (tests exercise the multi-chunk path)
-  static const int64_t budget = [] {
+  const int64_t budget = [] {
     const char* e = getenv("RSM_CHUNK_BYTES");
-    return e ? std::max<int64_t>(1, atoll(e)) : ((int64_t)6 << 30);
+    return e ? std::max<int64_t>(1, atoll(e)) : ((int64_t)12 << 30);
   }();
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(Tl, budget / tbytes));
-  const bool i8 = gram_on_tensor_cores();
   const int cpl = rsmk::gram_cols_per_lane(rex);
   int64_t ntiles = 0;
   if (i8) {
@@ -476,7 +478,6 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   // tensor-core path: K = trials * rex rows of int8 slices per trial chunk,
   // split into nk K-chunks (P slices) so the work units fill the SMs and each
   // chunk's int32 sums stay exact (k_gram_i8.cu)
-  const int S8 = rsmk::gram_i8_slices();
   const int64_t Kpad0 = ceil_div(std::max<int64_t>(chunk, 1) * rex, 32) * 32;
   int nk = 1;
   if (i8) {
@@ -496,8 +497,8 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     }
     c->P.ensure(sizeof(double) * (size_t)nslices * npad * npad);
     c->t_cm.ensure(sizeof(uint32_t) * chunk * cmw);
-    c->Vtrial.ensure((size_t)tbytes * chunk);
     if (i8) c->Wq.ensure((size_t)S8 * Kpad0 * npad);
+    else c->Vtrial.ensure((size_t)tbytes * chunk);
     int64_t Lmax = m2 ? out.sel.qmax : 0;
     if (!m2) for (int64_t t = t_lo; t < t_hi; ++t) Lmax = std::max<int64_t>(Lmax, hq[t]);
     const int64_t Lpad = std::max<int64_t>(2, (Lmax + 1) & ~int64_t(1));
@@ -519,7 +520,19 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
       a.t_lo = c0; a.t_hi = c1;
       a.block = K; a.rex = rex;
       a.t_cm = c->t_cm.as<uint32_t>(); a.cmw = cmw; a.npad = npad;
-      a.Vout = c->Vtrial.as<double>();
+      const int64_t Kpad = ceil_div((c1 - c0) * rex, 32) * 32;
+      if (i8) {
+        a.Wq = c->Wq.as<int8_t>();
+        a.Kpad = Kpad;
+        // rows past the chunk's trials * rex are zero (read by the last K-step)
+        const int64_t used = (c1 - c0) * rex;
+        if (Kpad > used)
+          for (int sl = 0; sl < S8; ++sl)
+            ck(cudaMemsetAsync(a.Wq + ((int64_t)sl * Kpad + used) * npad, 0, (size_t)(Kpad - used) * npad,
+                               c->stream), "memset");
+      } else {
+        a.Vout = c->Vtrial.as<double>();
+      }
       a.colcnt = c->colcnt.as<int>();
       if (!use_smem) {
         c->svd_scr.ensure(vecb * grid);
@@ -548,8 +561,6 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
       if (c0 == t_lo) record(c, 2);  // with several chunks, later stage-2 work counts as stage 3
       // stage 3
       if (i8) {
-        const int64_t Kpad = ceil_div((c1 - c0) * rex, 32) * 32;
-        rsmk::launch_slice_planes(c->Vtrial.as<double>(), c1 - c0, rex, npad, Kpad, c->Wq.as<int8_t>(), c->stream);
         rsmk::GramI8Args g{};
         g.W = c->Wq.as<int8_t>();
         g.npad = npad;
@@ -563,7 +574,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
         const char* dg = getenv("RSM_I8_DIAG");
         g.diag = dg ? atoi(dg) : 0;
         ck(rsmk::launch_gram_i8(g, c->sms, c->stream), "gram (tcgen05) launch");
-        c->launches += 2;
+        ++c->launches;
       } else {
         rsmk::GramArgs g{};
         g.t_cm = c->t_cm.as<uint32_t>();

@@ -467,4 +467,46 @@ __device__ __forceinline__ int warp_jacobi_abs(double* A, int lda, double* V, in
   }
 }
 
+// ---- stage 2 -> stage 3 hand-off: int8 digit slices (k_gram_i8.cu) ----
+// digits per value of the exact integer split of the harvested vectors
+constexpr int kGramSlices = 6;
+
+// Balanced signed digits: w = a[0] 2^-6 + sum_{1<=s<S} a[s] 2^(-6-8s) + e.
+// X = rint(w 2^(6+8(S-1))) is an exact integer (|X| <= 2^54 for |w| <= 1,
+// S <= 7; |e| <= 2^(-7-8(S-1))). Its balanced base-256 digits (every digit
+// but the leading one in [-128, 127]) come from one addition: with
+// Y = X + sum_{s<S-1} 128 * 256^s, byte s of Y minus 128 is digit s (LSB
+// first) and Y >> 8(S-1) is the leading digit a[0] (in [-64, 64]); "minus 128"
+// of a byte is its int8 reinterpretation after XOR 0x80. Returned packed: byte
+// s (from the least significant) holds a[S-1-s] as int8.
+template <int S>
+__device__ __forceinline__ unsigned long long digits_i8(double x) {
+  static_assert(S >= 2 && S <= 7, "digit count");
+  constexpr int LB = 8 * (S - 1);  // bits of the lower digits
+  constexpr unsigned long long C = 0x8080808080808080ull & ((1ull << LB) - 1ull);
+  const long long X = __double2ll_rn(x * (double)(1ll << (6 + LB)));
+  const long long Y = X + (long long)C;
+  return (((unsigned long long)Y ^ C) & ((1ull << LB) - 1ull)) | (((unsigned long long)(Y >> LB) & 0xFFull) << LB);
+}
+
+// Four consecutive columns j0..j0+3 of trial-vector row `krow`: one 32-bit
+// store per digit slice into W[s][krow][j0..j0+3] (S x Kpad x npad int8,
+// MN-major; a warp's lanes cover 128 consecutive bytes per store). The 4 x S
+// byte transpose is three byte permutes per slice.
+__device__ __forceinline__ void emit_slices4(int8_t* W, int64_t Kpad, int64_t npad, int64_t krow, int64_t j0,
+                                             double v0, double v1, double v2, double v3) {
+  constexpr int S = kGramSlices;
+  const unsigned long long z0 = digits_i8<S>(v0), z1 = digits_i8<S>(v1), z2 = digits_i8<S>(v2),
+                           z3 = digits_i8<S>(v3);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int b = S - 1 - s;  // byte of digit a[s]
+    const int sh = b < 4 ? 0 : 32;
+    const unsigned p = (unsigned)(b & 3);
+    const unsigned t01 = __byte_perm((unsigned)(z0 >> sh), (unsigned)(z1 >> sh), p | ((4u + p) << 4));
+    const unsigned t23 = __byte_perm((unsigned)(z2 >> sh), (unsigned)(z3 >> sh), p | ((4u + p) << 4));
+    *reinterpret_cast<uint32_t*>(W + ((int64_t)s * Kpad + krow) * npad + j0) = __byte_perm(t01, t23, 0x5410);
+  }
+}
+
 }  // namespace rsmd

@@ -32,7 +32,9 @@ struct SvdArgs {
   uint32_t* t_cm;        // local trials x cmw support words
   int64_t cmw;
   int64_t npad;          // expanded column count (multiple of 128)
-  double* Vout;          // local trials x (rp/2) planes x npad x 2 (see k_svd.cu)
+  double* Vout;          // local trials x (rp/2) planes x npad x 2 (see k_svd.cu), or null
+  int8_t* Wq;            // or: int8 digit slices [kGramSlices][Kpad][npad], rows t*rex + p (k_gram_i8.cu)
+  int64_t Kpad;
   int* colcnt;           // n per-column trial counts
   double* scratch;       // per-CTA vector scratch when shared memory is too small
   uint32_t* scratch_u32; // per-CTA 2*mwp words (column branch)
@@ -144,8 +146,6 @@ void launch_gram_reduce(const double* P, int nslices, int64_t npad, int64_t n, c
 int gram_i8_slices();
 int64_t gram_i8_kmax();
 void gram_i8_tiles(int64_t npad, std::vector<int2>& t);
-void launch_slice_planes(const double* V, int64_t T, int rex, int64_t npad, int64_t Kpad, int8_t* W,
-                         cudaStream_t s);
 cudaError_t launch_gram_i8(const GramI8Args& a, int sms, cudaStream_t s);
 // k_eig.cu
 int eig_part_width(int b);
