@@ -101,6 +101,16 @@ const char* rsm_last_error(const rsm_ctx* ctx);
 rsm_status rsm_ctx_create(rsm_ctx** out, int device, int world, int rank, const void* nccl_id);
 rsm_status rsm_ctx_destroy(rsm_ctx* ctx);
 rsm_status rsm_nccl_unique_id(void* out128);
+
+/* In-process rank group whose collectives go through host memory instead of
+ * NCCL (test / diagnostic hook): `world` contexts, possibly on one GPU, each
+ * driven by its own host thread, take the multi-rank code path -- trial
+ * shards, the accumulator and column-count all-reduce, row shards and the U
+ * all-gather -- with sums formed in rank order on every rank. */
+typedef struct rsm_host_group rsm_host_group;
+rsm_status rsm_host_group_create(int world, rsm_host_group** out);
+rsm_status rsm_host_group_destroy(rsm_host_group* g);
+rsm_status rsm_ctx_create_host_group(rsm_ctx** out, int device, rsm_host_group* g, int rank);
 /* Work split across ranks (host-only, no device): rank owns [lo, hi) of
  * total units -- accepted trials in stage 2-3, rows in stage 5. */
 void rsm_shard_range(int64_t total, int world, int rank, int64_t* lo, int64_t* hi);

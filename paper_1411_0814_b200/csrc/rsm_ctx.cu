@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -90,7 +91,7 @@ struct Nccl {
   }
 };
 Nccl g_nccl;
-constexpr int kNcclFloat64 = 8, kNcclInt64 = 4, kNcclSum = 0;
+constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclSum = 0;
 
 struct View {
   const double* Y;
@@ -108,12 +109,37 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace
 
+// In-process rank group whose collectives exchange through host memory: the
+// multi-rank code path (trial shards, accumulator all-reduce, row shards and
+// the U all-gather) runs with several contexts on one GPU, one host thread
+// per rank. Test and diagnostic use only; N GPUs use NCCL.
+struct rsm_host_group {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<std::vector<char>> buf;  // per-rank staging
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 struct rsm_ctx {
   int device = 0;
   int world = 1, rank = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
   NcclComm comm = nullptr;
+  rsm_host_group* hg = nullptr;  // host-exchange collectives instead of NCCL
   bool coll = false;  // collectives on (world > 1, or forced for a one-rank check)
   std::string err;
 
@@ -134,7 +160,7 @@ struct rsm_ctx {
   // workspace
   DevBuf sel_idx, sel_q, blockcnt, selstate, t_attempt, t_q, t_idx, t_cm, Vtrial,
       colcnt, svd_scr, svd_scr32, P, tiles, G, eX, eY, eZ, ePart, eW, eI, eD, Vhat, U, rowres,
-      flagged, dsum, cnt64, Wq, tiles8;
+      flagged, dsum, cnt64, Wq, tiles8, ugather;
   int64_t tiles_n = -1;
   int64_t tiles8_n = -1;  // tcgen05 stage-3 tile list valid for this npad
   int ntiles8 = 0;
@@ -162,6 +188,57 @@ namespace {
 thread_local std::string g_err;
 
 void record(rsm_ctx* c, int i) { ck(cudaEventRecord(c->ev[i], c->stream), "cudaEventRecord"); }
+
+// ---------------------------------------------------------------- collectives
+// Sum over ranks in place (FP64 or int32 elements): NCCL on the context
+// stream, or the host group (every rank adds the staged buffers in rank order,
+// so all ranks hold bitwise identical sums).
+template <class T>
+void coll_allreduce_sum(rsm_ctx* c, T* dev, size_t count) {
+  static_assert(sizeof(T) == 8 || sizeof(T) == 4, "f64 or i32");
+  if (!c->hg) {
+    if (g_nccl.allReduce(dev, dev, count, sizeof(T) == 8 ? kNcclFloat64 : kNcclInt32, kNcclSum, c->comm,
+                         c->stream) != 0)
+      fail(RSM_ERR_INTERNAL, "ncclAllReduce failed");
+    return;
+  }
+  rsm_host_group* g = c->hg;
+  const size_t bytes = sizeof(T) * count;
+  std::vector<char>& mine = g->buf[c->rank];
+  mine.resize(bytes);
+  ck(cudaMemcpyAsync(mine.data(), dev, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H allreduce");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  g->barrier();
+  std::vector<T> sum(count, T(0));
+  for (int r = 0; r < g->world; ++r) {
+    const T* x = reinterpret_cast<const T*>(g->buf[r].data());
+    for (size_t i = 0; i < count; ++i) sum[i] += x[i];
+  }
+  g->barrier();  // every rank has read every buffer
+  ck(cudaMemcpyAsync(dev, sum.data(), bytes, cudaMemcpyHostToDevice, c->stream), "H2D allreduce");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
+// recv[r * count .. (r+1) * count) = rank r's send (rank order)
+void coll_allgather(rsm_ctx* c, const double* send, double* recv, size_t count) {
+  if (!c->hg) {
+    if (g_nccl.allGather(send, recv, count, kNcclFloat64, c->comm, c->stream) != 0)
+      fail(RSM_ERR_INTERNAL, "ncclAllGather failed");
+    return;
+  }
+  rsm_host_group* g = c->hg;
+  const size_t bytes = sizeof(double) * count;
+  std::vector<char>& mine = g->buf[c->rank];
+  mine.resize(bytes);
+  ck(cudaMemcpyAsync(mine.data(), send, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H allgather");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  g->barrier();
+  for (int r = 0; r < g->world; ++r)
+    ck(cudaMemcpyAsync(recv + (size_t)r * count, g->buf[r].data(), bytes, cudaMemcpyHostToDevice, c->stream),
+       "H2D allgather");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  g->barrier();
+}
 
 // ---------------------------------------------------------------- layout
 // the byte mask, rebuilt from the packed rows when the host delivered words
@@ -597,13 +674,17 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   rsmk::launch_gram_reduce(c->P.as<double>(), nslices, npad, n, c->colcnt.as<int>(), c->G.as<double>(), c->stream);
   ++c->launches;
   if (c->coll) {
-    if (g_nccl.allReduce(c->G.p, c->G.p, (size_t)(n * n), kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
-      fail(RSM_ERR_INTERNAL, "ncclAllReduce failed");
+    // the one exchange of stages 1-3: partial accumulators (each with its
+    // shard's column counts on the diagonal) and the counts themselves, for
+    // the zero-row certificate of stage 4 (harvest.cpp:110-117 merges the
+    // per-worker Grams the same way)
+    coll_allreduce_sum(c, c->G.as<double>(), (size_t)(n * n));
+    coll_allreduce_sum(c, c->colcnt.as<int>(), (size_t)npad);
   }
   record(c, 4);
   ck(cudaGetLastError(), "gram reduce");
   c->G_n = n;
-  c->G_harvest = (c->world == 1);
+  c->G_harvest = true;  // G = diag(colcnt) - PSD with the global column counts
   return out;
 }
 
@@ -757,45 +838,29 @@ SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& out
   double ss = 0.0;
   int fl = 0;
   if (c->coll) {
-    // row shards: gather U, sum the scalars
-    double* tmp = nullptr;
-    ck(cudaMallocAsync((void**)&tmp, sizeof(double) * 2, c->stream), "malloc");
-    // pack [ss, flagged] as doubles for one allreduce
-    double host2[2];
-    ck(cudaMemcpyAsync(&ss, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
-    ck(cudaMemcpyAsync(&fl, c->flagged.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
-    ck(cudaStreamSynchronize(c->stream), "sync");
-    host2[0] = ss;
-    host2[1] = (double)fl;
-    ck(cudaMemcpyAsync(tmp, host2, sizeof(double) * 2, cudaMemcpyHostToDevice, c->stream), "H2D");
-    if (g_nccl.allReduce(tmp, tmp, 2, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
-      fail(RSM_ERR_INTERNAL, "ncclAllReduce failed");
-    ck(cudaMemcpyAsync(host2, tmp, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    // U row blocks are equal-sized only when world divides m; gather via
-    // per-rank broadcast-free allgather of a padded buffer
+    // row shards: sum the scalars on the device, gather U through a padded
+    // buffer (row blocks differ in size when world does not divide m)
+    coll_allreduce_sum(c, c->dsum.as<double>(), 1);
+    coll_allreduce_sum(c, c->flagged.as<int>(), 1);
     const int64_t maxrows = ceil_div(v.m, c->world);
-    DevBuf pad;
-    pad.ensure(sizeof(double) * maxrows * r * (c->world + 1));
-    double* sendb = pad.as<double>() + (size_t)maxrows * r * c->world;
-    ck(cudaMemcpyAsync(sendb, out + lo * r, sizeof(double) * (hi - lo) * r, cudaMemcpyDeviceToDevice, c->stream), "D2D");
-    if (g_nccl.allGather(sendb, pad.p, (size_t)(maxrows * r), kNcclFloat64, c->comm, c->stream) != 0)
-      fail(RSM_ERR_INTERNAL, "ncclAllGather failed");
+    c->ugather.ensure(sizeof(double) * maxrows * r * (c->world + 1));
+    double* pad = c->ugather.as<double>();
+    double* sendb = pad + (size_t)maxrows * r * c->world;
+    if (hi > lo)
+      ck(cudaMemcpyAsync(sendb, out + lo * r, sizeof(double) * (hi - lo) * r, cudaMemcpyDeviceToDevice, c->stream),
+         "D2D");
+    coll_allgather(c, sendb, pad, (size_t)(maxrows * r));
     for (int g = 0; g < c->world; ++g) {
       int64_t glo, ghi;
       rsm_shard_range(v.m, c->world, g, &glo, &ghi);
-      ck(cudaMemcpyAsync(out + glo * r, pad.as<double>() + (size_t)g * maxrows * r,
-                         sizeof(double) * (ghi - glo) * r, cudaMemcpyDeviceToDevice, c->stream), "D2D");
+      if (ghi > glo)
+        ck(cudaMemcpyAsync(out + glo * r, pad + (size_t)g * maxrows * r, sizeof(double) * (ghi - glo) * r,
+                           cudaMemcpyDeviceToDevice, c->stream), "D2D");
     }
-    ck(cudaStreamSynchronize(c->stream), "sync");
-    ck(cudaFreeAsync(tmp, c->stream), "free");
-    pad.release();
-    ss = host2[0];
-    fl = (int)host2[1];
-  } else {
-    ck(cudaMemcpyAsync(&ss, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
-    ck(cudaMemcpyAsync(&fl, c->flagged.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
-    ck(cudaStreamSynchronize(c->stream), "solve_u");
   }
+  ck(cudaMemcpyAsync(&ss, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(&fl, c->flagged.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "solve_u");
   ck(cudaGetLastError(), "solve_u kernels");
   SolveUOut o;
   o.flagged = fl;
@@ -999,6 +1064,35 @@ rsm_status rsm_ctx_create(rsm_ctx** out, int device, int world, int rank, const 
   });
 }
 
+rsm_status rsm_host_group_create(int world, rsm_host_group** out) {
+  return guard(nullptr, [&] {
+    if (!out) fail(RSM_ERR_INVALID_CONFIG, "null output pointer");
+    if (world < 1) fail(RSM_ERR_INVALID_CONFIG, "bad world");
+    rsm_host_group* g = new rsm_host_group();
+    g->world = world;
+    g->buf.resize(world);
+    *out = g;
+  });
+}
+
+rsm_status rsm_host_group_destroy(rsm_host_group* g) {
+  delete g;
+  return RSM_OK;
+}
+
+rsm_status rsm_ctx_create_host_group(rsm_ctx** out, int device, rsm_host_group* g, int rank) {
+  if (!g) return guard(nullptr, [&] { fail(RSM_ERR_INVALID_CONFIG, "null host group"); });
+  rsm_status st = rsm_ctx_create(out, device, 1, 0, nullptr);
+  if (st) return st;
+  return guard(*out, [&] {
+    if (rank < 0 || rank >= g->world) fail(RSM_ERR_INVALID_CONFIG, "bad world/rank");
+    (*out)->world = g->world;
+    (*out)->rank = rank;
+    (*out)->hg = g;
+    (*out)->coll = true;
+  });
+}
+
 rsm_status rsm_ctx_destroy(rsm_ctx* c) {
   if (!c) return RSM_OK;
   cudaSetDevice(c->device);
@@ -1008,7 +1102,7 @@ rsm_status rsm_ctx_destroy(rsm_ctx* c) {
                     &c->t_idx, &c->t_cm, &c->Vtrial, &c->colcnt, &c->svd_scr,
                     &c->svd_scr32, &c->P, &c->tiles, &c->G, &c->eX, &c->eY, &c->eZ, &c->ePart,
                     &c->eW, &c->eI, &c->eD, &c->Vhat, &c->U, &c->rowres, &c->flagged, &c->dsum,
-                    &c->cnt64, &c->Wq, &c->tiles8};
+                    &c->cnt64, &c->Wq, &c->tiles8, &c->ugather};
   for (DevBuf* b : bufs) b->release();
   if (c->hstage) cudaFreeHost(c->hstage);
   for (auto& e : c->ev) cudaEventDestroy(e);

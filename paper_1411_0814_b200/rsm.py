@@ -120,6 +120,9 @@ def lib():
         "rsm_fp64_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
         "rsm_dmma_peak_tflops": (i32, [C.c_int, C.POINTER(dbl)]),
         "rsm_shard_range": (None, [i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]),
+        "rsm_host_group_create": (i32, [C.c_int, C.POINTER(_P)]),
+        "rsm_host_group_destroy": (i32, [_P]),
+        "rsm_ctx_create_host_group": (i32, [C.POINTER(_P), C.c_int, _P, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -137,7 +140,8 @@ def exported_symbols():
             "rsm_ctx_launch_count", "rsm_ctx_last_load_h2d_bytes", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_als", "rsm_harvest_gram", "rsm_solve_v",
             "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_generate_tracks", "rsm_load_matrix_csv",
             "rsm_save_matrix_csv", "rsm_dataset_checksum", "rsm_free", "rsm_fp64_peak_tflops",
-            "rsm_dmma_peak_tflops", "rsm_shard_range"]
+            "rsm_dmma_peak_tflops", "rsm_shard_range", "rsm_host_group_create", "rsm_host_group_destroy",
+            "rsm_ctx_create_host_group"]
 
 
 def _check(st: int, ctx=None):
@@ -284,15 +288,35 @@ def _report(r: _Report) -> DecompositionReport:
 
 # ------------------------------------------------------------------ context
 
+class HostGroup:
+    """In-process rank group whose collectives go through host memory
+    (rsm_host_group_*): `world` Contexts, possibly on one GPU and each driven by
+    its own thread, take the multi-rank code path without NCCL."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        _check(lib().rsm_host_group_create(world, C.byref(h)))
+        self.h, self.world = h, world
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().rsm_host_group_destroy(self.h)
+            self.h = None
+
+
 class Context:
     """A device context: owns the device-resident matrix, workspace, stream
-    and (for world > 1) the NCCL communicator."""
+    and (for world > 1) the NCCL communicator or a HostGroup membership."""
 
-    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, nccl_id: bytes | None = None):
+    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, nccl_id: bytes | None = None,
+                 host_group: "HostGroup | None" = None):
         L = lib()
         h = C.c_void_p()
-        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        st = L.rsm_ctx_create(C.byref(h), device, world, rank, C.cast(idbuf, C.c_void_p) if idbuf else None)
+        if host_group is not None:
+            st = L.rsm_ctx_create_host_group(C.byref(h), device, host_group.h, rank)
+        else:
+            idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            st = L.rsm_ctx_create(C.byref(h), device, world, rank, C.cast(idbuf, C.c_void_p) if idbuf else None)
         _check(st)
         self.h = h
         self.m = self.n = 0
