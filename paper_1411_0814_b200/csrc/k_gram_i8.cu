@@ -351,7 +351,15 @@ cudaError_t launch_i8_t(const GramI8Args& a, int sms, cudaStream_t s) {
 
 }  // namespace
 
-int gram_i8_slices() { return rsmd::kGramSlices; }
+// RSM_I8_SLICES (5..7) overrides the default digit count
+int gram_i8_slices() {
+  static const int s = [] {
+    const char* e = getenv("RSM_I8_SLICES");
+    const int v = e ? atoi(e) : rsmd::kGramSlices;
+    return v < 5 ? 5 : (v > 7 ? 7 : v);
+  }();
+  return s;
+}
 
 // int32 exactness: a class sums at most S products of |digits| <= 128, so
 // |acc| <= S * 16384 * Kc < 2^31 for Kc <= 16384 and S <= 7
@@ -365,7 +373,11 @@ void gram_i8_tiles(int64_t npad, std::vector<int2>& t) {
 }
 
 cudaError_t launch_gram_i8(const GramI8Args& a, int sms, cudaStream_t s) {
-  return launch_i8_t<rsmd::kGramSlices>(a, sms, s);
+  switch (a.S) {
+    case 5: return launch_i8_t<5>(a, sms, s);
+    case 7: return launch_i8_t<7>(a, sms, s);
+    default: return launch_i8_t<6>(a, sms, s);
+  }
 }
 
 }  // namespace rsmk

@@ -107,6 +107,66 @@ __host__ __device__ constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 *
 
 }  // namespace
 
+// Normal-equation solve of one row (packed upper A, b, observed count nj):
+// Cholesky in registers; rows with nj < R or a pivot <= 1e-10 max diag take the
+// eigendecomposition pseudo-inverse. Returns true when the row is flagged
+// (detail/row_solve.hpp:26-35: fewer than r observations or rank < r). The
+// factor keeps the reciprocal of each pivot (one rsqrt per column), so the
+// factorisation and both substitutions multiply instead of dividing: R
+// reciprocal square roots on the dependent chain instead of R square roots
+// plus R(R+1)/2 + 2R divisions.
+template <int R>
+__device__ __forceinline__ bool row_solve(const double* A, const double* bv, int nj, double* u) {
+  constexpr int NA = R * (R + 1) / 2;
+  bool slow = nj < R;
+  if (!slow) {
+    double L[NA], Li[R];  // L: lower factor, row-major packed; Li: 1 / L_ii
+    double dmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) dmax = fmax(dmax, A[i * R - i * (i - 1) / 2]);
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        double v = A[j * R - j * (j - 1) / 2 + (i - j)];
+#pragma unroll
+        for (int k = 0; k < j; ++k) v = fma(-L[i * (i + 1) / 2 + k], L[j * (j + 1) / 2 + k], v);
+        if (i == j) {
+          if (!(v > 1e-10 * dmax)) slow = true;
+          Li[i] = rsqrt(fmax(v, 1e-300));
+          L[q] = v * Li[i];
+        } else {
+          L[q] = v * Li[j];
+        }
+        ++q;
+      }
+    }
+    if (!slow) {
+      double z[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        double v = bv[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) v = fma(-L[i * (i + 1) / 2 + k], z[k], v);
+        z[i] = v * Li[i];
+      }
+#pragma unroll
+      for (int i = R - 1; i >= 0; --i) {
+        double v = z[i];
+#pragma unroll
+        for (int k = i + 1; k < R; ++k) v = fma(-L[k * (k + 1) / 2 + i], u[k], v);
+        u[i] = v * Li[i];
+      }
+    }
+  }
+  if (slow) {
+    const int rank = pinv_solve<R>(A, bv, u);
+    return (nj < R) || (rank < R);
+  }
+  return false;
+}
+
 // One warp per row (rows strided over the grid's warps). STAGE 1: two row
 // buffers per warp in shared memory, the next row's values and mask words
 // arriving by two 1-D bulk copies (TMA) on the buffer's mbarrier, issued by
@@ -353,53 +413,7 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     const int nj = (int)total(NA + R);
 
     double u[R];
-    bool flagged = false;
-    bool slow = nj < R;
-    if (!slow) {
-      // Cholesky of the packed normal matrix (lower factor, row-major packed)
-      double L[NA];
-      double dmax = 0.0;
-#pragma unroll
-      for (int i = 0; i < R; ++i) dmax = fmax(dmax, A[i * R - i * (i - 1) / 2]);
-      int q = 0;
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-#pragma unroll
-        for (int j = 0; j <= i; ++j) {
-          double v = A[j * R - j * (j - 1) / 2 + (i - j)];
-#pragma unroll
-          for (int k = 0; k < j; ++k) v -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
-          if (i == j) {
-            if (!(v > 1e-10 * dmax)) slow = true;
-            L[q] = sqrt(fmax(v, 0.0));
-          } else {
-            L[q] = v / L[j * (j + 1) / 2 + j];
-          }
-          ++q;
-        }
-      }
-      if (!slow) {
-        double z[R];
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-          double v = bv[i];
-#pragma unroll
-          for (int k = 0; k < i; ++k) v -= L[i * (i + 1) / 2 + k] * z[k];
-          z[i] = v / L[i * (i + 1) / 2 + i];
-        }
-#pragma unroll
-        for (int i = R - 1; i >= 0; --i) {
-          double v = z[i];
-#pragma unroll
-          for (int k = i + 1; k < R; ++k) v -= L[k * (k + 1) / 2 + i] * u[k];
-          u[i] = v / L[i * (i + 1) / 2 + i];
-        }
-      }
-    }
-    if (slow) {
-      const int rank = pinv_solve<R>(A, bv, u);
-      flagged = (nj < R) || (rank < R);
-    }
+    const bool flagged = row_solve<R>(A, bv, nj, u);
     // second pass over the row still in shared memory: direct residual
     double ss = 0.0;
     auto res_y = [&](int64_t c, bool k, double yraw) {
@@ -448,74 +462,28 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
   }
 }
 
-// Normal-equation solve of one row (packed upper A, b, observed count nj):
-// Cholesky in registers; rows with nj < R or a pivot <= 1e-10 max diag take the
-// eigendecomposition pseudo-inverse. Returns true when the row is flagged
-// (detail/row_solve.hpp:26-35: fewer than r observations or rank < r). Same
-// arithmetic as the solve inside k_solve_u.
-template <int R>
-__device__ __forceinline__ bool row_solve(const double* A, const double* bv, int nj, double* u) {
-  constexpr int NA = R * (R + 1) / 2;
-  bool slow = nj < R;
-  if (!slow) {
-    double L[NA];
-    double dmax = 0.0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) dmax = fmax(dmax, A[i * R - i * (i - 1) / 2]);
-    int q = 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-#pragma unroll
-      for (int j = 0; j <= i; ++j) {
-        double v = A[j * R - j * (j - 1) / 2 + (i - j)];
-#pragma unroll
-        for (int k = 0; k < j; ++k) v -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
-        if (i == j) {
-          if (!(v > 1e-10 * dmax)) slow = true;
-          L[q] = sqrt(fmax(v, 0.0));
-        } else {
-          L[q] = v / L[j * (j + 1) / 2 + j];
-        }
-        ++q;
-      }
-    }
-    if (!slow) {
-      double z[R];
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        double v = bv[i];
-#pragma unroll
-        for (int k = 0; k < i; ++k) v -= L[i * (i + 1) / 2 + k] * z[k];
-        z[i] = v / L[i * (i + 1) / 2 + i];
-      }
-#pragma unroll
-      for (int i = R - 1; i >= 0; --i) {
-        double v = z[i];
-#pragma unroll
-        for (int k = i + 1; k < R; ++k) v -= L[k * (k + 1) / 2 + i] * u[k];
-        u[i] = v / L[i * (i + 1) / 2 + i];
-      }
-    }
-  }
-  if (slow) {
-    const int rank = pinv_solve<R>(A, bv, u);
-    return (nj < R) || (rank < R);
-  }
-  return false;
-}
-
-// Fused-pass row solver (r <= 4, V-hat in shared memory, rows staged by TMA):
-// as k_solve_u<R, true, 1>, but the residual pass of a warp's row k runs in
-// the same column loop as the accumulation pass of its next row k+1, so every
-// shared-memory read of V-hat (the dominant shared-memory traffic) serves both
-// passes. Row k stays in its buffer until that loop ends; the buffer is then
-// refilled with row k+2 while row k+1 is solved.
+// Fused-pass row solver (r <= 4, V-hat in shared memory, rows staged by TMA).
+// The residual pass of a warp's row k runs in the same column loop as the
+// accumulation pass of its next row k+1, so every shared-memory read of V-hat
+// serves both rows. Row k stays in its buffer until that loop ends; the
+// buffer is then refilled with row k+2 (already pulled into L2 by a bulk
+// prefetch issued when the loop started) while row k+1 is solved.
+//
+// Per column the loop does only what every cell needs: V_O^T y (R FMAs on the
+// selected value) for row k+1 and the direct residual (R FMAs from y, one
+// select, one FMA) for row k. The normal matrix V_O^T V_O is formed from the
+// MINORITY cells of the row: when at least half the row is observed, as
+// V^T V (once per CTA, fixed order) minus the hidden cells' outer products,
+// otherwise directly from the observed cells; each lane walks the set bits of
+// its own mask words. At config 3 (rho = 0.8) that is ~0.2 n outer products per
+// row instead of n.
 template <int R>
 __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   constexpr int NP = (R + 1) / 2;
   constexpr int NA = R * (R + 1) / 2;
-  constexpr int NV = pow2_at_least(NA + R + 1);
+  constexpr int NV = pow2_at_least(NA + R);
   extern __shared__ __align__(16) double sm[];
+  __shared__ double Aall[NA];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int64_t npd = (n + 1) & ~int64_t(1);
@@ -533,6 +501,31 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     const double x0 = a.V[c * R + 2 * p];
     const double x1 = (2 * p + 1 < R) ? a.V[c * R + 2 * p + 1] : 0.0;
     Vp[e] = make_double2(x0, x1);
+  }
+  if (warp == 0) {
+    // V^T V (packed upper): lane l sums columns l, l+32, ..., then a fixed
+    // butterfly -- the same order in every CTA and launch shape
+    double part[NA];
+#pragma unroll
+    for (int p = 0; p < NA; ++p) part[p] = 0.0;
+    for (int64_t c = lane; c < n; c += 32) {
+      double v[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) v[k] = a.V[c * R + k];
+      int p = 0;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = i; j < R; ++j) {
+          part[p] = fma(v[i], v[j], part[p]);
+          ++p;
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < NA; ++p) {
+      const double t = warp_sum(part[p]);
+      if (lane == 0) Aall[p] = t;
+    }
   }
   __syncthreads();
   auto vload = [&](int64_t c, double* v) {
@@ -563,6 +556,13 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
           : "memory");
     }
   };
+  auto prefetch_l2 = [&](int64_t row) {
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.Y + row * n), "r"(ybytes) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.bitsR + row * a.nwp), "r"(wbytes)
+                   : "memory");
+    }
+  };
   unsigned phase = 0u;
   auto wait_buf = [&](int b) {
     const unsigned bar = smem_u32(bars + 2 * warp + b);
@@ -582,46 +582,67 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   if (r0 >= a.row_hi) return;
   const int64_t nrows = (a.row_hi - r0 + nw - 1) / nw;  // this warp's rows: r0 + k nw
   const int nfull = (int)(n >> 5);
+  const int nwn = (int)((n + 31) >> 5);  // mask words holding columns
   const bool tail = (int64_t)nfull * 32 + lane < n;
   issue(r0, 0);
   if (nrows > 1) issue(r0 + nw, 1);
-  // accumulation terms of column c of a row (hidden cells selected away)
-  auto accum = [&](double* acc, const double* v, double yraw, bool k) {
-    const double kf = k ? 1.0 : 0.0;
+  // V_O^T y term of column c (the hidden cell's NaN is selected away)
+  auto accum_b = [&](double* acc, const double* v, double yraw, bool k) {
     const double yc = k ? yraw : 0.0;
-    double t[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) t[i] = kf * v[i];
-    int p = 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-#pragma unroll
-      for (int j = i; j < R; ++j) {
-        acc[p] = fma(t[i], v[j], acc[p]);
-        ++p;
-      }
 #pragma unroll
     for (int i = 0; i < R; ++i) acc[NA + i] = fma(yc, v[i], acc[NA + i]);
   };
-  auto resid = [&](double& ss, const double* v, const double* u, double yraw, bool k) {
-    double p = 0.0;
+  // direct residual term: d = y - u.v from y (nu = -u), zero when hidden
+  auto resid = [&](double& ss, const double* v, const double* nu, double yraw, bool k) {
+    double d = yraw;
 #pragma unroll
-    for (int q = 0; q < R; ++q) p = fma(u[q], v[q], p);
-    const double d = k ? yraw - p : 0.0;
+    for (int q = 0; q < R; ++q) d = fma(nu[q], v[q], d);
+    d = k ? d : 0.0;
     ss = fma(d, d, ss);
   };
-  // reduce a row's accumulators and solve it
+  // normal matrix from the row's minority cells, then reduce and solve
   auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u) -> bool {
     int cnt = 0;
-    for (int64_t w = lane; w < a.nwp; w += 32) cnt += __popc(wd[w]);
-    acc[NA + R] = (double)cnt;
+    for (int w = lane; w < nwn; w += 32) cnt += __popc(wd[w]);
+    const int nj = warp_sum_int(cnt);  // mask words are zero beyond n
+    const bool hid = 2 * (int64_t)nj >= n;
+    for (int w = lane; w < nwn; w += 32) {
+      const int rem = (int)(n - (int64_t)w * 32);
+      const unsigned valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+      unsigned bits = hid ? (~wd[w] & valid) : wd[w];
+      // two cells per iteration (independent loads and FMA chains); a lone
+      // last cell pairs with itself at weight 0
+      while (bits) {
+        const int p0 = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const bool two = bits != 0u;
+        const int p1 = two ? __ffs(bits) - 1 : p0;
+        bits &= bits - 1u;
+        double v[R], x[R];
+        vload((int64_t)w * 32 + p0, v);
+        vload((int64_t)w * 32 + p1, x);
+        const double s1 = two ? 1.0 : 0.0;
+        int p = 0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const double xs = s1 * x[i];
+#pragma unroll
+          for (int j = i; j < R; ++j) {
+            acc[p] = fma(xs, x[j], fma(v[i], v[j], acc[p]));
+            ++p;
+          }
+        }
+      }
+    }
     warp_reduce_halving<NV>(acc, lane);
     double A[NA], bv[R];
 #pragma unroll
-    for (int p = 0; p < NA; ++p) A[p] = warp_total<NV>(acc, p);
+    for (int p = 0; p < NA; ++p) {
+      const double t = warp_total<NV>(acc, p);
+      A[p] = hid ? Aall[p] - t : t;
+    }
 #pragma unroll
     for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, NA + i);
-    const int nj = (int)warp_total<NV>(acc, NA + R);
     return row_solve<R>(A, bv, nj, u);
   };
   // row 0: accumulation pass alone
@@ -634,20 +655,18 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     double acc[NV];
 #pragma unroll
     for (int p = 0; p < NV; ++p) acc[p] = 0.0;
-#pragma unroll 2
+#pragma unroll 4
     for (int w = 0; w < nfull; ++w) {
       const int64_t c = w * 32 + lane;
       double v[R];
       vload(c, v);
-      const bool k = (wd[w] >> lane) & 1u;
-      accum(acc, v, k ? y[c] : 0.0, k);
+      accum_b(acc, v, y[c], (wd[w] >> lane) & 1u);
     }
     if (tail) {
       const int64_t c = (int64_t)nfull * 32 + lane;
       double v[R];
       vload(c, v);
-      const bool k = (wd[nfull] >> lane) & 1u;
-      accum(acc, v, k ? y[c] : 0.0, k);
+      accum_b(acc, v, y[c], (wd[nfull] >> lane) & 1u);
     }
     flagged = finish(acc, wd, u);
   }
@@ -657,6 +676,10 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     const double* y = ybuf(b);
     const uint32_t* wd = reinterpret_cast<const uint32_t*>(y + npd);
     const bool has_next = k + 1 < nrows;
+    if (k + 2 < nrows) prefetch_l2(r0 + (k + 2) * nw);
+    double nu[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) nu[q] = -u[q];
     double ss = 0.0;
     double acc[NV];
 #pragma unroll
@@ -665,41 +688,35 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     const uint32_t* wn = reinterpret_cast<const uint32_t*>(yn + npd);
     if (has_next) {
       wait_buf(b ^ 1);
-      // residual of row k and accumulation of row k+1 share the V-hat reads
-#pragma unroll 2
+      // residual of row k and V_O^T y of row k+1 share the V-hat reads
+#pragma unroll 4
       for (int w = 0; w < nfull; ++w) {
         const int64_t c = w * 32 + lane;
         double v[R];
         vload(c, v);
-        const bool k0 = (wd[w] >> lane) & 1u;
-        const bool k1 = (wn[w] >> lane) & 1u;
-        resid(ss, v, u, k0 ? y[c] : 0.0, k0);
-        accum(acc, v, k1 ? yn[c] : 0.0, k1);
+        resid(ss, v, nu, y[c], (wd[w] >> lane) & 1u);
+        accum_b(acc, v, yn[c], (wn[w] >> lane) & 1u);
       }
       if (tail) {
         const int64_t c = (int64_t)nfull * 32 + lane;
         double v[R];
         vload(c, v);
-        const bool k0 = (wd[nfull] >> lane) & 1u;
-        const bool k1 = (wn[nfull] >> lane) & 1u;
-        resid(ss, v, u, k0 ? y[c] : 0.0, k0);
-        accum(acc, v, k1 ? yn[c] : 0.0, k1);
+        resid(ss, v, nu, y[c], (wd[nfull] >> lane) & 1u);
+        accum_b(acc, v, yn[c], (wn[nfull] >> lane) & 1u);
       }
     } else {
-#pragma unroll 2
+#pragma unroll 4
       for (int w = 0; w < nfull; ++w) {
         const int64_t c = w * 32 + lane;
         double v[R];
         vload(c, v);
-        const bool k0 = (wd[w] >> lane) & 1u;
-        resid(ss, v, u, k0 ? y[c] : 0.0, k0);
+        resid(ss, v, nu, y[c], (wd[w] >> lane) & 1u);
       }
       if (tail) {
         const int64_t c = (int64_t)nfull * 32 + lane;
         double v[R];
         vload(c, v);
-        const bool k0 = (wd[nfull] >> lane) & 1u;
-        resid(ss, v, u, k0 ? y[c] : 0.0, k0);
+        resid(ss, v, nu, y[c], (wd[nfull] >> lane) & 1u);
       }
     }
     ss = warp_sum(ss);

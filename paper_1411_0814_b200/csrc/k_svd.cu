@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
             v[u] = 0.0;
             if (cc[u] >= 0) v[u] = M2 ? vec[o * Lp + cc[u]] * inv : Vacc[cc[u] * KMAX + o];
           }
-          emit_slices4(a.Wq, a.Kpad, a.npad, tl * rex + i, j0, v[0], v[1], v[2], v[3]);
+          emit_slices4(a.S, a.Wq, a.Kpad, a.npad, tl * rex + i, j0, v[0], v[1], v[2], v[3]);
         }
       }
       __syncthreads();
@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
             }
 #pragma unroll
             for (int p = 0; p < R1; ++p)
-              emit_slices4(a.Wq, a.Kpad, a.npad, tl * rex + p, j0, v[0][p], v[1][p], v[2][p], v[3][p]);
+              emit_slices4(a.S, a.Wq, a.Kpad, a.npad, tl * rex + p, j0, v[0][p], v[1][p], v[2][p], v[3][p]);
           }
           __syncwarp();
           continue;
@@ -961,7 +961,7 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
           double v[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) v[u] = in[u] ? srow[p][cidx[u]] * scl[p] : 0.0;
-          emit_slices4(a.Wq, a.Kpad, a.npad, tl * rex + p, j0, v[0], v[1], v[2], v[3]);
+          emit_slices4(a.S, a.Wq, a.Kpad, a.npad, tl * rex + p, j0, v[0], v[1], v[2], v[3]);
         }
       }
       __syncwarp();

@@ -601,6 +601,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
       if (i8) {
         a.Wq = c->Wq.as<int8_t>();
         a.Kpad = Kpad;
+        a.S = S8;
         // rows past the chunk's trials * rex are zero (read by the last K-step)
         const int64_t used = (c1 - c0) * rex;
         if (Kpad > used)
@@ -650,6 +651,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
         g.accumulate = c0 > t_lo ? 1 : 0;
         const char* dg = getenv("RSM_I8_DIAG");
         g.diag = dg ? atoi(dg) : 0;
+        g.S = S8;
         ck(rsmk::launch_gram_i8(g, c->sms, c->stream), "gram (tcgen05) launch");
         ++c->launches;
       } else {

@@ -468,7 +468,8 @@ __device__ __forceinline__ int warp_jacobi_abs(double* A, int lda, double* V, in
 }
 
 // ---- stage 2 -> stage 3 hand-off: int8 digit slices (k_gram_i8.cu) ----
-// digits per value of the exact integer split of the harvested vectors
+// digits per value of the exact integer split of the harvested vectors:
+// kGramSlices by default, 5..7 selectable (gram_i8_slices, k_gram_i8.cu)
 constexpr int kGramSlices = 6;
 
 // Balanced signed digits: w = a[0] 2^-6 + sum_{1<=s<S} a[s] 2^(-6-8s) + e.
@@ -493,9 +494,9 @@ __device__ __forceinline__ unsigned long long digits_i8(double x) {
 // store per digit slice into W[s][krow][j0..j0+3] (S x Kpad x npad int8,
 // MN-major; a warp's lanes cover 128 consecutive bytes per store). The 4 x S
 // byte transpose is three byte permutes per slice.
-__device__ __forceinline__ void emit_slices4(int8_t* W, int64_t Kpad, int64_t npad, int64_t krow, int64_t j0,
-                                             double v0, double v1, double v2, double v3) {
-  constexpr int S = kGramSlices;
+template <int S>
+__device__ __forceinline__ void emit_slices4_t(int8_t* W, int64_t Kpad, int64_t npad, int64_t krow, int64_t j0,
+                                               double v0, double v1, double v2, double v3) {
   const unsigned long long z0 = digits_i8<S>(v0), z1 = digits_i8<S>(v1), z2 = digits_i8<S>(v2),
                            z3 = digits_i8<S>(v3);
 #pragma unroll
@@ -507,6 +508,13 @@ __device__ __forceinline__ void emit_slices4(int8_t* W, int64_t Kpad, int64_t np
     const unsigned t23 = __byte_perm((unsigned)(z2 >> sh), (unsigned)(z3 >> sh), p | ((4u + p) << 4));
     *reinterpret_cast<uint32_t*>(W + ((int64_t)s * Kpad + krow) * npad + j0) = __byte_perm(t01, t23, 0x5410);
   }
+}
+
+__device__ __forceinline__ void emit_slices4(int S, int8_t* W, int64_t Kpad, int64_t npad, int64_t krow,
+                                             int64_t j0, double v0, double v1, double v2, double v3) {
+  if (S == 5) emit_slices4_t<5>(W, Kpad, npad, krow, j0, v0, v1, v2, v3);
+  else if (S == 7) emit_slices4_t<7>(W, Kpad, npad, krow, j0, v0, v1, v2, v3);
+  else emit_slices4_t<6>(W, Kpad, npad, krow, j0, v0, v1, v2, v3);
 }
 
 }  // namespace rsmd

@@ -33,8 +33,9 @@ struct SvdArgs {
   int64_t cmw;
   int64_t npad;          // expanded column count (multiple of 128)
   double* Vout;          // local trials x (rp/2) planes x npad x 2 (see k_svd.cu), or null
-  int8_t* Wq;            // or: int8 digit slices [kGramSlices][Kpad][npad], rows t*rex + p (k_gram_i8.cu)
+  int8_t* Wq;            // or: int8 digit slices [S][Kpad][npad], rows t*rex + p (k_gram_i8.cu)
   int64_t Kpad;
+  int S;                 // digit slices (gram_i8_slices)
   int* colcnt;           // n per-column trial counts
   double* scratch;       // per-CTA vector scratch when shared memory is too small
   uint32_t* scratch_u32; // per-CTA 2*mwp words (column branch)
@@ -69,6 +70,7 @@ struct GramI8Args {
   double* P;         // nk x npad x npad partials (-W^T W per K-chunk)
   int accumulate;    // add to P (trial chunks after the first)
   int diag;          // RSM_I8_DIAG: 0 normal, 1 loads only, 2 MMAs only (timing experiments)
+  int S;             // digit slices (gram_i8_slices)
 };
 
 struct EigArgs {
