@@ -134,7 +134,7 @@ __device__ __forceinline__ bool row_solve(const double* A, const double* bv, int
         for (int k = 0; k < j; ++k) v = fma(-L[i * (i + 1) / 2 + k], L[j * (j + 1) / 2 + k], v);
         if (i == j) {
           if (!(v > 1e-10 * dmax)) slow = true;
-          Li[i] = rsqrt(fmax(v, 1e-300));
+          Li[i] = rsqrt_fast(fmax(v, 1e-300));
           L[q] = v * Li[i];
         } else {
           L[q] = v * Li[j];
@@ -471,26 +471,29 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
 //
 // Per column the loop does only what every cell needs: V_O^T y (R FMAs on the
 // selected value) for row k+1 and the direct residual (R FMAs from y, one
-// select, one FMA) for row k. The normal matrix V_O^T V_O is formed from the
-// MINORITY cells of the row: when at least half the row is observed, as
-// V^T V (once per CTA, fixed order) minus the hidden cells' outer products,
-// otherwise directly from the observed cells; each lane walks the set bits of
-// its own mask words. At config 3 (rho = 0.8) that is ~0.2 n outer products per
-// row instead of n.
+// select, one FMA) for row k. The normal matrix V_O^T V_O is formed word by
+// word from each 32-column mask word's MINORITY cells: a word with at least 16
+// observed cells contributes V_w^T V_w (its 32 columns' Gram, tabulated once
+// per CTA in a fixed order) minus its hidden cells' outer products, any other
+// word its observed cells' outer products; each lane walks the bits of its own
+// words, so at most 16 outer products per word and ~0.2 n per row at config 3
+// (rho = 0.8) instead of n. The observed count and row k's residual ride in
+// the same warp reduction as row k+1's normal equations.
 template <int R>
 __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   constexpr int NP = (R + 1) / 2;
   constexpr int NA = R * (R + 1) / 2;
-  constexpr int NV = pow2_at_least(NA + R);
+  constexpr int NV = pow2_at_least(NA + R + 2);  // A, b, count, previous row's residual
   extern __shared__ __align__(16) double sm[];
-  __shared__ double Aall[NA];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int64_t npd = (n + 1) & ~int64_t(1);
   const int nwarps = blockDim.x >> 5;
+  const int nwn = (int)((n + 31) >> 5);  // mask words holding columns
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm);  // [SU_MAXW][2]
   double2* Vp = reinterpret_cast<double2*>(sm + 2 * SU_MAXW);
-  double* wb = sm + 2 * SU_MAXW + 2 * NP * n;
+  double* Vw = sm + 2 * SU_MAXW + 2 * NP * n;  // nwn x NA per-word Grams
+  double* wb = Vw + (((int64_t)nwn * NA + 1) & ~int64_t(1));
   const int64_t bufd = npd + a.nwp / 2;
   auto ybuf = [&](int b) { return wb + (2 * warp + b) * bufd; };
   if (threadIdx.x < 2 * nwarps)
@@ -502,13 +505,13 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     const double x1 = (2 * p + 1 < R) ? a.V[c * R + 2 * p + 1] : 0.0;
     Vp[e] = make_double2(x0, x1);
   }
-  if (warp == 0) {
-    // V^T V (packed upper): lane l sums columns l, l+32, ..., then a fixed
-    // butterfly -- the same order in every CTA and launch shape
+  // per-word Gram V_w^T V_w (packed upper): one thread sums a word's columns
+  // in column order -- the same bits in every CTA and launch shape
+  for (int w = threadIdx.x; w < nwn; w += blockDim.x) {
     double part[NA];
 #pragma unroll
     for (int p = 0; p < NA; ++p) part[p] = 0.0;
-    for (int64_t c = lane; c < n; c += 32) {
+    for (int64_t c = (int64_t)w * 32; c < n && c < (int64_t)w * 32 + 32; ++c) {
       double v[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) v[k] = a.V[c * R + k];
@@ -522,10 +525,7 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
         }
     }
 #pragma unroll
-    for (int p = 0; p < NA; ++p) {
-      const double t = warp_sum(part[p]);
-      if (lane == 0) Aall[p] = t;
-    }
+    for (int p = 0; p < NA; ++p) Vw[(int64_t)w * NA + p] = part[p];
   }
   __syncthreads();
   auto vload = [&](int64_t c, double* v) {
@@ -582,7 +582,6 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   if (r0 >= a.row_hi) return;
   const int64_t nrows = (a.row_hi - r0 + nw - 1) / nw;  // this warp's rows: r0 + k nw
   const int nfull = (int)(n >> 5);
-  const int nwn = (int)((n + 31) >> 5);  // mask words holding columns
   const bool tail = (int64_t)nfull * 32 + lane < n;
   issue(r0, 0);
   if (nrows > 1) issue(r0 + nw, 1);
@@ -600,16 +599,24 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     d = k ? d : 0.0;
     ss = fma(d, d, ss);
   };
-  // normal matrix from the row's minority cells, then reduce and solve
-  auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u) -> bool {
+  // normal matrix from each word's minority cells, then one reduction of the
+  // normal equations, the observed count and the previous row's residual
+  // (ss_prev, returned summed), and the solve
+  auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u, double& ss_prev) -> bool {
     int cnt = 0;
-    for (int w = lane; w < nwn; w += 32) cnt += __popc(wd[w]);
-    const int nj = warp_sum_int(cnt);  // mask words are zero beyond n
-    const bool hid = 2 * (int64_t)nj >= n;
     for (int w = lane; w < nwn; w += 32) {
       const int rem = (int)(n - (int64_t)w * 32);
       const unsigned valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
-      unsigned bits = hid ? (~wd[w] & valid) : wd[w];
+      const unsigned obs = wd[w] & valid;
+      const int no = __popc(obs);
+      cnt += no;
+      const bool hid = 2 * no >= __popc(valid);
+      const double sg = hid ? -1.0 : 1.0;
+      unsigned bits = hid ? (~obs & valid) : obs;
+      if (hid) {
+#pragma unroll
+        for (int p = 0; p < NA; ++p) acc[p] += Vw[(int64_t)w * NA + p];
+      }
       // two cells per iteration (independent loads and FMA chains); a lone
       // last cell pairs with itself at weight 0
       while (bits) {
@@ -621,28 +628,29 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
         double v[R], x[R];
         vload((int64_t)w * 32 + p0, v);
         vload((int64_t)w * 32 + p1, x);
-        const double s1 = two ? 1.0 : 0.0;
+        const double s1 = two ? sg : 0.0;
         int p = 0;
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-          const double xs = s1 * x[i];
+          const double vs = sg * v[i], xs = s1 * x[i];
 #pragma unroll
           for (int j = i; j < R; ++j) {
-            acc[p] = fma(xs, x[j], fma(v[i], v[j], acc[p]));
+            acc[p] = fma(xs, x[j], fma(vs, v[j], acc[p]));
             ++p;
           }
         }
       }
     }
+    acc[NA + R] = (double)cnt;
+    acc[NA + R + 1] = ss_prev;
     warp_reduce_halving<NV>(acc, lane);
     double A[NA], bv[R];
 #pragma unroll
-    for (int p = 0; p < NA; ++p) {
-      const double t = warp_total<NV>(acc, p);
-      A[p] = hid ? Aall[p] - t : t;
-    }
+    for (int p = 0; p < NA; ++p) A[p] = warp_total<NV>(acc, p);
 #pragma unroll
     for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, NA + i);
+    const int nj = (int)warp_total<NV>(acc, NA + R);
+    ss_prev = warp_total<NV>(acc, NA + R + 1);
     return row_solve<R>(A, bv, nj, u);
   };
   // row 0: accumulation pass alone
@@ -668,7 +676,8 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
       vload(c, v);
       accum_b(acc, v, y[c], (wd[nfull] >> lane) & 1u);
     }
-    flagged = finish(acc, wd, u);
+    double none = 0.0;
+    flagged = finish(acc, wd, u, none);
   }
   for (int64_t k = 0; k < nrows; ++k) {
     const int64_t row = r0 + k * nw;
@@ -719,7 +728,6 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
         resid(ss, v, nu, y[c], (wd[nfull] >> lane) & 1u);
       }
     }
-    ss = warp_sum(ss);
     if (lane < R) {
       double uk = 0.0;
 #pragma unroll
@@ -727,13 +735,12 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
         if (q == lane) uk = u[q];
       a.U[row * R + lane] = uk;
     }
-    if (lane == 0) {
-      a.rowres[row] = ss;
-      if (flagged) atomicAdd(a.flagged, 1);
-    }
+    if (lane == 0 && flagged) atomicAdd(a.flagged, 1);
     __syncwarp();  // row k's buffer is free: refill it with row k+2
     if (k + 2 < nrows) issue(r0 + (k + 2) * nw, b);
-    if (has_next) flagged = finish(acc, wn, u);
+    if (has_next) flagged = finish(acc, wn, u, ss);  // ss: row k's residual, summed
+    else ss = warp_sum(ss);
+    if (lane == 0) a.rowres[row] = ss;
   }
 }
 
@@ -816,11 +823,13 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
   if (head + vbytes + 8 * per_warp <= cap) {
     // V-hat and >= 8 warps of staged rows
     if constexpr (R <= 4) {
-      if (bulk && !fused_off) {
-        const size_t capw = 227 * 1024 - 2048;
-        int w = (int)std::min<size_t>(SU_MAXW, (capw - head - vbytes) / per_warp);
+      constexpr int NA = R * (R + 1) / 2;
+      const size_t wgram = sizeof(double) * (((size_t)((a.n + 31) / 32) * NA + 1) & ~(size_t)1);
+      if (bulk && !fused_off && head + vbytes + wgram + 8 * per_warp <= cap) {
+        const size_t capw = 227 * 1024 - 1024;  // the kernel has no static shared memory
+        int w = (int)std::min<size_t>(SU_MAXW, (capw - head - vbytes - wgram) / per_warp);
         if (w < 1) w = 1;
-        const size_t smem = head + vbytes + (size_t)w * per_warp;
+        const size_t smem = head + vbytes + wgram + (size_t)w * per_warp;
         cudaFuncSetAttribute(k_solve_u_fused<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t rows = a.row_hi - a.row_lo;
         int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);

@@ -49,6 +49,20 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// 1/sqrt(v) to ~1 ulp: single-precision seed and two Newton steps (relative
+// error 2^-22 -> 2^-43 -> rounding) when v is inside float range, else the
+// library rsqrt (a long software sequence)
+__device__ __forceinline__ double rsqrt_fast(double v) {
+  if (v > 1e-30 && v < 1e30) {
+    double r = (double)rsqrtf((float)v);
+    const double hv = 0.5 * v;
+    r = r * fma(-hv * r, r, 1.5);
+    r = r * fma(-hv * r, r, 1.5);
+    return r;
+  }
+  return rsqrt(v);
+}
+
 __device__ __forceinline__ int warp_sum_int(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
