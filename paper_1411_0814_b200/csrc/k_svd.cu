@@ -553,7 +553,7 @@ __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C) {
   if (!(tr > 0.0)) return false;
   // Cholesky of G (packed lower) with a floor on the pivots (G may be
   // singular: the floor only regularises the inverse iteration)
-  double L[P];
+  double L[P], Li[K];  // Li: reciprocal pivots (the solves multiply)
   auto li = [](int i, int j) { return i * (i + 1) / 2 + j; };
 #pragma unroll
   for (int j = 0; j < K; ++j) {
@@ -561,13 +561,14 @@ __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C) {
 #pragma unroll
     for (int k = 0; k < j; ++k) d -= L[li(j, k)] * L[li(j, k)];
     d = fmax(d, 1e-30 * tr);
-    L[li(j, j)] = sqrt(d);
+    Li[j] = rsqrt_fast(d);
+    L[li(j, j)] = d * Li[j];
 #pragma unroll
     for (int i = j + 1; i < K; ++i) {
       double v = gat(i, j);
 #pragma unroll
       for (int k = 0; k < j; ++k) v -= L[li(i, k)] * L[li(j, k)];
-      L[li(i, j)] = v / L[li(j, j)];
+      L[li(i, j)] = v * Li[j];
     }
   }
   double x[K];
@@ -581,19 +582,19 @@ __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C) {
       double v = x[i];
 #pragma unroll
       for (int k = 0; k < i; ++k) v -= L[li(i, k)] * z[k];
-      z[i] = v / L[li(i, i)];
+      z[i] = v * Li[i];
     }
 #pragma unroll
     for (int i = K - 1; i >= 0; --i) {
       double v = z[i];
 #pragma unroll
       for (int k = i + 1; k < K; ++k) v -= L[li(k, i)] * z[k];
-      z[i] = v / L[li(i, i)];
+      z[i] = v * Li[i];
     }
     double nz = 0.0, dot = 0.0;
 #pragma unroll
     for (int i = 0; i < K; ++i) nz += z[i] * z[i];
-    nz = rsqrt(nz);
+    nz = rsqrt_fast(nz);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       z[i] *= nz;
@@ -642,13 +643,14 @@ __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C) {
 #pragma unroll
     for (int k = 0; k < j; ++k) d -= L[li(j, k)] * L[li(j, k)];
     if (!(d > 1e-8 * dmax)) return false;
-    L[li(j, j)] = sqrt(d);
+    Li[j] = rsqrt_fast(d);
+    L[li(j, j)] = d * Li[j];
 #pragma unroll
     for (int i = j + 1; i < R; ++i) {
       double t = gat(i, j) - beta * (v[i] * w[j] + w[i] * v[j]) + beta * beta * gam * v[i] * v[j];
 #pragma unroll
       for (int k = 0; k < j; ++k) t -= L[li(i, k)] * L[li(j, k)];
-      L[li(i, j)] = t / L[li(j, j)];
+      L[li(i, j)] = t * Li[j];
     }
   }
   // C = Q L^{-T}: row i of C solves L c = q_i, q_ij = delta_ij - beta v_i v_j
@@ -660,7 +662,7 @@ __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C) {
       double t = (i == j ? 1.0 : 0.0) - beta * v[i] * v[j];
 #pragma unroll
       for (int k = 0; k < j; ++k) t -= L[li(j, k)] * c[k];
-      c[j] = t / L[li(j, j)];
+      c[j] = t * Li[j];
     }
 #pragma unroll
     for (int j = 0; j < R; ++j) C[i * R + j] = c[j];
@@ -690,6 +692,16 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
   for (int64_t t = a.t_lo + (int64_t)blockIdx.x * SVDW_WARPS + warp; t < a.t_hi; t += nwarps) {
     const int64_t tl = t - a.t_lo;
     const int myidx = lane < K ? a.t_idx[t * K + lane] : 0;
+    // pull this warp's next trial's K rows (values and mask words) into L2
+    // while this one is gathered and solved
+    if (lane < K && t + nwarps < a.t_hi && (a.n & 1) == 0) {
+      const int64_t nr = a.t_idx[(t + nwarps) * K + lane];
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.Y + nr * a.n), "r"((unsigned)(a.n * 8))
+                   : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.bitsR + nr * a.nwp),
+                   "r"((unsigned)(a.nwp * 4))
+                   : "memory");
+    }
     int rows[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) rows[i] = __shfl_sync(0xffffffffu, myidx, i);
