@@ -692,16 +692,6 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
   for (int64_t t = a.t_lo + (int64_t)blockIdx.x * SVDW_WARPS + warp; t < a.t_hi; t += nwarps) {
     const int64_t tl = t - a.t_lo;
     const int myidx = lane < K ? a.t_idx[t * K + lane] : 0;
-    // pull this warp's next trial's K rows (values and mask words) into L2
-    // while this one is gathered and solved
-    if (lane < K && t + nwarps < a.t_hi && (a.n & 1) == 0) {
-      const int64_t nr = a.t_idx[(t + nwarps) * K + lane];
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.Y + nr * a.n), "r"((unsigned)(a.n * 8))
-                   : "memory");
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.bitsR + nr * a.nwp),
-                   "r"((unsigned)(a.nwp * 4))
-                   : "memory");
-    }
     int rows[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) rows[i] = __shfl_sync(0xffffffffu, myidx, i);
@@ -732,33 +722,27 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     }
     const int L = run;
     __syncwarp();
-    // gather S (K x L): lane = column within each 32-column word. The K rows
-    // are read whole and unconditionally, UW words at a time, so K*UW loads
-    // per lane are in flight (hidden cells are loaded but never used)
-    constexpr int UW = 4;
-    for (int64_t j0 = 0; j0 < a.n; j0 += 32 * UW) {
-      double yv[UW][K];
+    // gather S (K x L): lane = column within each 32-column word. Every
+    // support cell is copied global -> shared by an asynchronous 8-byte copy
+    // (cp.async), so all of a trial's K x L loads are in flight at once and
+    // the warp waits for them once (one memory round trip per trial)
+    for (int64_t j0 = 0; j0 < a.n; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const uint32_t word = cm[j0 >> 5];
+      const uint32_t bit = 1u << lane;
+      if (j < a.n && (word & bit)) {
+        const int c = (int)pre[j0 >> 5] + __popc(word & (bit - 1u));
 #pragma unroll
-      for (int u = 0; u < UW; ++u) {
-        const int64_t j = j0 + 32 * u + lane;
-#pragma unroll
-        for (int i = 0; i < K; ++i) yv[u][i] = j < a.n ? __ldg(a.Y + (int64_t)rows[i] * a.n + j) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < UW; ++u) {
-        const int64_t j = j0 + 32 * u + lane;
-        if (j0 + 32 * u < a.n) {
-          const uint32_t word = cm[(j0 >> 5) + u];
-          const uint32_t bit = 1u << lane;
-          if (j < a.n && (word & bit)) {
-            const int c = (int)pre[(j0 >> 5) + u] + __popc(word & (bit - 1u));
-#pragma unroll
-            for (int i = 0; i < K; ++i) S[i * Lp + c] = yv[u][i];
-            atomicAdd(a.colcnt + j, 1);
-          }
+        for (int i = 0; i < K; ++i) {
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(S + i * Lp + c);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(a.Y + (int64_t)rows[i] * a.n + j)
+                       : "memory");
         }
+        atomicAdd(a.colcnt + j, 1);
       }
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncwarp();
     // one-sided Jacobi, Gram-accelerated. The Gram of the rotated vectors is
     // accumulated in the rotation pass itself (one read of S per iteration).
