@@ -271,8 +271,9 @@ __device__ __noinline__ void chol_small(int nc, EigShared& sh) {
       if (k < nc) {
         const double d = __shfl_sync(0xffffffffu, a[k], k);
         if (!(d > 0.0)) ok = false;
-        const double l = sqrt(fmax(d, 0.0));
-        const double inv = l > 0.0 ? 1.0 / l : 0.0;
+        // one reciprocal square root per pivot on the dependent chain
+        const double inv = d > 0.0 ? rsqrt_fast(d) : 0.0;
+        const double l = d > 0.0 ? d * inv : 0.0;
         if (lane == k) a[k] = l;
         if (lane > k) a[k] *= inv;
         // trailing update: a[j] -= L(lane,k) L(j,k) for k < j <= lane
@@ -451,10 +452,8 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     Xo[e] = v;
   }
   __syncthreads();
-  if (!full) {
-    cholqr(a, grid, X, Xo, b, ld, pcol, row_lo, nr, buf, pw, sh);
-    cholqr(a, grid, X, Xo, b, ld, -1, row_lo, nr, buf, pw, sh);
-  }
+  // the random start block is well conditioned: one CholQR orthonormalises it
+  if (!full) cholqr(a, grid, X, Xo, b, ld, pcol, row_lo, nr, buf, pw, sh);
 
   double acut = 0.5 * ub;
   double maxres = 0.0, lmax = 0.0;

@@ -66,6 +66,36 @@ __global__ void __launch_bounds__(256) k_select(const uint32_t* __restrict__ bit
     for (int t = 0; t < block; ++t) idx_out[a * block + t] = out[t];
   }
   __syncwarp();
+  if (nwords <= 64 && (stride & 3) == 0 && apw == 32) {
+    // short scans (row branch, n <= 2048): each lane ANDs its own attempt's
+    // rows with 16-byte loads, all of them in flight at once (the words past
+    // n up to the stride are zero padding)
+    if (lane < apw && a < count) {
+      const int32_t* rows = my + lane * block;
+      uint4 acc[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc[u] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      for (int t = 0; t < block; ++t) {
+        const uint4* rb = reinterpret_cast<const uint4*>(bits + (int64_t)rows[t] * stride);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          if (4 * u < nwords) {
+            const uint4 x = __ldg(rb + u);
+            acc[u].x &= x.x;
+            acc[u].y &= x.y;
+            acc[u].z &= x.z;
+            acc[u].w &= x.w;
+          }
+        }
+      }
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (4 * u < nwords) cnt += __popc(acc[u].x) + __popc(acc[u].y) + __popc(acc[u].z) + __popc(acc[u].w);
+      q_out[a] = cnt;
+    }
+    return;
+  }
   for (int i = 0; i < apw; ++i) {
     const int64_t ai = base + i;
     if (ai >= count) break;

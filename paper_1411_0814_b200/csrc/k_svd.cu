@@ -726,19 +726,23 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     // support cell is copied global -> shared by an asynchronous 8-byte copy
     // (cp.async), so all of a trial's K x L loads are in flight at once and
     // the warp waits for them once (one memory round trip per trial)
-    for (int64_t j0 = 0; j0 < a.n; j0 += 32) {
-      const int64_t j = j0 + lane;
-      const uint32_t word = cm[j0 >> 5];
-      const uint32_t bit = 1u << lane;
-      if (j < a.n && (word & bit)) {
-        const int c = (int)pre[j0 >> 5] + __popc(word & (bit - 1u));
+    {
+      const unsigned sb = (unsigned)__cvta_generic_to_shared(S) + 8u * (unsigned)lane;  // + 8 c per cell
+      const double* yrow[K];
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          const unsigned dst = (unsigned)__cvta_generic_to_shared(S + i * Lp + c);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(a.Y + (int64_t)rows[i] * a.n + j)
-                       : "memory");
+      for (int i = 0; i < K; ++i) yrow[i] = a.Y + (int64_t)rows[i] * a.n + lane;
+      const uint32_t below = (1u << lane) - 1u;
+      for (int w = 0; 32 * (int64_t)w < a.n; ++w) {
+        const uint32_t word = cm[w];
+        if ((word >> lane) & 1u) {  // support bits exist only for j < n
+          const unsigned dst = sb + 8u * (unsigned)((int)pre[w] + __popc(word & below) - lane);
+#pragma unroll
+          for (int i = 0; i < K; ++i)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * (unsigned)(i * Lp)),
+                         "l"(yrow[i] + 32 * (int64_t)w)
+                         : "memory");
+          atomicAdd(a.colcnt + 32 * (int64_t)w + lane, 1);
         }
-        atomicAdd(a.colcnt + j, 1);
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");

@@ -400,9 +400,9 @@ __device__ __noinline__ int warp_jacobi_reg(double* A, int lda, double* V, int l
         // no division on the step's critical path
         const double dd = aqq - app, ee = 2.0 * off;
         const double r2 = fma(dd, dd, ee * ee);
-        const double rr = r2 * rsqrt(r2);
+        const double rr = r2 * rsqrt_fast(r2);
         const double w = rr + fabs(dd);
-        const double g = rsqrt(2.0 * rr * w);
+        const double g = rsqrt_fast(2.0 * rr * w);
         c = w * g;
         sn = (dd >= 0.0 ? ee : -ee) * g;
       }

@@ -20,3 +20,11 @@ for i in range(int(os.environ.get("REPS", "2"))):
     t0 = time.time()
     _, rep = ctx.decompose(cfg, fetch=False)
     print(i, f"{(time.time() - t0) * 1e3:.2f} ms", ctx.stage_ms(), ctx.solver_stats(), rep.e, flush=True)
+if int(os.environ.get("REPS", "2")) >= 4:
+    import numpy as np
+    st = []
+    for i in range(int(os.environ.get("REPS", "2"))):
+        ctx.decompose(cfg, fetch=False)
+        st.append(ctx.stage_ms())
+    med = np.median(np.array(st), axis=0)
+    print("median", " ".join(f"{x:.4f}" for x in med), "(select svd gram reduce solve_v solve_u total)", flush=True)
