@@ -9,6 +9,11 @@
 #include <exception>
 #include <vector>
 
+#include <string>
+
+#ifdef REF_HAVE_IO
+#include "rsm/io.hpp"
+#endif
 #include "rsm/sampler.hpp"
 #include "rsm/solver.hpp"
 #include "rsm/synth.hpp"
@@ -199,5 +204,74 @@ double ref_masked_residual_norm(const double* Y, const uint8_t* mask, int64_t m,
   std::memcpy(F.v.data(), V, sizeof(double) * n * r);
   return masked_residual_norm(M, F);
 }
+
+#ifdef REF_HAVE_IO
+// io.cpp (src/io.cpp:56-254): loader, saver, checksum and run report, as the
+// reference compiles them. Strings come back in a caller buffer (length
+// returned; -1 when it does not fit).
+int ref_have_io() { return 1; }
+
+int ref_load_matrix(const char* path, int64_t* m, int64_t* n, double* Y, uint8_t* mask, int64_t cap) {
+  return guard([&] {
+    MaskedMatrix M = load_matrix(path);
+    *m = M.m;
+    *n = M.n;
+    if (Y && mask && M.m * M.n <= cap) {
+      std::memcpy(Y, M.values.data(), sizeof(double) * M.m * M.n);
+      std::memcpy(mask, M.mask.data(), (size_t)(M.m * M.n));
+    }
+  });
+}
+
+int ref_save_matrix(const char* path, const double* Y, const uint8_t* mask, int64_t m, int64_t n) {
+  return guard([&] { save_matrix(make(Y, mask, m, n), path); });
+}
+
+int ref_dataset_checksum(const double* Y, const uint8_t* mask, int64_t m, int64_t n, uint64_t* out) {
+  return guard([&] { *out = dataset_checksum(make(Y, mask, m, n)); });
+}
+
+// make_report + serialize_report for a decompose config and result
+int ref_serialize_report(int64_t rank, int mode, int64_t block, int64_t vectors_per_trial, uint64_t trials,
+                         double epsilon, uint64_t seed, double tol, int workers, double e, uint64_t attempted,
+                         uint64_t accepted, uint64_t z, int64_t underdetermined, int64_t gram_rank, int borderline,
+                         double wall, uint64_t checksum, char* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    RsmConfig cfg;
+    cfg.rank = rank;
+    cfg.mode = mode == 0 ? Mode::M1 : Mode::M2;
+    cfg.block = block;
+    cfg.vectors_per_trial = vectors_per_trial;
+    cfg.plan.trials = trials;
+    cfg.plan.epsilon = epsilon;
+    cfg.seed = seed;
+    cfg.gram_rank_tol = tol;
+    cfg.workers = workers;
+    DecompositionReport rep;
+    rep.e = e;
+    rep.trials_attempted = attempted;
+    rep.trials_accepted = accepted;
+    rep.z = z;
+    rep.underdetermined_rows = underdetermined;
+    rep.gram_rank = gram_rank;
+    rep.borderline_rank_gate = borderline != 0;
+    rep.wall_time = wall;
+    const std::string s = serialize_report(make_report(cfg, rep, checksum));
+    *len = (int64_t)s.size();
+    if ((int64_t)s.size() < cap) std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+
+// parse_report -> serialize_report (the reference's own round trip)
+int ref_reserialize_report(const char* text, char* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    const std::string s = serialize_report(parse_report(text));
+    *len = (int64_t)s.size();
+    if ((int64_t)s.size() < cap) std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+#else
+int ref_have_io() { return 0; }
+#endif
 
 }  // extern "C"

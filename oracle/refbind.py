@@ -33,6 +33,14 @@ def lib():
         L.ref_als.argtypes = [P, P, i64, i64, i64, i64, u64, C.c_int, P, P, C.POINTER(i64), C.POINTER(d)]
         L.ref_masked_residual_norm.restype = d
         L.ref_masked_residual_norm.argtypes = [P, P, i64, i64, P, P, i64]
+        L.ref_have_io.restype = C.c_int
+        if L.ref_have_io():
+            L.ref_load_matrix.argtypes = [C.c_char_p, C.POINTER(i64), C.POINTER(i64), P, P, i64]
+            L.ref_save_matrix.argtypes = [C.c_char_p, P, P, i64, i64]
+            L.ref_dataset_checksum.argtypes = [P, P, i64, i64, C.POINTER(u64)]
+            L.ref_serialize_report.argtypes = [i64, C.c_int, i64, i64, u64, d, u64, d, C.c_int, d, u64, u64, u64,
+                                               i64, i64, C.c_int, d, u64, C.c_char_p, i64, C.POINTER(i64)]
+            L.ref_reserialize_report.argtypes = [C.c_char_p, C.c_char_p, i64, C.POINTER(i64)]
         _lib = L
     return _lib
 
@@ -133,3 +141,51 @@ def decompose(Y, W, rank, trials, mode=0, block=0, vectors_per_trial=0, seed=0, 
     rep = dict(e=e.value, trials_attempted=int(u64[0]), trials_accepted=int(u64[1]), z=int(u64[2]),
                underdetermined_rows=int(i64[0]), gram_rank=int(i64[1]), borderline=bool(i64[2]), wall_time=wall.value)
     return U, V, rep
+
+
+# ---- io.cpp (src/io.cpp:56-254), when build_ref.sh found the JSON header ----
+
+def have_io():
+    return available() and bool(lib().ref_have_io())
+
+
+def load_matrix(path):
+    """rsm::load_matrix -> (Y, W); raises RefError with the reference's exit code."""
+    m, n = C.c_int64(), C.c_int64()
+    _chk(lib().ref_load_matrix(os.fsencode(path), C.byref(m), C.byref(n), None, None, 0))
+    Y = np.zeros((m.value, n.value))
+    W = np.zeros((m.value, n.value), np.uint8)
+    _chk(lib().ref_load_matrix(os.fsencode(path), C.byref(m), C.byref(n), _p(Y), _p(W), Y.size))
+    return Y, W
+
+
+def save_matrix(Y, W, path):
+    Y = np.ascontiguousarray(Y, dtype=np.float64)
+    W = np.ascontiguousarray(W, dtype=np.uint8)
+    _chk(lib().ref_save_matrix(os.fsencode(path), _p(Y), _p(W), Y.shape[0], Y.shape[1]))
+
+
+def dataset_checksum(Y, W):
+    Y = np.ascontiguousarray(Y, dtype=np.float64)
+    W = np.ascontiguousarray(W, dtype=np.uint8)
+    out = C.c_uint64()
+    _chk(lib().ref_dataset_checksum(_p(Y), _p(W), Y.shape[0], Y.shape[1], C.byref(out)))
+    return int(out.value)
+
+
+def serialize_report(rank, mode, block, vectors_per_trial, trials, epsilon, seed, tol, workers, e, attempted,
+                     accepted, z, underdetermined, gram_rank, borderline, wall, checksum):
+    """make_report + serialize_report (mode: 0 = m1, 1 = m2)."""
+    buf = C.create_string_buffer(1 << 16)
+    ln = C.c_int64()
+    _chk(lib().ref_serialize_report(rank, mode, block, vectors_per_trial, trials, epsilon, seed, tol, workers, e,
+                                    attempted, accepted, z, underdetermined, gram_rank, int(borderline), wall,
+                                    checksum, buf, len(buf), C.byref(ln)))
+    return buf.value.decode()
+
+
+def reserialize_report(text):
+    buf = C.create_string_buffer(1 << 16)
+    ln = C.c_int64()
+    _chk(lib().ref_reserialize_report(text.encode(), buf, len(buf), C.byref(ln)))
+    return buf.value.decode()
