@@ -143,13 +143,19 @@ def algorithmic(c, qs, nwp_bytes, attempts):
 
 # ------------------------------------------------------------------ CPU arm
 
-def cpu_reference_sample(Y, W, c, G=None, trials_prefix=64, rows_sample=16384):
-    """Time the reference CPU path (oracle/_ref) on a bounded sample and
-    extrapolate a full decomposition: harvest_gram on a prefix of accepted
-    trials (per-trial work is i.i.d.), dsyev on the full n x n accumulator,
-    solve_u + residual on a row slice."""
+def cpu_reference_sample(Y, W, c, G=None, V=None, trials_prefix=64, rows_sample=16384):
+    """Time the reference CPU path (oracle/_ref: the reference's own sources,
+    all host threads) on a bounded sample of the workload and extrapolate one
+    full decomposition:
+      harvest_gram on the first `trials_prefix` accepted trials (per-trial work
+        is i.i.d., so the full harvest is that time x T / accepted);
+      solve_v (LAPACKE dsyev + rank gate) on G -- the full accumulator when the
+        caller has it, else the reference's own prefix accumulator (same n x n
+        dsyev; its rank gate may fail on a prefix, after dsyev has run);
+      solve_u + the e pass on `rows_sample` rows against V (the decomposition's
+        V-hat, else the planted basis it converges to), x m / rows.
+    Every factor is returned as a field."""
     from oracle import refbind as R
-    kind = "reference"
     if not R.available():
         return None
     threads = os.cpu_count() or 1
@@ -160,23 +166,46 @@ def cpu_reference_sample(Y, W, c, G=None, trials_prefix=64, rows_sample=16384):
         pass
     p = P()
     p.mode, p.block, p.rank, p.min_count, p.seed, p.ell = 1, c["k"], r, r + 1, c["seed"], 0
-    _, att, acc, _, t_h = R.harvest(Y, W, p, trials_prefix, workers=threads, timed=True)
-    if G is None:
-        # dsyev cost is data-independent to first order: time it on a symmetric
-        # positive definite matrix of the same size when the accumulator is absent
-        A = np.random.default_rng(1).standard_normal((n, n))
-        G = A @ A.T + n * np.eye(n)
-    _, _, _, t_v = R.solve_v(G, r, 1e-9, timed=True)
+    Gp, att, acc, _, t_h = R.harvest(Y, W, p, trials_prefix, workers=threads, timed=True)
+    g_src = "full accumulator (device harvest)" if G is not None else f"reference prefix accumulator ({acc} trials)"
+    Vv, gr, _, t_v = R.solve_v(G if G is not None else Gp, r, 1e-9, timed=True, gate_failure_ok=True)
+    if V is None:
+        V = Vv
+    v_src = "V-hat of the decomposition"
+    if V is None:
+        _, _, B = R.generate(min(m, 2 * n), n, r, c["rho"], c["sigma"], c["seed"], with_basis=True)
+        V = np.linalg.qr(B)[0]
+        v_src = "planted basis (orthonormalised)"
     rs = min(rows_sample, m)
     Ys, Ws = np.ascontiguousarray(Y[:rs]), np.ascontiguousarray(W[:rs])
-    V = np.linalg.qr(np.random.default_rng(0).standard_normal((n, r)))[0]
-    _, _, t_u = R.solve_u(Ys, Ws, V, r, workers=threads, timed=True)
-    est = t_h * c["T"] / max(acc, 1) + t_v + t_u * m / rs
-    sample = (f"harvest_gram on the first {acc} accepted trials ({t_h:.2f}s, x{c['T'] / max(acc, 1):.0f}), "
-              f"solve_v dsyev(n={n}) on the full accumulator ({t_v:.2f}s), solve_u+residual on {rs} rows "
-              f"({t_u:.2f}s, x{m / rs:.0f}); extrapolated full decompose {est:.1f}s")
-    return dict(value=c["T"] / est, unit="submatrices/s", cores=threads, kind=kind, sample=sample,
-                est_decompose_s=est)
+    _, _, t_u = R.solve_u(Ys, Ws, np.ascontiguousarray(V), r, workers=threads, timed=True)
+    f_h, f_u = c["T"] / max(acc, 1), m / rs
+    est = t_h * f_h + t_v + t_u * f_u
+    sample = (f"harvest_gram on the first {acc} accepted trials ({t_h:.2f}s, x{f_h:.0f}), solve_v dsyev(n={n}) on "
+              f"the {g_src} ({t_v:.2f}s), solve_u+residual on {rs} rows against the {v_src} ({t_u:.2f}s, "
+              f"x{f_u:.0f}); extrapolated full decompose {est:.1f}s")
+    return dict(value=c["T"] / est, unit="submatrices/s", cores=threads, kind="reference", sample=sample,
+                est_decompose_s=est,
+                extrapolation={"harvest_s": t_h, "harvest_trials": acc, "harvest_factor": f_h, "solve_v_s": t_v,
+                               "solve_v_input": g_src, "solve_u_s": t_u, "solve_u_rows": rs, "solve_u_factor": f_u,
+                               "solve_u_basis": v_src})
+
+
+def cpu_reference_config1(threads=None):
+    """A fully measured (not extrapolated) reference decomposition of BASELINE
+    config 1 (2000 x 200, r = 3, k = 4, 2000 submatrices): the reference's own
+    rsm::decompose on its own generator's instance."""
+    from oracle import refbind as R
+    if not R.available():
+        return None
+    c = CONFIGS["config1"]
+    threads = threads or os.cpu_count() or 1
+    Y, W = R.generate(c["m"], c["n"], c["r"], c["rho"], c["sigma"], c["seed"])
+    t0 = time.perf_counter()
+    out = R.decompose(Y, W, c["r"], c["T"], mode=1, block=c["k"], seed=c["seed"], workers=threads)
+    wall = time.perf_counter() - t0
+    return {"workload": c["workload"], "decompose_s": wall, "value": c["T"] / wall, "unit": "submatrices/s",
+            "cores": threads, "e": out[2]["e"], "measured": "full decompose, not extrapolated"}
 
 
 def arm_config(c, world):
@@ -190,21 +219,22 @@ def run_reference_arm(args, c):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_1411_0814_b200 import rsm
     from oracle import refbind as R
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
         return 0
     m, n = c["m"], c["n"]
-    M = rsm.generate(m, n, c["r"], c["rho"], c["sigma"], c["seed"])
-    G = None  # dsyev is timed on a same-size SPD matrix (see cpu_reference_sample)
+    # the reference's own generator (src/synth.cpp via oracle/_ref), not ours
+    Y, W = R.generate(m, n, c["r"], c["rho"], c["sigma"], c["seed"])
     vals = []
     for s in range(args.warmup + args.steps):
-        res = cpu_reference_sample(M.values, M.mask, c, G=G, trials_prefix=8, rows_sample=4096)
+        # >= 4 trials per host thread, so the prefix keeps every thread busy
+        res = cpu_reference_sample(Y, W, c, trials_prefix=max(32, 4 * (os.cpu_count() or 1)), rows_sample=4096)
         if s >= args.warmup:
             vals.append(res)
     v = statistics.median([x["value"] for x in vals])
     est = statistics.median([x["est_decompose_s"] for x in vals])
+    c1 = cpu_reference_config1()
     line = {"metric": "submatrices/s (full RSM decompose)", "value": v, "unit": "submatrices/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -212,8 +242,9 @@ def run_reference_arm(args, c):
             "config": arm_config(c, args.gpus),
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "submatrices/s", "cores": vals[0]["cores"], "kind": "reference",
-                             "sample": vals[0]["sample"]},
-            "e2e": {"value": v, "unit": "submatrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": vals[0]["sample"], "extrapolation": vals[len(vals) // 2]["extrapolation"]},
+            "e2e": {"value": v, "unit": "submatrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "config1_measured": c1}
     print(json.dumps(line))
     return 0
 
@@ -361,10 +392,34 @@ def main():
         except Exception:
             pass
         try:
-            cpu = cpu_reference_sample(Y, W, c, G=G)
+            cpu = cpu_reference_sample(Y, W, c, G=G, V=F.v)
+            cpu["config1_measured"] = cpu_reference_config1()
         except Exception as ex:  # report, never fail the GPU line
             cpu = {"value": None, "unit": "submatrices/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {ex}"}
+    c1 = None
+    if rank == 0 and world == 1 and args.config == "config3":
+        # config 1 on this GPU (device time of one decompose, median of 9), the
+        # GPU side of the fully measured config-1 reference comparison
+        cc = CONFIGS["config1"]
+        ctx1 = rsm.Context(local)
+        ctx1.generate(cc["m"], cc["n"], cc["r"], cc["rho"], cc["sigma"], cc["seed"])
+        cfg1 = rsm.RsmConfig(rank=cc["r"], mode=rsm.Mode.M2, block=cc["k"], plan=rsm.TrialPlan(cc["T"]),
+                             seed=cc["seed"])
+        s1 = torch.cuda.ExternalStream(ctx1.stream)
+        t1 = []
+        for i in range(12):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s1)
+            ctx1.decompose(cfg1, fetch=False)
+            e1.record(s1)
+            e1.synchronize()
+            if i >= 3:
+                t1.append(e0.elapsed_time(e1))
+        ms1 = statistics.median(t1)
+        c1 = {"workload": cc["workload"], "ms_per_decompose": ms1, "value": cc["T"] / (ms1 / 1e3),
+              "unit": "submatrices/s", "note": "device time, inputs resident (device generator)"}
+        ctx1.close()
     stage_info["solve_v"]["solver"] = ctx.solver_stats()
     if args.stages and rank == 0:
         print(json.dumps(stage_info), file=sys.stderr)
@@ -377,7 +432,7 @@ def main():
                 "e2e": {"value": T / (e2e_ms / 1e3), "unit": "submatrices/s", "ms_per_step": e2e_ms,
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "roofline": roof, "stages": stage_info, "cpu_baseline": cpu, "clocks": clk,
-                "gpu_launches": launches,
+                "gpu_launches": launches, "config1": c1,
                 "harvest": {"value": T / (float(np.sum(med[:4])) * 1e-3), "unit": "submatrices/s",
                             "note": "T / device time of stages 1-3 (selection, SVD, Gram), SURVEY.md 8(d)"},
                 "report": {"e": rep.e, "attempted": rep.trials_attempted, "accepted": rep.trials_accepted,

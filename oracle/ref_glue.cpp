@@ -128,7 +128,13 @@ int ref_solve_v(const double* G, int64_t n, int64_t r, double tol, double* V, in
     GramAccumulator A(n);
     std::memcpy(A.raw().data(), G, sizeof(double) * n * n);
     const auto t0 = std::chrono::steady_clock::now();
-    SolveVResult s = solve_v(A, r, tol);
+    SolveVResult s;
+    try {
+      s = solve_v(A, r, tol);
+    } catch (...) {  // the rank gate failed after dsyev ran: still report its time
+      if (secs) *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      throw;
+    }
     if (secs) *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::memcpy(V, s.v.data(), sizeof(double) * n * r);
     *gram_rank = s.gram_rank;
