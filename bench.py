@@ -364,7 +364,31 @@ def main():
     stage_info["solve_v"].update(alg_bytes=alg["s4_bytes"])
     stage_info["solve_u"].update(alg_bytes=alg["s5_bytes"], gbs=alg["s5_bytes"] / (med[5] * 1e-3) / 1e9)
     dom = names[int(np.argmax(med[:6]))]
-    if dom in ("gram", "svd"):
+    if dom == "gram" and os.environ.get("RSM_GRAM", "") != "dfma":
+        # stage 3 runs on the tcgen05 tensor cores as an exact int8 digit
+        # split (k_gram_i8.cu): bound = the int8 tensor pipe. achieved = the
+        # int8 MMA operations the kernel's algorithm issues (upper-triangle
+        # 128 x 64 tiles x K = trials * r rows x S(S+1)/2 digit pairs x 2);
+        # the FP64 work it stands for is reported beside it
+        # against the FP64 (DFMA) peak.
+        S = int(os.environ.get("RSM_I8_SLICES", "6"))
+        npad = ((n + 127) // 128) * 128
+        ntiles = sum(1 for a in range(npad // 128) for b in range(npad // 64) if 64 * b + 63 >= 128 * a)
+        kpad = ((T * r + 31) // 32) * 32
+        ops = 2.0 * ntiles * 128 * 64 * kpad * (S * (S + 1) // 2)
+        ach = ops / (med[2] * 1e-3) / 1e12
+        i8_peak = 4500.0
+        roof = {"kernel": "gram (k_gram_i8, tcgen05 kind::i8)", "bound": "tensor", "achieved": ach, "peak": i8_peak,
+                "unit": "TFLOP/s", "frac": ach / i8_peak,
+                "peak_source": "fallback: B200_PROFILING.md nominal dense fp8/int8 4.5 PFLOP/s (MEASURED_PEAKS.json "
+                               "has no int8 figure; 2 x its bf16 burst = %.0f)" % (2 * json.load(open(
+                                   os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", 0.0)
+                                   if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 0.0),
+                "alg_int8_ops": ops, "digit_slices": S,
+                "fp64_equivalent": {"alg_flops": alg["s3_flops_survey"], "achieved": stage_info["gram"]["tflops"],
+                                    "peak": fp64, "frac": stage_info["gram"]["tflops"] / fp64, "unit": "TFLOP/s",
+                                    "peak_source": "measured in-run (DFMA microbenchmark, rsm_fp64_peak_tflops)"}}
+    elif dom in ("gram", "svd"):
         ach = stage_info[dom]["tflops"]
         roof = {"kernel": dom, "bound": "fp64", "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
                 "frac": ach / fp64, "peak_source": "measured in-run (DFMA microbenchmark, rsm_fp64_peak_tflops)"}
@@ -398,7 +422,7 @@ def main():
             cpu = {"value": None, "unit": "submatrices/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {ex}"}
     c1 = None
-    if rank == 0 and world == 1 and args.config == "config3":
+    if rank == 0 and world == 1 and args.config == "config3" and not args.no_cpu_baseline:
         # config 1 on this GPU (device time of one decompose, median of 9), the
         # GPU side of the fully measured config-1 reference comparison
         cc = CONFIGS["config1"]

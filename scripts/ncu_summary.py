@@ -29,6 +29,33 @@ def details(rep):
             print(f"{r[ki][:40]:40s} | {r[mi]:36s} = {r[vi]} {r[ui]}")
 
 
+RAW = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+       'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
+       'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
+       'sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active',
+       'sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active',
+       'sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active',
+       'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed',
+       'l1tex__throughput.avg.pct_of_peak_sustained_active',
+       'lts__t_sector_hit_rate.pct', 'smsp__issue_active.avg.pct_of_peak_sustained_active']
+
+
+def raw(rep):
+    """FP64 / tensor (IMMA, DMMA) pipe, shared-memory and DRAM lines per kernel
+    from the raw page (the details page does not carry them)."""
+    out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return
+    h, units = rows[0], rows[1]
+    ki = h.index('Kernel Name')
+    for r in rows[2:]:
+        for m in RAW:
+            if m in h:
+                i = h.index(m)
+                print(f"{r[ki][:40]:40s} | {m:72s} = {r[i]} {units[i]}")
+
+
 def sass(rep, k):
     s = subprocess.run(['ncu', '-i', rep, '-k', 'regex:' + k, '--page', 'source', '--csv', '--print-source=sass'],
                        capture_output=True, text=True).stdout
@@ -69,5 +96,6 @@ def sass(rep, k):
 
 if __name__ == '__main__':
     details(sys.argv[1])
+    raw(sys.argv[1])
     for k in sys.argv[2:]:
         sass(sys.argv[1], k)
