@@ -22,6 +22,13 @@
  *   rsm_load_matrix_csv   <- rsm::load_matrix          include/rsm/io.hpp:14, src/io.cpp:56-99
  *   rsm_save_matrix_csv   <- rsm::save_matrix          include/rsm/io.hpp:18, src/io.cpp:101-116
  *   rsm_dataset_checksum  <- rsm::dataset_checksum     include/rsm/io.hpp:22, src/io.cpp:140-154
+ *   rsm_sample            <- rsm::sample_m1 / sample_m2 (one attempt) include/rsm/sampler.hpp:41-47,
+ *                                                      src/sampler.cpp:12-87
+ *   rsm_small_singular_vectors <- rsm::small_singular_vectors include/rsm/spectra.hpp:61,
+ *                                                      src/spectra.cpp:48-86
+ *   rsm_gram_update       <- GramAccumulator::accumulate / accumulate_dense / merge
+ *                                                      include/rsm/spectra.hpp:36-43, src/spectra.cpp:7-46
+ *   rsm_masked_objective  <- rsm::masked_objective     include/rsm/core.hpp:95, src/core.cpp:41-44
  *
  * Host buffers are caller-owned; device memory is owned by the context.
  * Calls are synchronous on return, one host thread per context. Matrices
@@ -200,6 +207,37 @@ rsm_status rsm_solve_u(const double* values, const uint8_t* mask, int64_t m, int
 rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, int64_t m,
                                     int64_t n, const double* U, const double* V, int64_t r,
                                     double* e);
+
+/* -------------------------------------------- per-call building blocks */
+/* The reference's single-trial and accumulator functions, one call at a time
+ * on the device (the decomposition above never calls them; they serve the
+ * drop-in header's attempt_trial / sample_m* / GramAccumulator surface).
+ *
+ * rsm_sample: attempt `trial_index` of the TRIAL stream draws `count` indices
+ * (mode 1 = M2: rows of the m x n matrix; mode 0 = M1: columns), sorted
+ * (drawn[count], bit-exact with the reference), and keeps every column (M2) /
+ * row (M1) observed on all of them, ascending, in kept[] (capacity n for M2,
+ * m for M1), *nkept of them. count <= 16 on the device. */
+rsm_status rsm_sample(const double* values, const uint8_t* mask, int64_t m, int64_t n, int32_t mode,
+                      int64_t count, uint64_t seed, uint64_t trial_index, int64_t* drawn, int64_t* kept,
+                      int64_t* nkept);
+/* rsm::small_singular_vectors: the ell right singular vectors of the p x q
+ * row-major S with the smallest singular values, ascending, each sign-fixed
+ * (largest-magnitude entry positive); zeta is ell x q, sv the singular values
+ * (0 for vectors past the rank). The reference's validation and messages;
+ * on the device min(p, q) <= 32. Vectors of a repeated (e.g. zero) singular
+ * value are a basis of its space, as any SVD's are. */
+rsm_status rsm_small_singular_vectors(const double* S, int64_t p, int64_t q, int64_t r, int64_t ell,
+                                      double* zeta, double* sv);
+/* G (n x n, host, in/out) += sum_v x_v x_v^T over the nvec dense rows of X
+ * (nvec x n; may be NULL when nvec = 0), then += G2 when G2 is not NULL:
+ * per element in vector order with separate multiply and add, bit-identical
+ * to GramAccumulator::accumulate/accumulate_dense followed by merge. */
+rsm_status rsm_gram_update(double* G, int64_t n, const double* X, int64_t nvec, const double* G2);
+/* rsm::masked_objective: norm 0 = Frobenius (sqrt of the observed squared
+ * residual); any other norm fails with the reference's invalid_config. */
+rsm_status rsm_masked_objective(const double* values, const uint8_t* mask, int64_t m, int64_t n,
+                                const double* U, const double* V, int64_t r, int32_t norm, double* out);
 
 /* FP64 DFMA throughput of the device (TFLOP/s), the roofline denominator of
  * the FP64-bound stages (not in MEASURED_PEAKS.json). */

@@ -48,3 +48,20 @@ for t in $TESTS; do
 done
 wait
 echo "build_ref: ok ($OUT)"
+# The reference's own unit suites compiled against the B200 DROP-IN instead of
+# the reference library: include/rsm_gpu ahead of everything (its rsm/*.hpp
+# forward to include/rsm_gpu/rsm.hpp), linked to librsm_b200.so. Run on a GPU
+# by tests/test_cpp_dropin.py (oracle/_ref/dropin_test_*).
+LIBDIR="$(cd "$HERE/.." && pwd)/paper_1411_0814_b200"
+DROPIN="$(cd "$HERE/.." && pwd)/include/rsm_gpu"
+if [ -f "$LIBDIR/librsm_b200.so" ]; then
+  for t in test_core test_sampler test_spectra test_solver; do
+    exe="$OUT/dropin_$t"
+    if [ ! -f "$exe" ] || [ "$REF/tests/$t.cpp" -nt "$exe" ] || [ "$DROPIN/rsm.hpp" -nt "$exe" ] || [ "$LIBDIR/librsm_b200.so" -nt "$exe" ]; then
+      g++ -std=c++20 -O1 -w -I"$DROPIN" -I"$HERE/ref_shim" -I"$REF/tests" -o "$exe" "$REF/tests/$t.cpp" \
+        -L"$LIBDIR" -lrsm_b200 -Wl,-rpath,'$ORIGIN/../../paper_1411_0814_b200' "$OPENBLAS" -Wl,-rpath,"$SCIPY_LIBS" &
+    fi
+  done
+  wait
+  echo "build_ref: drop-in suites ok"
+fi

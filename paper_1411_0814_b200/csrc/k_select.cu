@@ -33,36 +33,8 @@ __global__ void __launch_bounds__(256) k_select(const uint32_t* __restrict__ bit
   int32_t* my = sidx + (size_t)warp * apw * block;
   const int64_t a = base + lane;
   if (lane < apw && a < count) {
-    uint64_t st = rng_state(seed, 5 /* stream::TRIAL */, a0 + (uint64_t)a);
-    int32_t key[2 * KMAX], val[2 * KMAX];
-    int nmap = 0;
-    for (int t = 0; t < block; ++t) {
-      const int32_t j = t + (int32_t)next_below(st, (uint64_t)(pool - t));
-      int32_t vt = t, vj = j;
-      int ft = -1, fj = -1;
-      for (int e = 0; e < nmap; ++e) {
-        if (key[e] == t) { vt = val[e]; ft = e; }
-        if (key[e] == j) { vj = val[e]; fj = e; }
-      }
-      // swap(idx[t], idx[j])
-      if (ft < 0) { key[nmap] = t; ft = nmap++; }
-      val[ft] = vj;
-      if (fj < 0) {
-        if (j != t) { key[nmap] = j; fj = nmap++; val[fj] = vt; }
-      } else {
-        val[fj] = vt;
-      }
-    }
     int32_t* out = my + lane * block;
-    for (int t = 0; t < block; ++t) {
-      int32_t v = t;
-      for (int e = 0; e < nmap; ++e)
-        if (key[e] == t) { v = val[e]; break; }
-      // insertion into the sorted prefix
-      int p = t - 1;
-      while (p >= 0 && out[p] > v) { out[p + 1] = out[p]; --p; }
-      out[p + 1] = v;
-    }
+    draw_sorted(seed, a0 + (uint64_t)a, pool, block, out);
     for (int t = 0; t < block; ++t) idx_out[a * block + t] = out[t];
   }
   __syncwarp();

@@ -413,7 +413,12 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     const int nj = (int)total(NA + R);
 
     double u[R];
-    const bool flagged = row_solve<R>(A, bv, nj, u);
+    bool flagged = row_solve<R>(A, bv, nj, u);
+    if (a.Ugiven) {  // residual of given factors: the same arithmetic from here on
+#pragma unroll
+      for (int q = 0; q < R; ++q) u[q] = a.Ugiven[row * R + q];
+      flagged = false;
+    }
     // second pass over the row still in shared memory: direct residual
     double ss = 0.0;
     auto res_y = [&](int64_t c, bool k, double yraw) {
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   // normal matrix from each word's minority cells, then one reduction of the
   // normal equations, the observed count and the previous row's residual
   // (ss_prev, returned summed), and the solve
-  auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u, double& ss_prev) -> bool {
+  auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u, double& ss_prev, int64_t frow) -> bool {
     int cnt = 0;
     for (int w = lane; w < nwn; w += 32) {
       const int rem = (int)(n - (int64_t)w * 32);
@@ -651,7 +656,13 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, NA + i);
     const int nj = (int)warp_total<NV>(acc, NA + R);
     ss_prev = warp_total<NV>(acc, NA + R + 1);
-    return row_solve<R>(A, bv, nj, u);
+    const bool fl = row_solve<R>(A, bv, nj, u);
+    if (a.Ugiven) {  // residual of given factors: the same arithmetic from here on
+#pragma unroll
+      for (int q = 0; q < R; ++q) u[q] = a.Ugiven[frow * R + q];
+      return false;
+    }
+    return fl;
   };
   // row 0: accumulation pass alone
   double u[R];
@@ -677,7 +688,7 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
       accum_b(acc, v, y[c], (wd[nfull] >> lane) & 1u);
     }
     double none = 0.0;
-    flagged = finish(acc, wd, u, none);
+    flagged = finish(acc, wd, u, none, r0);
   }
   for (int64_t k = 0; k < nrows; ++k) {
     const int64_t row = r0 + k * nw;
@@ -738,7 +749,7 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     if (lane == 0 && flagged) atomicAdd(a.flagged, 1);
     __syncwarp();  // row k's buffer is free: refill it with row k+2
     if (k + 2 < nrows) issue(r0 + (k + 2) * nw, b);
-    if (has_next) flagged = finish(acc, wn, u, ss);  // ss: row k's residual, summed
+    if (has_next) flagged = finish(acc, wn, u, ss, row + nw);  // ss: row k's residual, summed
     else ss = warp_sum(ss);
     if (lane == 0) a.rowres[row] = ss;
   }

@@ -161,6 +161,7 @@ struct rsm_ctx {
   DevBuf sel_idx, sel_q, blockcnt, selstate, t_attempt, t_q, t_idx, t_cm, Vtrial,
       colcnt, svd_scr, svd_scr32, P, tiles, G, eX, eY, eZ, ePart, eW, eI, eD, Vhat, U, rowres,
       flagged, dsum, cnt64, Wq, tiles8, ugather;
+  DevBuf aux0, aux1, aux2, aux3;  // per-call utilities (rsm_sample, rsm_small_singular_vectors, rsm_gram_update)
   int64_t tiles_n = -1;
   int64_t tiles8_n = -1;  // tcgen05 stage-3 tile list valid for this npad
   int ntiles8 = 0;
@@ -810,7 +811,8 @@ struct SolveUOut {
 // stage 5 on view v: rows of `out` (v.m x r) from the basis (v.n x r), plus
 // the residual sum and the flagged-row count; row-sharded over ranks with
 // the shards gathered into `out` (detail/row_solve.hpp:12-36, solver.cpp:64-89)
-SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& outbuf, int64_t r) {
+SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& outbuf, int64_t r,
+                     const double* ugiven = nullptr) {
   if (r < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_u: rank must be positive");
   if (r > 8) fail(RSM_ERR_INVALID_CONFIG, "device row solver supports r <= 8");
   outbuf.ensure(sizeof(double) * v.m * r);
@@ -830,6 +832,7 @@ SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& out
   a.rowres = c->rowres.as<double>();
   a.flagged = c->flagged.as<int>();
   a.r = (int)r;
+  a.Ugiven = ugiven;
   if (hi > lo) {
     rsmk::launch_solve_u(a, c->stream);
     rsmk::launch_sum_rows(c->rowres.as<double>() + lo, hi - lo, c->dsum.as<double>(), c->stream);
@@ -953,6 +956,13 @@ void als_impl(rsm_ctx* c, int64_t r, int64_t iterations, uint64_t seed, double* 
     solve_rows(c, vt, c->U.as<double>(), c->Vhat, r);
   }
   us = solve_rows(c, vm, c->Vhat.as<double>(), c->U, r);
+  if (m < n) {
+    // masked_residual_norm evaluates wide matrices on the transpose (as
+    // decompose does); take e the same way so the two agree bit for bit
+    const double ss_rows = us.ss;
+    us.ss = solve_rows(c, vt, c->U.as<double>(), c->aux1, r, c->Vhat.as<double>()).ss;
+    (void)ss_rows;
+  }
   c->Vhat_n = n;
   c->Vhat_r = r;
   c->U_m = m;
@@ -1388,19 +1398,35 @@ rsm_status rsm_solve_u(const double* values, const uint8_t* mask, int64_t m, int
   return st;
 }
 
-rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, int64_t m, int64_t n,
-                                    const double* U, const double* V, int64_t r, double* e) {
-  // core.cpp:35-39 on the device: the stage-5 residual pass with U given is
-  // not exposed separately; compute via a solve-free kernel path.
+// observed squared residual sum (core.cpp:15-31) of given factors on the
+// default context: the per-row warp kernel and the fixed-order row sum
+static rsm_status residual_ss(const double* values, const uint8_t* mask, int64_t m, int64_t n, const double* U,
+                              const double* V, int64_t r, double* ss_out, int64_t* known) {
   rsm_ctx* c = nullptr;
   rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
   if (st) return st;
   std::lock_guard<std::mutex> lk(c->oneshot);
   st = rsm_ctx_load(c, values, mask, m, n);
   if (st) { g_err = c->err; return st; }
-  return guard(c, [&] {
-    if (c->known == 0) fail(RSM_ERR_INVALID_CONFIG, "empty mask: no known entries");
+  st = guard(c, [&] {
     if (r < 1 || r > 16) fail(RSM_ERR_INVALID_CONFIG, "residual: 1 <= r <= 16 on the device");
+    if (r <= 8) {
+      // the stage-5 kernel's residual pass with the rows' solutions given, on
+      // the orientation decompose uses (the transpose when m < n): the same
+      // arithmetic and summation order, so decompose's e and this agree bit
+      // for bit (solver.cpp:142 computes e with masked_residual_norm itself)
+      const bool tr = m < n;
+      const View v = make_view(c, tr, false);
+      c->Vhat.ensure(sizeof(double) * v.n * r);
+      c->aux0.ensure(sizeof(double) * v.m * r);
+      ck(cudaMemcpyAsync(c->Vhat.p, tr ? U : V, sizeof(double) * v.n * r, cudaMemcpyHostToDevice, c->stream), "H2D");
+      ck(cudaMemcpyAsync(c->aux0.p, tr ? V : U, sizeof(double) * v.m * r, cudaMemcpyHostToDevice, c->stream), "H2D");
+      c->U_m = 0;
+      c->Vhat_n = 0;
+      *ss_out = solve_rows(c, v, c->Vhat.as<double>(), c->aux1, r, c->aux0.as<double>()).ss;
+      *known = c->known;
+      return;
+    }
     const View v = make_view(c, false, false);
     c->U.ensure(sizeof(double) * m * r);
     c->Vhat.ensure(sizeof(double) * n * r);
@@ -1413,12 +1439,144 @@ rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, i
     rsmk::launch_residual(v.Y, v.bitsR, m, n, v.nwp, c->U.as<double>(), c->Vhat.as<double>(), (int)r,
                           c->rowres.as<double>(), c->stream);
     rsmk::launch_sum_rows(c->rowres.as<double>(), m, c->dsum.as<double>(), c->stream);
-    double ss = 0.0;
-    ck(cudaMemcpyAsync(&ss, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(ss_out, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "residual");
     ck(cudaGetLastError(), "residual kernels");
-    *e = std::sqrt(ss) / std::sqrt((double)c->known);
+    *known = c->known;
   });
+  if (st) g_err = c->err;
+  return st;
+}
+
+rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, int64_t m, int64_t n,
+                                    const double* U, const double* V, int64_t r, double* e) {
+  // core.cpp:35-39 on the device
+  double ss = 0.0;
+  int64_t known = 0;
+  rsm_status st = residual_ss(values, mask, m, n, U, V, r, &ss, &known);
+  if (st) return st;
+  if (known == 0) {
+    g_err = "empty mask: no known entries";
+    return RSM_ERR_INVALID_CONFIG;
+  }
+  *e = std::sqrt(ss) / std::sqrt((double)known);
+  return RSM_OK;
+}
+
+rsm_status rsm_masked_objective(const double* values, const uint8_t* mask, int64_t m, int64_t n, const double* U,
+                                const double* V, int64_t r, int32_t norm, double* out) {
+  // core.cpp:41-44: only the Frobenius norm exists
+  if (norm != 0) {
+    g_err = "unsupported norm: only frobenius is implemented";
+    return RSM_ERR_INVALID_CONFIG;
+  }
+  double ss = 0.0;
+  int64_t known = 0;
+  rsm_status st = residual_ss(values, mask, m, n, U, V, r, &ss, &known);
+  if (st) return st;
+  *out = std::sqrt(ss);
+  return RSM_OK;
+}
+
+rsm_status rsm_sample(const double* values, const uint8_t* mask, int64_t m, int64_t n, int32_t mode,
+                      int64_t count, uint64_t seed, uint64_t trial_index, int64_t* drawn, int64_t* kept,
+                      int64_t* nkept) {
+  // sampler.cpp:27-87 for one attempt: the draw on the device with the
+  // selection kernels' code, the kept set from the bit-packed mask
+  const bool m2 = mode == RSM_MODE_M2;
+  if (m2 ? (count < 1 || count > m) : (count < 1 || count > n)) {
+    g_err = m2 ? "sample_m2: row count out of range" : "sample_m1: column count out of range";
+    return RSM_ERR_INVALID_CONFIG;
+  }
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
+  st = rsm_ctx_load(c, values, mask, m, n);
+  if (st) { g_err = c->err; return st; }
+  st = guard(c, [&] {
+    if (count > rsmd::KMAX) fail(RSM_ERR_INVALID_CONFIG, "device path supports at most 16 drawn indices");
+    const View v = make_view(c, false, !m2);
+    const uint32_t* bits = m2 ? v.bitsR : v.bitsC;
+    const int64_t stride = m2 ? v.nwp : v.mwp;
+    const int64_t nwords = m2 ? ceil_div(n, 32) : ceil_div(m, 32);
+    const int64_t pool = m2 ? m : n;
+    const int64_t other = m2 ? n : m;
+    c->aux0.ensure(sizeof(int32_t) * rsmd::KMAX);
+    c->aux1.ensure(sizeof(uint32_t) * nwords);
+    c->aux2.ensure(sizeof(int32_t) * other);
+    c->aux3.ensure(sizeof(int64_t));
+    rsmk::launch_sample_one(bits, stride, nwords, pool, (int)count, seed, trial_index, c->aux0.as<int32_t>(),
+                            c->aux1.as<uint32_t>(), c->aux2.as<int32_t>(), c->aux3.as<int64_t>(), c->stream);
+    ++c->launches;
+    std::vector<int32_t> d((size_t)count), k((size_t)other);
+    int64_t nk = 0;
+    ck(cudaMemcpyAsync(&nk, c->aux3.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(d.data(), c->aux0.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(k.data(), c->aux2.p, sizeof(int32_t) * other, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sample");
+    ck(cudaGetLastError(), "sample kernel");
+    for (int64_t i = 0; i < count; ++i) drawn[i] = d[(size_t)i];
+    for (int64_t i = 0; i < nk; ++i) kept[i] = k[(size_t)i];
+    *nkept = nk;
+  });
+  if (st) g_err = c->err;
+  return st;
+}
+
+rsm_status rsm_small_singular_vectors(const double* S, int64_t p, int64_t q, int64_t r, int64_t ell, double* zeta,
+                                      double* sv) {
+  // spectra.cpp:48-56: the reference's validation, in its order
+  if (q - r < 1) { g_err = "degenerate submatrix: needs more than r columns"; return RSM_ERR_INVALID_CONFIG; }
+  if (p < r + 1) { g_err = "degenerate submatrix: needs more than r rows"; return RSM_ERR_INVALID_CONFIG; }
+  if (ell < 1 || ell > q - r) { g_err = "vector count must lie in [1, cols-r]"; return RSM_ERR_INVALID_CONFIG; }
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
+  st = guard(c, [&] {
+    if (std::min(p, q) > 32) fail(RSM_ERR_INVALID_CONFIG, "device path supports min(rows, cols) <= 32");
+    if (p * q > ((int64_t)1 << 28) || q > 65536) fail(RSM_ERR_INVALID_CONFIG, "submatrix too large for the device path");
+    c->aux0.ensure(sizeof(double) * p * q);
+    c->aux1.ensure(sizeof(double) * rsmk::small_svd_scratch_doubles((int)p, (int)q));
+    c->aux2.ensure(sizeof(double) * ell * q);
+    c->aux3.ensure(sizeof(double) * ell);
+    ck(cudaMemcpyAsync(c->aux0.p, S, sizeof(double) * p * q, cudaMemcpyHostToDevice, c->stream), "H2D S");
+    rsmk::launch_small_svd(c->aux0.as<double>(), (int)p, (int)q, (int)ell, c->aux1.as<double>(),
+                           c->aux2.as<double>(), c->aux3.as<double>(), c->stream);
+    ++c->launches;
+    ck(cudaMemcpyAsync(zeta, c->aux2.p, sizeof(double) * ell * q, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(sv, c->aux3.p, sizeof(double) * ell, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "small svd");
+    ck(cudaGetLastError(), "small svd kernel");
+  });
+  if (st) g_err = c->err;
+  return st;
+}
+
+rsm_status rsm_gram_update(double* G, int64_t n, const double* X, int64_t nvec, const double* G2) {
+  if (n < 1) { g_err = "gram accumulator: dimension must be positive"; return RSM_ERR_INVALID_CONFIG; }
+  if (nvec < 0 || (nvec > 0 && !X)) { g_err = "accumulate: dimension mismatch"; return RSM_ERR_INVALID_CONFIG; }
+  rsm_ctx* c = nullptr;
+  rsm_status st = guard(nullptr, [&] { c = default_ctx(); });
+  if (st) return st;
+  std::lock_guard<std::mutex> lk(c->oneshot);
+  st = guard(c, [&] {
+    c->aux0.ensure(sizeof(double) * n * n);
+    c->aux1.ensure(sizeof(double) * std::max<int64_t>(nvec, 1) * n);
+    if (G2) c->aux2.ensure(sizeof(double) * n * n);
+    ck(cudaMemcpyAsync(c->aux0.p, G, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "H2D G");
+    if (nvec > 0) ck(cudaMemcpyAsync(c->aux1.p, X, sizeof(double) * nvec * n, cudaMemcpyHostToDevice, c->stream), "H2D X");
+    if (G2) ck(cudaMemcpyAsync(c->aux2.p, G2, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream), "H2D G2");
+    rsmk::launch_gram_update(c->aux0.as<double>(), n, c->aux1.as<double>(), nvec, G2 ? c->aux2.as<double>() : nullptr,
+                             c->stream);
+    ++c->launches;
+    ck(cudaMemcpyAsync(G, c->aux0.p, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->stream), "D2H G");
+    ck(cudaStreamSynchronize(c->stream), "gram update");
+    ck(cudaGetLastError(), "gram update kernel");
+  });
+  if (st) g_err = c->err;
+  return st;
 }
 
 }  // extern "C"

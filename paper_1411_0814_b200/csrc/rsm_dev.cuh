@@ -43,6 +43,42 @@ __device__ __forceinline__ uint64_t next_below(uint64_t& s, uint64_t bound) {
   }
 }
 
+// draw_without_replacement (sampler.cpp:12-23) for attempt `a` of the TRIAL
+// stream: the partial Fisher-Yates on a virtual identity permutation (a
+// position -> value map of the <= 2 block touched slots), then the drawn
+// values sorted ascending into out[0..block). block <= KMAX.
+__device__ inline void draw_sorted(uint64_t seed, uint64_t a, int64_t pool, int block, int32_t* out) {
+  uint64_t st = rng_state(seed, 5 /* stream::TRIAL */, a);
+  int32_t key[2 * KMAX], val[2 * KMAX];
+  int nmap = 0;
+  for (int t = 0; t < block; ++t) {
+    const int32_t j = t + (int32_t)next_below(st, (uint64_t)(pool - t));
+    int32_t vt = t, vj = j;
+    int ft = -1, fj = -1;
+    for (int e = 0; e < nmap; ++e) {
+      if (key[e] == t) { vt = val[e]; ft = e; }
+      if (key[e] == j) { vj = val[e]; fj = e; }
+    }
+    // swap(idx[t], idx[j])
+    if (ft < 0) { key[nmap] = t; ft = nmap++; }
+    val[ft] = vj;
+    if (fj < 0) {
+      if (j != t) { key[nmap] = j; fj = nmap++; val[fj] = vt; }
+    } else {
+      val[fj] = vt;
+    }
+  }
+  for (int t = 0; t < block; ++t) {
+    int32_t v = t;
+    for (int e = 0; e < nmap; ++e)
+      if (key[e] == t) { v = val[e]; break; }
+    // insertion into the sorted prefix
+    int p = t - 1;
+    while (p >= 0 && out[p] > v) { out[p + 1] = out[p]; --p; }
+    out[p + 1] = v;
+  }
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -107,6 +107,8 @@ struct SolveUArgs {
   double* rowres;   // m residual^2 per row
   int* flagged;     // count (integer atomics)
   int r;
+  const double* Ugiven;  // non-null: rows' solutions given (m x r), only the residual pass
+                         // counts (masked_residual_norm through the stage-5 arithmetic)
 };
 
 // rsm_ctx.cu: message for rsm_last_error(NULL) from host-only entry points
@@ -155,6 +157,14 @@ cudaError_t launch_eig(const EigArgs& a, int grid, cudaStream_t s);
 int eig_max_grid();
 void launch_sign_fix(double* V, int64_t n, int r, cudaStream_t s);
 void launch_zero_rows(const double* G, int64_t n, const int* cnt, int* out, cudaStream_t s);
+// k_dropin.cu (drop-in header utilities, one call at a time)
+void launch_sample_one(const uint32_t* bits, int64_t stride, int64_t nwords, int64_t pool, int count, uint64_t seed,
+                       uint64_t index, int32_t* drawn, uint32_t* words, int32_t* kept, int64_t* nkept,
+                       cudaStream_t s);
+size_t small_svd_scratch_doubles(int p, int q);
+void launch_small_svd(const double* S, int p, int q, int ell, double* scratch, double* zeta, double* sv,
+                      cudaStream_t s);
+void launch_gram_update(double* G, int64_t n, const double* X, int64_t nvec, const double* G2, cudaStream_t s);
 // k_solve_u.cu
 void launch_solve_u(const SolveUArgs& a, cudaStream_t s);
 void launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s);

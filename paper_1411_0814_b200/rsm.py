@@ -123,6 +123,10 @@ def lib():
         "rsm_host_group_create": (i32, [C.c_int, C.POINTER(_P)]),
         "rsm_host_group_destroy": (i32, [_P]),
         "rsm_ctx_create_host_group": (i32, [C.POINTER(_P), C.c_int, _P, C.c_int]),
+        "rsm_sample": (i32, [_P, _P, i64, i64, i32, i64, u64, u64, _P, _P, C.POINTER(i64)]),
+        "rsm_small_singular_vectors": (i32, [_P, i64, i64, i64, i64, _P, _P]),
+        "rsm_gram_update": (i32, [_P, i64, _P, i64, _P]),
+        "rsm_masked_objective": (i32, [_P, _P, i64, i64, _P, _P, i64, i32, C.POINTER(dbl)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -141,7 +145,8 @@ def exported_symbols():
             "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_generate_tracks", "rsm_load_matrix_csv",
             "rsm_save_matrix_csv", "rsm_dataset_checksum", "rsm_free", "rsm_fp64_peak_tflops",
             "rsm_dmma_peak_tflops", "rsm_shard_range", "rsm_host_group_create", "rsm_host_group_destroy",
-            "rsm_ctx_create_host_group"]
+            "rsm_ctx_create_host_group", "rsm_sample", "rsm_small_singular_vectors", "rsm_gram_update",
+            "rsm_masked_objective"]
 
 
 def _check(st: int, ctx=None):
@@ -615,3 +620,105 @@ def dataset_checksum(M: MaskedMatrix) -> int:
     if st:
         raise Error(st, lib().rsm_last_error(None).decode())
     return int(out.value)
+
+
+# ------------------------------------------------ per-call building blocks
+# The reference's single-trial and accumulator functions (sampler.hpp,
+# spectra.hpp, solver.hpp:40-42, core.hpp:95), one device call each.
+
+@dataclass
+class Submatrix:
+    """rsm::Submatrix (include/rsm/sampler.hpp:13-28)."""
+    row_indices: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray  # |rows| x |cols|
+
+    def rows(self) -> int:
+        return len(self.row_indices)
+
+    def cols(self) -> int:
+        return len(self.col_indices)
+
+
+@dataclass
+class ConstraintVector:
+    """rsm::ConstraintVector (include/rsm/spectra.hpp:12-19)."""
+    col_indices: np.ndarray
+    zeta: np.ndarray
+    singular_value: float = 0.0
+
+
+def _sample(M: MaskedMatrix, mode: int, count: int, seed: int, index: int, min_keep: int):
+    other = M.n if mode == Mode.M2 else M.m
+    drawn = np.zeros(max(count, 1), np.int64)
+    kept = np.zeros(max(other, 1), np.int64)
+    nk = C.c_int64()
+    _check(lib().rsm_sample(_ptr(M.values), _ptr(M.mask), M.m, M.n, int(mode), count, seed, index, _ptr(drawn),
+                            _ptr(kept), C.byref(nk)))
+    drawn, kept = drawn[:count], kept[:nk.value]
+    if nk.value < min_keep:
+        return None
+    rows, cols = (drawn, kept) if mode == Mode.M2 else (kept, drawn)
+    return Submatrix(rows, cols, np.ascontiguousarray(M.values[np.ix_(rows, cols)]))
+
+
+def sample_m1(M: MaskedMatrix, l: int, seed: int, trial_index: int, min_rows: int = 1):
+    """rsm::sample_m1 (sampler.cpp:27-56): None when fewer than min_rows rows survive."""
+    return _sample(M, Mode.M1, l, seed, trial_index, min_rows)
+
+
+def sample_m2(M: MaskedMatrix, k: int, seed: int, trial_index: int, min_cols: int = 1):
+    """rsm::sample_m2 (sampler.cpp:58-87): None when fewer than min_cols columns survive."""
+    return _sample(M, Mode.M2, k, seed, trial_index, min_cols)
+
+
+def small_singular_vectors(S: Submatrix, r: int, ell: int):
+    """rsm::small_singular_vectors (spectra.cpp:48-86) -> [ConstraintVector]."""
+    V = np.ascontiguousarray(S.values, dtype=np.float64)
+    p, q = V.shape
+    zeta = np.zeros((max(ell, 1), q))
+    sv = np.zeros(max(ell, 1))
+    _check(lib().rsm_small_singular_vectors(_ptr(V), p, q, r, ell, _ptr(zeta), _ptr(sv)))
+    return [ConstraintVector(np.asarray(S.col_indices), zeta[t].copy(), float(sv[t])) for t in range(ell)]
+
+
+def attempt_trial(M: MaskedMatrix, p: TrialParams, index: int):
+    """rsm::attempt_trial (harvest.cpp:37-51): None when rejected."""
+    if p.mode == Mode.M1:
+        S = sample_m1(M, p.block, p.seed, index, p.min_count)
+        return None if S is None else small_singular_vectors(S, p.rank, p.ell)
+    S = sample_m2(M, p.block, p.seed, index, p.min_count)
+    if S is None:
+        return None
+    avail = S.cols() - p.rank
+    ell = min(p.ell, avail) if p.ell > 0 else avail
+    return small_singular_vectors(S, p.rank, ell)
+
+
+def embed(cv: ConstraintVector, n: int) -> np.ndarray:
+    """rsm::embed (spectra.cpp:88-96)."""
+    if np.any((cv.col_indices < 0) | (cv.col_indices >= n)):
+        raise Error(errc.invalid_config, "embed: column index out of range")
+    x = np.zeros(n)
+    x[cv.col_indices] = cv.zeta
+    return x
+
+
+def gram_update(G: np.ndarray, X: np.ndarray | None = None, G2: np.ndarray | None = None) -> np.ndarray:
+    """G += sum_v x_v x_v^T (+ G2) on the device, bit-identical to the
+    reference's GramAccumulator::accumulate / merge loops (spectra.cpp:7-46)."""
+    G = np.ascontiguousarray(G, dtype=np.float64).copy()
+    n = G.shape[0]
+    Xc = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, n) if X is not None else None
+    G2c = np.ascontiguousarray(G2, dtype=np.float64) if G2 is not None else None
+    _check(lib().rsm_gram_update(_ptr(G), n, _ptr(Xc), 0 if Xc is None else Xc.shape[0], _ptr(G2c)))
+    return G
+
+
+def masked_objective(M: MaskedMatrix, F: Factorization, norm: int = 0) -> float:
+    """rsm::masked_objective (core.cpp:41-44): norm 0 = Frobenius."""
+    out = C.c_double()
+    _check(lib().rsm_masked_objective(_ptr(M.values), _ptr(M.mask), M.m, M.n,
+                                      _ptr(np.ascontiguousarray(F.u)), _ptr(np.ascontiguousarray(F.v)),
+                                      F.u.shape[1], norm, C.byref(out)))
+    return out.value

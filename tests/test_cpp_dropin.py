@@ -27,3 +27,20 @@ def test_dropin_reference_cases_on_gpu(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+SUITES = ["test_core", "test_sampler", "test_spectra", "test_solver"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_unit_suites_against_dropin(suite):
+    """The reference's OWN doctest suites (tests/<suite>.cpp of the reference),
+    compiled by oracle/build_ref.sh against include/rsm_gpu (the drop-in) and
+    librsm_b200.so instead of the reference library, run on the GPU."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_" + suite)
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_* not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600, cwd="/tmp")
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " 0 failed" in r.stdout
