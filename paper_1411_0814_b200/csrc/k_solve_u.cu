@@ -484,7 +484,12 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
 // words, so at most 16 outer products per word and ~0.2 n per row at config 3
 // (rho = 0.8) instead of n. The observed count and row k's residual ride in
 // the same warp reduction as row k+1's normal equations.
-template <int R>
+// WALK = false: the minority outer products are accumulated inside the
+// streaming loop instead (row-level decision: V^T V minus the hidden cells
+// when at least half the row is observed, else the observed cells), with the
+// basis row already in registers -- no extra shared-memory reads, ~14 more
+// FP64 instructions per cell.
+template <int R, bool WALK>
 __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   constexpr int NP = (R + 1) / 2;
   constexpr int NA = R * (R + 1) / 2;
@@ -531,6 +536,13 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     }
 #pragma unroll
     for (int p = 0; p < NA; ++p) Vw[(int64_t)w * NA + p] = part[p];
+  }
+  __syncthreads();
+  __shared__ double Aall[NA];  // V^T V = sum of the word Grams in word order
+  if (!WALK && threadIdx.x < NA) {
+    double t = 0.0;
+    for (int w = 0; w < nwn; ++w) t += Vw[(int64_t)w * NA + threadIdx.x];
+    Aall[threadIdx.x] = t;
   }
   __syncthreads();
   auto vload = [&](int64_t c, double* v) {
@@ -597,6 +609,27 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     for (int i = 0; i < R; ++i) acc[NA + i] = fma(yc, v[i], acc[NA + i]);
   };
   // direct residual term: d = y - u.v from y (nu = -u), zero when hidden
+  // in-loop minority outer product (WALK = false): weight sg on the selected cells
+  auto accum_A = [&](double* acc, const double* v, bool k, bool hid) {
+    const double w = (hid ? !k : k) ? (hid ? -1.0 : 1.0) : 0.0;
+    double t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) t[i] = w * v[i];
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int j = i; j < R; ++j) {
+        acc[p] = fma(t[i], v[j], acc[p]);
+        ++p;
+      }
+  };
+  // observed count of a row (all lanes get it) and its minority side
+  auto row_count = [&](const uint32_t* wd) -> int {
+    int c = 0;
+    for (int w = lane; w < nwn; w += 32) c += __popc(wd[w]);
+    return warp_sum_int(c);
+  };
   auto resid = [&](double& ss, const double* v, const double* nu, double yraw, bool k) {
     double d = yraw;
 #pragma unroll
@@ -607,9 +640,17 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   // normal matrix from each word's minority cells, then one reduction of the
   // normal equations, the observed count and the previous row's residual
   // (ss_prev, returned summed), and the solve
-  auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u, double& ss_prev, int64_t frow) -> bool {
+  auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u, double& ss_prev, int64_t frow, int njr,
+                    bool hidr) -> bool {
     int cnt = 0;
-    for (int w = lane; w < nwn; w += 32) {
+    if (!WALK) {
+      if (hidr) {
+#pragma unroll
+        for (int p = 0; p < NA; ++p) acc[p] += lane == 0 ? Aall[p] : 0.0;
+      }
+      cnt = lane == 0 ? njr : 0;
+    }
+    for (int w = lane; WALK && w < nwn; w += 32) {
       const int rem = (int)(n - (int64_t)w * 32);
       const unsigned valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
       const unsigned obs = wd[w] & valid;
@@ -671,6 +712,8 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     wait_buf(0);
     const double* y = ybuf(0);
     const uint32_t* wd = reinterpret_cast<const uint32_t*>(y + npd);
+    const int nj0 = WALK ? 0 : row_count(wd);
+    const bool hid0 = 2 * (int64_t)nj0 >= n;
     double acc[NV];
 #pragma unroll
     for (int p = 0; p < NV; ++p) acc[p] = 0.0;
@@ -679,16 +722,20 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
       const int64_t c = w * 32 + lane;
       double v[R];
       vload(c, v);
-      accum_b(acc, v, y[c], (wd[w] >> lane) & 1u);
+      const bool k0 = (wd[w] >> lane) & 1u;
+      accum_b(acc, v, y[c], k0);
+      if (!WALK) accum_A(acc, v, k0, hid0);
     }
     if (tail) {
       const int64_t c = (int64_t)nfull * 32 + lane;
       double v[R];
       vload(c, v);
-      accum_b(acc, v, y[c], (wd[nfull] >> lane) & 1u);
+      const bool k0 = (wd[nfull] >> lane) & 1u;
+      accum_b(acc, v, y[c], k0);
+      if (!WALK) accum_A(acc, v, k0, hid0);
     }
     double none = 0.0;
-    flagged = finish(acc, wd, u, none, r0);
+    flagged = finish(acc, wd, u, none, r0, nj0, hid0);
   }
   for (int64_t k = 0; k < nrows; ++k) {
     const int64_t row = r0 + k * nw;
@@ -706,8 +753,14 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     for (int p = 0; p < NV; ++p) acc[p] = 0.0;
     const double* yn = ybuf(b ^ 1);
     const uint32_t* wn = reinterpret_cast<const uint32_t*>(yn + npd);
+    int nj1 = 0;
+    bool hid1 = false;
     if (has_next) {
       wait_buf(b ^ 1);
+      if (!WALK) {
+        nj1 = row_count(wn);
+        hid1 = 2 * (int64_t)nj1 >= n;
+      }
       // residual of row k and V_O^T y of row k+1 share the V-hat reads
 #pragma unroll 4
       for (int w = 0; w < nfull; ++w) {
@@ -715,14 +768,18 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
         double v[R];
         vload(c, v);
         resid(ss, v, nu, y[c], (wd[w] >> lane) & 1u);
-        accum_b(acc, v, yn[c], (wn[w] >> lane) & 1u);
+        const bool k1 = (wn[w] >> lane) & 1u;
+        accum_b(acc, v, yn[c], k1);
+        if (!WALK) accum_A(acc, v, k1, hid1);
       }
       if (tail) {
         const int64_t c = (int64_t)nfull * 32 + lane;
         double v[R];
         vload(c, v);
         resid(ss, v, nu, y[c], (wd[nfull] >> lane) & 1u);
-        accum_b(acc, v, yn[c], (wn[nfull] >> lane) & 1u);
+        const bool k1 = (wn[nfull] >> lane) & 1u;
+        accum_b(acc, v, yn[c], k1);
+        if (!WALK) accum_A(acc, v, k1, hid1);
       }
     } else {
 #pragma unroll 4
@@ -749,7 +806,7 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     if (lane == 0 && flagged) atomicAdd(a.flagged, 1);
     __syncwarp();  // row k's buffer is free: refill it with row k+2
     if (k + 2 < nrows) issue(r0 + (k + 2) * nw, b);
-    if (has_next) flagged = finish(acc, wn, u, ss, row + nw);  // ss: row k's residual, summed
+    if (has_next) flagged = finish(acc, wn, u, ss, row + nw, nj1, hid1);  // ss: row k's residual, summed
     else ss = warp_sum(ss);
     if (lane == 0) a.rowres[row] = ss;
   }
@@ -841,11 +898,20 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
         int w = (int)std::min<size_t>(SU_MAXW, (capw - head - vbytes - wgram) / per_warp);
         if (w < 1) w = 1;
         const size_t smem = head + vbytes + wgram + (size_t)w * per_warp;
-        cudaFuncSetAttribute(k_solve_u_fused<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        static const bool walk = [] {
+          const char* e = getenv("RSM_SU_WALK");
+          return !(e && atoi(e) == 0);
+        }();
         const int64_t rows = a.row_hi - a.row_lo;
         int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
         if (blocks < 1) blocks = 1;
-        k_solve_u_fused<R><<<(unsigned)blocks, w * 32, smem, s>>>(a);
+        if (walk) {
+          cudaFuncSetAttribute(k_solve_u_fused<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          k_solve_u_fused<R, true><<<(unsigned)blocks, w * 32, smem, s>>>(a);
+        } else {
+          cudaFuncSetAttribute(k_solve_u_fused<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          k_solve_u_fused<R, false><<<(unsigned)blocks, w * 32, smem, s>>>(a);
+        }
         return;
       }
     }

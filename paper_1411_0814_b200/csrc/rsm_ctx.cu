@@ -162,6 +162,7 @@ struct rsm_ctx {
       colcnt, svd_scr, svd_scr32, P, tiles, G, eX, eY, eZ, ePart, eW, eI, eD, Vhat, U, rowres,
       flagged, dsum, cnt64, Wq, tiles8, ugather;
   DevBuf aux0, aux1, aux2, aux3;  // per-call utilities (rsm_sample, rsm_small_singular_vectors, rsm_gram_update)
+  double* hsmall = nullptr;  // pinned host staging: eig stats [0,96), stage-5 scalars [96,100)
   int64_t tiles_n = -1;
   int64_t tiles8_n = -1;  // tcgen05 stage-3 tile list valid for this npad
   int ntiles8 = 0;
@@ -698,7 +699,19 @@ struct SolveVOut {
   std::vector<double> w;
 };
 
-SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
+double* pinned_small(rsm_ctx* c) {
+  if (!c->hsmall) ck(cudaMallocHost(&c->hsmall, sizeof(double) * 128), "cudaMallocHost");
+  return c->hsmall;
+}
+
+struct EigLaunch {
+  int b = 0, grid = 0;
+};
+
+// stage 4 enqueued: zero-row count, the cooperative eigensolver, the sign
+// fix, and the solver's status/Ritz values copied to pinned host memory --
+// no host synchronisation (solve_v_finish reads them after the caller's sync)
+EigLaunch solve_v_launch(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   // solver.cpp:15-62
   if (n < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_v: empty accumulator");
   if (r < 1 || r >= n) fail(RSM_ERR_INVALID_CONFIG, "solve_v: need 1 <= r < n");
@@ -754,14 +767,27 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   ck(rsmk::launch_eig(a, grid, c->stream), "cooperative eig launch");
   rsmk::launch_sign_fix(c->Vhat.as<double>(), n, (int)r, c->stream);
   c->launches += 2;
-  double w[32];
-  int istat[8];
-  double dstat[32];
-  ck(cudaMemcpyAsync(w, c->eW.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream), "D2H");
-  ck(cudaMemcpyAsync(istat, c->eI.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
-  ck(cudaMemcpyAsync(dstat, c->eD.p, sizeof(double) * 32, cudaMemcpyDeviceToHost, c->stream), "D2H");
-  ck(cudaStreamSynchronize(c->stream), "solve_v");
+  double* hs = pinned_small(c);
+  ck(cudaMemcpyAsync(hs, c->eW.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(hs + 32, c->eD.p, sizeof(double) * 32, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(hs + 64, c->eI.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  EigLaunch L;
+  L.b = b;
+  L.grid = grid;
+  return L;
+}
+
+// after the stream has been synchronised: solver statistics, the rank gate
+// and borderline flag (solver.cpp:32-60), errors raised as the reference's
+SolveVOut solve_v_finish(rsm_ctx* c, const EigLaunch& L, int64_t n, int64_t r, double tol) {
   ck(cudaGetLastError(), "eig kernels");
+  const int b = L.b, grid = L.grid;
+  const double* hs = c->hsmall;
+  double w[32], dstat[32];
+  int istat[8];
+  std::memcpy(w, hs, sizeof(double) * b);
+  std::memcpy(dstat, hs + 32, sizeof(double) * 32);
+  std::memcpy(istat, hs + 64, sizeof(int) * 8);
   c->solver_stats[0] = istat[3];
   c->solver_stats[1] = istat[4];
   c->solver_stats[2] = dstat[0];
@@ -802,6 +828,12 @@ SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   return o;
 }
 
+SolveVOut solve_v_impl(rsm_ctx* c, int64_t n, int64_t r, double tol) {
+  const EigLaunch L = solve_v_launch(c, n, r, tol);
+  ck(cudaStreamSynchronize(c->stream), "solve_v");
+  return solve_v_finish(c, L, n, r, tol);
+}
+
 // ------------------------------------------------------------------ stage 5
 struct SolveUOut {
   int64_t flagged = 0;
@@ -812,7 +844,7 @@ struct SolveUOut {
 // the residual sum and the flagged-row count; row-sharded over ranks with
 // the shards gathered into `out` (detail/row_solve.hpp:12-36, solver.cpp:64-89)
 SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& outbuf, int64_t r,
-                     const double* ugiven = nullptr) {
+                     const double* ugiven = nullptr, bool defer = false) {
   if (r < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_u: rank must be positive");
   if (r > 8) fail(RSM_ERR_INVALID_CONFIG, "device row solver supports r <= 8");
   outbuf.ensure(sizeof(double) * v.m * r);
@@ -863,13 +895,32 @@ SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& out
                            cudaMemcpyDeviceToDevice, c->stream), "D2D");
     }
   }
+  SolveUOut o;
+  if (defer) {
+    // scalars to pinned host memory; the caller synchronises and reads them
+    // with deferred_rows()
+    double* hs = pinned_small(c);
+    ck(cudaMemcpyAsync(hs + 96, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(hs + 97, c->flagged.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    return o;
+  }
   ck(cudaMemcpyAsync(&ss, c->dsum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaMemcpyAsync(&fl, c->flagged.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "solve_u");
   ck(cudaGetLastError(), "solve_u kernels");
-  SolveUOut o;
   o.flagged = fl;
   o.ss = ss;
+  return o;
+}
+
+// the stage-5 scalars of a deferred solve_rows, after the stream sync
+SolveUOut deferred_rows(rsm_ctx* c) {
+  ck(cudaGetLastError(), "solve_u kernels");
+  SolveUOut o;
+  o.ss = c->hsmall[96];
+  int fl = 0;
+  std::memcpy(&fl, c->hsmall + 97, sizeof(int));
+  o.flagged = fl;
   return o;
 }
 
@@ -900,22 +951,32 @@ void decompose_impl(rsm_ctx* c, const rsm_config* cfg, double* Uout, double* Vou
   rep->trials_attempted = h.sel.attempted;
   rep->trials_accepted = h.sel.accepted;
   rep->z = h.z;
-  SolveVOut sv = solve_v_impl(c, v.n, cfg->rank, cfg->gram_rank_tol);
-  record(c, 5);
-  rep->gram_rank = sv.gram_rank;
-  rep->borderline_rank_gate = sv.borderline;
-  SolveUOut su = solve_u_impl(c, v, cfg->rank);
-  record(c, 6);
-  rep->underdetermined_rows = su.flagged;
-  rep->e = std::sqrt(su.ss) / std::sqrt((double)c->known);  // core.cpp:35-39
-  c->oriented_T = tr;
+  // stages 4 and 5 are enqueued back to back: stage 5 needs only V-hat (on
+  // the device), so the host reads the eigensolver's status and the rank
+  // gate once, after the final synchronisation (a failed gate discards the
+  // stage-5 results and raises as the reference does)
   const int64_t r = cfg->rank;
+  const EigLaunch L = solve_v_launch(c, v.n, r, cfg->gram_rank_tol);
+  record(c, 5);
+  c->Vhat_n = 0;
+  c->U_m = 0;
+  solve_rows(c, v, c->Vhat.as<double>(), c->U, r, nullptr, /*defer=*/true);
+  record(c, 6);
   // oriented U is (v.m x r), oriented V is (v.n x r); the transpose swaps them
   double* hostU = tr ? Vout : Uout;
   double* hostV = tr ? Uout : Vout;
   if (hostU) ck(cudaMemcpyAsync(hostU, c->U.p, sizeof(double) * v.m * r, cudaMemcpyDeviceToHost, c->stream), "D2H U");
   if (hostV) ck(cudaMemcpyAsync(hostV, c->Vhat.p, sizeof(double) * v.n * r, cudaMemcpyDeviceToHost, c->stream), "D2H V");
   ck(cudaStreamSynchronize(c->stream), "decompose");
+  const SolveVOut sv = solve_v_finish(c, L, v.n, r, cfg->gram_rank_tol);
+  rep->gram_rank = sv.gram_rank;
+  rep->borderline_rank_gate = sv.borderline;
+  const SolveUOut su = deferred_rows(c);
+  c->U_m = v.m;
+  c->U_r = r;
+  rep->underdetermined_rows = su.flagged;
+  rep->e = std::sqrt(su.ss) / std::sqrt((double)c->known);  // core.cpp:35-39
+  c->oriented_T = tr;
   float ms = 0.f;
   for (int i = 0; i < 6; ++i) {
     ck(cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]), "event");
@@ -1114,9 +1175,10 @@ rsm_status rsm_ctx_destroy(rsm_ctx* c) {
                     &c->t_idx, &c->t_cm, &c->Vtrial, &c->colcnt, &c->svd_scr,
                     &c->svd_scr32, &c->P, &c->tiles, &c->G, &c->eX, &c->eY, &c->eZ, &c->ePart,
                     &c->eW, &c->eI, &c->eD, &c->Vhat, &c->U, &c->rowres, &c->flagged, &c->dsum,
-                    &c->cnt64, &c->Wq, &c->tiles8, &c->ugather};
+                    &c->cnt64, &c->Wq, &c->tiles8, &c->ugather, &c->aux0, &c->aux1, &c->aux2, &c->aux3};
   for (DevBuf* b : bufs) b->release();
   if (c->hstage) cudaFreeHost(c->hstage);
+  if (c->hsmall) cudaFreeHost(c->hsmall);
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   cudaStreamDestroy(c->stream);
