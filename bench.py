@@ -281,8 +281,16 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     ctx = rsm.Context(local, world, rank, nccl_id)
-    Yt, Wt, Y, W = gen_input(c, rank)
     m, n, r, T = c["m"], c["n"], c["r"], c["T"]
+    # a large instance (config 4: 16 GiB of values) is generated on each rank's
+    # device for the resident leg; the host copy the e2e leg uploads is pinned
+    # per rank only while all ranks together stay within HOST_PIN_BUDGET
+    host_bytes = m * n * 9
+    big = host_bytes > (4 << 30)
+    host_ok = host_bytes * world <= int(os.environ.get("HOST_PIN_BUDGET", str(96 << 30)))
+    Yt = Wt = Y = W = None
+    if host_ok:
+        Yt, Wt, Y, W = gen_input(c, rank)
     cfg = rsm.RsmConfig(rank=r, mode=rsm.Mode.M2, block=c["k"], plan=rsm.TrialPlan(T), seed=c["seed"])
     stream = torch.cuda.ExternalStream(ctx.stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
@@ -293,7 +301,10 @@ def main():
             dist.barrier()
 
     # ---- device-resident leg (value) ----
-    ctx.load_arrays(Y, W)
+    if big or Y is None:
+        ctx.generate(m, n, r, c["rho"], c["sigma"], c["seed"])  # the same instance, on the device
+    else:
+        ctx.load_arrays(Y, W)
     for _ in range(args.warmup):
         ctx.decompose(cfg, fetch=False)
     clocks = Clocks(local)
@@ -321,9 +332,7 @@ def main():
 
     # ---- end-to-end leg (public API, host buffers) ----
     e2e_times = []
-    U = np.empty((m, r))
-    V = np.empty((n, r))
-    for s in range(args.warmup + args.steps):
+    for s in range(args.warmup + args.steps if host_ok else 0):
         flush.zero_()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -338,8 +347,8 @@ def main():
     if dist is not None:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_ms = et.item() / args.steps
-    h2d = ctx.last_load_h2d_bytes()  # values + the mask as bit-packed on the host
-    d2h = (m + n) * r * 8
+    h2d = ctx.last_load_h2d_bytes() if host_ok else 0  # values + the mask as bit-packed on the host
+    d2h = (m + n) * r * 8 if host_ok else 0
 
     # ---- roofline of the dominant kernel ----
     st = np.array(stage_rows)  # select, svd, gram, reduce, solve_v, solve_u, total
@@ -408,7 +417,7 @@ def main():
     roof["traffic"] = tr
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and Y is not None:
         G = None
         try:
             # the accumulator the reference's solve_v would see (from the device harvest)
@@ -453,8 +462,11 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (reference generator streams, seed 0)",
                 "config": arm_config(c, world),
-                "e2e": {"value": T / (e2e_ms / 1e3), "unit": "submatrices/s", "ms_per_step": e2e_ms,
-                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "e2e": ({"value": T / (e2e_ms / 1e3), "unit": "submatrices/s", "ms_per_step": e2e_ms,
+                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h} if host_ok else
+                        {"value": None, "unit": "submatrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                         "skipped": f"pinned host copy per rank ({host_bytes / 2**30:.0f} GiB x {world}) exceeds "
+                                    "HOST_PIN_BUDGET"}),
                 "roofline": roof, "stages": stage_info, "cpu_baseline": cpu, "clocks": clk,
                 "gpu_launches": launches, "config1": c1,
                 "harvest": {"value": T / (float(np.sum(med[:4])) * 1e-3), "unit": "submatrices/s",
