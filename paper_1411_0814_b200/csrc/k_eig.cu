@@ -720,8 +720,7 @@ int eig_max_grid() {
   int dev = 0, sms = 0, nb = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k_eig<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_BYTES);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eig<17>, ET, DYN_BYTES);
+  nb = occupancy((const void*)k_eig<17>, ET, DYN_BYTES);
   return sms * (nb > 0 ? nb : 1);
 }
 
@@ -747,10 +746,10 @@ cudaError_t launch_eig(const EigArgs& a0, int grid, cudaStream_t s) {
   }
   void* args[] = {(void*)&a};
   if (a.b + 1 <= 12) {
-    cudaFuncSetAttribute(k_eig<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_BYTES);
+    ensure_smem((const void*)k_eig<12>, DYN_BYTES);
     return cudaLaunchCooperativeKernel((void*)k_eig<12>, dim3(grid), dim3(ET), args, dyn, s);
   }
-  cudaFuncSetAttribute(k_eig<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_BYTES);
+  ensure_smem((const void*)k_eig<17>, DYN_BYTES);
   return cudaLaunchCooperativeKernel((void*)k_eig<17>, dim3(grid), dim3(ET), args, dyn, s);
 }
 

@@ -342,7 +342,7 @@ cudaError_t launch_i8_t(const GramI8Args& a, int sms, cudaStream_t s) {
   if (!make_map(&ma, a.W, a.npad, a.Kpad, S, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&mb, a.W, a.npad, a.Kpad, S, BN, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
-  cudaFuncSetAttribute(k_gram_i8<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  ensure_smem((const void*)k_gram_i8<S>, C::SMEM);
   const int64_t nunits = (int64_t)a.ntiles * a.nk;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, sms));
   k_gram_i8<S><<<grid, NTHREADS, C::SMEM, s>>>(ma, mb, a);

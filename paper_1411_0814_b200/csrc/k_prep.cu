@@ -4,6 +4,10 @@
 // (n x mwp) for the column branch, the device transpose used when m < n
 // (rsm::MaskedMatrix::transposed, core.hpp:50-56 / solver.cpp:130-140), and
 // the observed-cell count (core.hpp:44-48).
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "rsm_internal.h"
 
 namespace rsmk {
@@ -131,6 +135,38 @@ void launch_count_bits(const uint32_t* bits, int64_t nwords, unsigned long long*
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   k_count_bits<<<(unsigned)blocks, 256, 0, s>>>(bits, nwords, out);
+}
+
+// ---- memoised launch configuration (rsm_internal.h) ----
+namespace {
+std::mutex g_cfg_mu;
+std::map<std::pair<int, const void*>, size_t> g_smem_set;
+std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
+}  // namespace
+
+void ensure_smem(const void* fn, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  size_t& cur = g_smem_set[{dev, fn}];
+  if (smem <= cur && cur != 0) return;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess) cur = smem;
+}
+
+int occupancy(const void* fn, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    auto it = g_occ.find({dev, fn, threads, smem});
+    if (it != g_occ.end()) return it->second;
+  }
+  ensure_smem(fn, smem);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem);
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  g_occ[{dev, fn, threads, smem}] = nb;
+  return nb;
 }
 
 }  // namespace rsmk

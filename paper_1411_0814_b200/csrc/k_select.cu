@@ -102,28 +102,40 @@ __global__ void k_acc_count(const int32_t* __restrict__ q, int64_t count, int32_
 // of the running accepted total (capped at T)
 __global__ void k_acc_scan(int32_t* __restrict__ blockcnt, int64_t nb, SelState* st,
                            uint64_t T) {
-  __shared__ long long part[1024];
-  const int tid = threadIdx.x;
+  __shared__ long long wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t per = (nb + blockDim.x - 1) / blockDim.x;
   const int64_t lo = tid * per, hi = (lo + per < nb) ? lo + per : nb;
-  long long s = 0;
-  for (int64_t b = lo; b < hi; ++b) s += blockcnt[b];
-  part[tid] = s;
+  long long own = 0;
+  for (int64_t b = lo; b < hi; ++b) own += blockcnt[b];
+  // block-wide inclusive scan of the per-thread sums (warp scans + a scan of
+  // the warp totals)
+  long long inc = own;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wsum[warp] = inc;
   __syncthreads();
-  if (tid == 0) {
-    long long run = 0;
-    for (int t = 0; t < (int)blockDim.x; ++t) {
-      const long long v = part[t];
-      part[t] = run;
-      run += v;
+  if (warp == 0) {
+    long long w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
     }
-    const unsigned long long before = st->acc;
-    st->acc_before = before;
-    const unsigned long long tot = before + (unsigned long long)run;
-    st->acc = tot < T ? tot : T;
+    wsum[lane] = w;
   }
   __syncthreads();
-  long long run = part[tid];
+  inc += warp > 0 ? wsum[warp - 1] : 0;
+  long long run = inc - own;  // exclusive prefix of this thread's range
+  if (tid == (int)blockDim.x - 1) {
+    const unsigned long long before = st->acc;
+    st->acc_before = before;
+    const unsigned long long tot = before + (unsigned long long)inc;
+    st->acc = tot < T ? tot : T;
+  }
   for (int64_t b = lo; b < hi; ++b) {
     const long long v = blockcnt[b];
     blockcnt[b] = (int32_t)run;  // exclusive offset within the chunk

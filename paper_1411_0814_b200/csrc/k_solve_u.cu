@@ -865,7 +865,7 @@ static void launch_solve_u_k(const SolveUArgs& a, size_t fixed, size_t per_warp,
   int w = per_warp ? (int)std::min<size_t>(wmax, (cap - fixed) / per_warp) : wmax;
   if (w < 1) w = 1;
   const size_t smem = fixed + (size_t)w * per_warp;
-  cudaFuncSetAttribute(k_solve_u<R, VSMEM, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem((const void*)k_solve_u<R, VSMEM, STAGE>, smem);
   const int64_t rows = a.row_hi - a.row_lo;
   int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
   if (blocks < 1) blocks = 1;
@@ -876,7 +876,7 @@ template <int R>
 static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);  // cached by the runtime
   constexpr int NP = (R + 1) / 2;
   const size_t head = sizeof(double) * 2 * SU_MAXW;  // mbarriers
   const size_t vbytes = sizeof(double) * 2 * NP * (size_t)a.n;
@@ -906,10 +906,10 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
         int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
         if (blocks < 1) blocks = 1;
         if (walk) {
-          cudaFuncSetAttribute(k_solve_u_fused<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          ensure_smem((const void*)k_solve_u_fused<R, true>, smem);
           k_solve_u_fused<R, true><<<(unsigned)blocks, w * 32, smem, s>>>(a);
         } else {
-          cudaFuncSetAttribute(k_solve_u_fused<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          ensure_smem((const void*)k_solve_u_fused<R, false>, smem);
           k_solve_u_fused<R, false><<<(unsigned)blocks, w * 32, smem, s>>>(a);
         }
         return;
@@ -939,8 +939,38 @@ void launch_solve_u(const SolveUArgs& a, cudaStream_t s) {
   }
 }
 
+// two-level deterministic sum for long vectors: SUMP blocks sum fixed
+// contiguous chunks (fixed strided order + tree), one thread adds the SUMP
+// partials in order
+constexpr int SUMP = 64;
+__global__ void k_sum_part(const double* __restrict__ v, int64_t n, double* __restrict__ part) {
+  __shared__ double red[256];
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+  double s = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += v[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+__global__ void k_sum_final(const double* __restrict__ part, int np, double* __restrict__ out) {
+  double s = 0.0;
+  for (int i = 0; i < np; ++i) s += part[i];
+  *out = s;
+}
+
+// out[0] = sum of v[0..n); out must have room for 2 + SUMP doubles (partials)
 void launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s) {
-  k_sum_rows<<<1, 1024, 0, s>>>(v, n, out);
+  if (n <= 32768) {
+    k_sum_rows<<<1, 1024, 0, s>>>(v, n, out);
+    return;
+  }
+  k_sum_part<<<SUMP, 256, 0, s>>>(v, n, out + 2);
+  k_sum_final<<<1, 1, 0, s>>>(out + 2, SUMP, out);
 }
 
 }  // namespace rsmk

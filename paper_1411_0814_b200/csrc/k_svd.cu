@@ -997,9 +997,7 @@ bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s) {
   const int64_t Tl = a.t_hi - a.t_lo;
 #define RSM_SVDW(KK)                                                                                \
   case KK: {                                                                                        \
-    cudaFuncSetAttribute(k_svd_warp<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
-    int occ = 0;                                                                                    \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_svd_warp<KK>, SVDW_WARPS * 32, smem);     \
+    int occ = occupancy((const void*)k_svd_warp<KK>, SVDW_WARPS * 32, smem);                       \
     if (occ < 1) occ = 1;                                                                           \
     const int64_t grid = std::min<int64_t>((Tl + SVDW_WARPS - 1) / SVDW_WARPS, (int64_t)sms * occ); \
     k_svd_warp<KK><<<(unsigned)std::max<int64_t>(grid, 1), SVDW_WARPS * 32, smem, s>>>(a);          \
@@ -1021,24 +1019,17 @@ size_t svd_smem_fixed(int64_t cmw, bool m2) {
 
 void launch_svd(const SvdArgs& a, bool m2, int grid, size_t smem, cudaStream_t s) {
   if (m2) {
-    cudaFuncSetAttribute(k_svd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem((const void*)k_svd<true>, smem);
     k_svd<true><<<grid, svd_cta_threads<true>(), smem, s>>>(a);
   } else {
-    cudaFuncSetAttribute(k_svd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem((const void*)k_svd<false>, smem);
     k_svd<false><<<grid, svd_cta_threads<false>(), smem, s>>>(a);
   }
 }
 
 int svd_occupancy(bool m2, size_t smem) {
-  int nb = 0;
-  if (m2) {
-    cudaFuncSetAttribute(k_svd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_svd<true>, svd_cta_threads<true>(), smem);
-  } else {
-    cudaFuncSetAttribute(k_svd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_svd<false>, svd_cta_threads<false>(), smem);
-  }
-  return nb;
+  return m2 ? occupancy((const void*)k_svd<true>, svd_cta_threads<true>(), smem)
+            : occupancy((const void*)k_svd<false>, svd_cta_threads<false>(), smem);
 }
 
 }  // namespace rsmk

@@ -851,7 +851,7 @@ SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& out
   double* out = outbuf.as<double>();
   c->rowres.ensure(sizeof(double) * v.m);
   c->flagged.ensure(sizeof(int) * 2);
-  c->dsum.ensure(sizeof(double) * 2);
+  c->dsum.ensure(sizeof(double) * (2 + 64));  // + partials of launch_sum_rows
   ck(cudaMemsetAsync(c->flagged.p, 0, sizeof(int) * 2, c->stream), "memset");
   int64_t lo, hi;
   rsm_shard_range(v.m, c->world, c->rank, &lo, &hi);
@@ -1493,7 +1493,7 @@ static rsm_status residual_ss(const double* values, const uint8_t* mask, int64_t
     c->U.ensure(sizeof(double) * m * r);
     c->Vhat.ensure(sizeof(double) * n * r);
     c->rowres.ensure(sizeof(double) * m);
-    c->dsum.ensure(sizeof(double) * 2);
+    c->dsum.ensure(sizeof(double) * (2 + 64));  // + partials of launch_sum_rows
     ck(cudaMemcpyAsync(c->U.p, U, sizeof(double) * m * r, cudaMemcpyHostToDevice, c->stream), "H2D U");
     ck(cudaMemcpyAsync(c->Vhat.p, V, sizeof(double) * n * r, cudaMemcpyHostToDevice, c->stream), "H2D V");
     c->U_m = 0;

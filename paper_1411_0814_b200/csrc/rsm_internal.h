@@ -9,6 +9,14 @@
 
 namespace rsmk {
 
+// Host-side launch configuration, memoised per (kernel, block, dynamic smem):
+// cudaFuncSetAttribute / cudaOccupancy* cost microseconds of host time, and
+// after the selection's host sync every microsecond of it is GPU idle time.
+// ensure_smem raises a kernel's dynamic-shared-memory limit once (only ever
+// upwards); occupancy returns blocks per SM for (kernel, threads, smem).
+void ensure_smem(const void* fn, size_t smem);
+int occupancy(const void* fn, int threads, size_t smem);
+
 // device-resident selection state (stage 1 compaction)
 struct SelState {
   unsigned long long acc;             // accepted so far, capped at T
