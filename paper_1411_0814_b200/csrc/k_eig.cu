@@ -650,10 +650,38 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     if (acut <= 0.0) acut = 1e-6 * ub;
   }
   if (status == 1 && maxres <= 1e-9 * ub) status = 0;  // converged to a looser bound
-  // ---- outputs ----
-  for (int q = tid; q < nr * r; q += ET) {
-    const int lr = q / r, j = q % r;
-    a.V[(int64_t)(row_lo + lr) * r + j] = Xo[lr * ld + j];
+  // ---- outputs, sign-fixed (solver.cpp:47-60): each column's largest-
+  // magnitude entry made positive, the first index winning ties. Per-CTA
+  // candidates (signed value, row) -> partials, one grid sync, every CTA
+  // scans the candidates in CTA order (rows ascend with the CTA index) ----
+  {
+    __shared__ double flip[BMAX];
+    if (tid < r) {
+      double best = -1.0, val = 0.0;
+      int arg = row_lo;
+      for (int lr = 0; lr < nr; ++lr) {
+        const double x = Xo[lr * ld + tid];
+        if (fabs(x) > best) { best = fabs(x); val = x; arg = row_lo + lr; }
+      }
+      *pslot(a, buf, pw, tid) = nr > 0 ? val : 0.0;
+      *pslot(a, buf, pw, r + tid) = nr > 0 ? (double)arg : -1.0;
+    }
+    grid.sync();
+    if (tid < r) {
+      const int nc = (int)gridDim.x;
+      double best = -1.0, val = 0.0;
+      for (int cta = 0; cta < nc; ++cta) {
+        const double x = a.part[((size_t)buf * pw + tid) * nc + cta];
+        const double id = a.part[((size_t)buf * pw + r + tid) * nc + cta];
+        if (id >= 0.0 && fabs(x) > best) { best = fabs(x); val = x; }
+      }
+      flip[tid] = val < 0.0 ? -1.0 : 1.0;
+    }
+    __syncthreads();
+    for (int q = tid; q < nr * r; q += ET) {
+      const int lr = q / r, j = q % r;
+      a.V[(int64_t)(row_lo + lr) * r + j] = flip[j] * Xo[lr * ld + j];
+    }
   }
   if (blockIdx.x == 0 && tid == 0) {
     for (int j = 0; j < b; ++j) a.w[j] = sh.theta[j];

@@ -764,9 +764,8 @@ EigLaunch solve_v_launch(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   a.zero_rows = c->eI.as<int>() + 7;
   rsmk::launch_zero_rows(a.G, n, a.cnt, c->eI.as<int>() + 7, c->stream);
   ++c->launches;
-  ck(rsmk::launch_eig(a, grid, c->stream), "cooperative eig launch");
-  rsmk::launch_sign_fix(c->Vhat.as<double>(), n, (int)r, c->stream);
-  c->launches += 2;
+  ck(rsmk::launch_eig(a, grid, c->stream), "cooperative eig launch");  // sign fix included
+  c->launches += 1;
   double* hs = pinned_small(c);
   ck(cudaMemcpyAsync(hs, c->eW.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaMemcpyAsync(hs + 32, c->eD.p, sizeof(double) * 32, cudaMemcpyDeviceToHost, c->stream), "D2H");
