@@ -725,7 +725,11 @@ EigLaunch solve_v_launch(rsm_ctx* c, int64_t n, int64_t r, double tol) {
   }
   const int ld = b + 1;
   const int maxgrid = rsmk::eig_max_grid();
-  int grid = (int)std::min<int64_t>(maxgrid, std::max<int64_t>(1, ceil_div(n, 8)));
+  static const int rows_min = [] {
+    const char* e = getenv("RSM_EIG_ROWS");  // rows per CTA (experiments)
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  int grid = (int)std::min<int64_t>(maxgrid, std::max<int64_t>(1, ceil_div(n, rows_min)));
   const int rows_per_cta = (int)ceil_div(n, grid);
   grid = (int)ceil_div(n, rows_per_cta);
   const int pw = rsmk::eig_part_width(b);
