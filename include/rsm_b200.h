@@ -200,8 +200,21 @@ rsm_status rsm_als(const double* values, const uint8_t* mask, int64_t m, int64_t
 rsm_status rsm_harvest_gram(const double* values, const uint8_t* mask, int64_t m, int64_t n,
                             const rsm_trial_params* p, uint64_t trials, double* G,
                             uint64_t* attempted, uint64_t* accepted, uint64_t* z);
+/* Minor eigenvectors (solver.cpp:15-62) by Chebyshev-filtered subspace
+ * iteration, not the full dsyev spectrum: the rank-gate threshold uses a
+ * power-iteration estimate of lambda_max (a lower bound after >= 8 matvecs),
+ * so gram_rank and borderline can differ from the reference only for an
+ * eigenvalue within that estimate's error of tol * lambda_max. */
 rsm_status rsm_solve_v(const double* G, int64_t n, int64_t r, double tol, double* V,
                        int64_t* gram_rank, int32_t* borderline);
+/* Row solves (solver.cpp:64-89). Deviation from the reference's COD: a row's
+ * rank is decided on its r x r normal matrix (Cholesky pivot <= 1e-10 of the
+ * largest diagonal -> eigen-decomposition pseudo-inverse, rank = eigenvalues
+ * above 64 eps of the largest) instead of Eigen's column-pivoted QR of the
+ * gathered basis rows. Exactly deficient rows (fewer than r observations, a
+ * rank-deficient V_O) are flagged and solved at minimum norm as the
+ * reference does; rows with cond(V_O) between ~1e5 and ~1e15 can be
+ * classified differently. */
 rsm_status rsm_solve_u(const double* values, const uint8_t* mask, int64_t m, int64_t n,
                        const double* V, int64_t r, double* U, int64_t* underdetermined_rows);
 rsm_status rsm_masked_residual_norm(const double* values, const uint8_t* mask, int64_t m,
