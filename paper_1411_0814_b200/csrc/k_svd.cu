@@ -211,6 +211,26 @@ __device__ __noinline__ void cta_gather_cols(const double* __restrict__ Y, int64
 template <bool M2>
 constexpr int svd_cta_threads() { return M2 ? 128 : 512; }
 
+template <int K>
+__device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C);
+
+__device__ __forceinline__ bool it_fast(const int* flags) { return flags[3] != 0; }
+
+// runtime-K dispatch of topr_basis_small (row-branch CTA kernel, K <= 9)
+__device__ __noinline__ bool topr_basis_rt(int K, const double* Gsm, double* C) {
+  switch (K) {
+    case 2: return topr_basis_small<2>(Gsm, C);
+    case 3: return topr_basis_small<3>(Gsm, C);
+    case 4: return topr_basis_small<4>(Gsm, C);
+    case 5: return topr_basis_small<5>(Gsm, C);
+    case 6: return topr_basis_small<6>(Gsm, C);
+    case 7: return topr_basis_small<7>(Gsm, C);
+    case 8: return topr_basis_small<8>(Gsm, C);
+    case 9: return topr_basis_small<9>(Gsm, C);
+    default: return false;
+  }
+}
+
 template <bool M2>
 __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -373,6 +393,21 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
         }
       }
       __syncthreads();
+      if (M2 && it == 0 && a.fast_basis && a.rex == K - 1 && K <= 9) {
+        // r = k - 1: an orthonormal basis of the top-r subspace straight from
+        // the Gram (topr_basis_small: one lane, no Jacobi sweeps); its
+        // coefficients C (K x r) go to W, the output is V = S^T C
+        if (tid == 0) {
+          int p = 0;
+          for (int i = 0; i < K; ++i)
+            for (int j = i; j < K; ++j) Tmp[p++] = gram[i * KMAX + j];
+          flags[3] = topr_basis_rt(K, Tmp, W) ? 1 : 0;
+        }
+        __syncthreads();
+        if (flags[3]) break;
+      } else if (it == 0 && tid == 0) {
+        flags[3] = 0;
+      }
       if (warp == 0) {
         int big = 0;
         for (int e = lane; e < K * K; e += 32) {
@@ -435,8 +470,9 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
       }
       __syncthreads();
     }
+    const bool fast = M2 && it_fast(flags);
     // descending singular values, ties by index (stable)
-    if (tid == 0) {
+    if (tid == 0 && !fast) {
       for (int i = 0; i < K; ++i) ord[i] = i;
       for (int i = 1; i < K; ++i) {
         const int x = ord[i];
@@ -469,14 +505,24 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
           cc[u] = c;
         }
         for (int i = 0; i < rex; ++i) {
-          const int o = ord[i];
-          const double sg = M2 ? sig[o] : 0.0;
-          const double inv = sg > 0.0 ? 1.0 / sg : 0.0;
           double v[4];
+          if (fast) {  // V = S^T C
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            v[u] = 0.0;
-            if (cc[u] >= 0) v[u] = M2 ? vec[o * Lp + cc[u]] * inv : Vacc[cc[u] * KMAX + o];
+            for (int u = 0; u < 4; ++u) {
+              double t = 0.0;
+              if (cc[u] >= 0)
+                for (int k = 0; k < K; ++k) t = fma(vec[k * Lp + cc[u]], W[k * rex + i], t);
+              v[u] = t;
+            }
+          } else {
+            const int o = ord[i];
+            const double sg = M2 ? sig[o] : 0.0;
+            const double inv = sg > 0.0 ? 1.0 / sg : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              v[u] = 0.0;
+              if (cc[u] >= 0) v[u] = M2 ? vec[o * Lp + cc[u]] * inv : Vacc[cc[u] * KMAX + o];
+            }
           }
           emit_slices4(a.S, a.Wq, a.Kpad, a.npad, tl * rex + i, j0, v[0], v[1], v[2], v[3]);
         }
@@ -500,7 +546,11 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
           for (int h = 0; h < 2; ++h) {
             const int i = 2 * p + h;
             if (i < rex) {
-              if (M2) {
+              if (M2 && fast) {
+                double t = 0.0;
+                for (int k = 0; k < K; ++k) t = fma(vec[k * Lp + c], W[k * rex + i], t);
+                v[h] = t;
+              } else if (M2) {
                 // V_top rows over the column support: rotated_row_i[c] / sigma_i
                 const int o = ord[i];
                 const double sg = sig[o];
@@ -671,6 +721,12 @@ __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C) {
 }
 
 constexpr int SVDW_WARPS = 4;
+// largest k whose warp kernel takes the top-r basis path (r = k - 1) before
+// falling back to one-sided Jacobi (config 4: k = 9)
+#ifndef RSM_FASTK
+#define RSM_FASTK 9
+#endif
+constexpr int FASTK = RSM_FASTK;
 
 template <int K>
 __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
@@ -770,7 +826,7 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     for (int it = 0;; ++it) {
 #pragma unroll
       for (int p = 0; p < P; ++p) g[p] = warp_sum(g[p]);
-      if constexpr (K <= 6) {
+      if constexpr (K <= FASTK) {
         if (it == 0 && rex == K - 1 && a.fast_basis) {
           // r = k - 1: an orthonormal basis of the top-r subspace straight
           // from the Gram (see topr_basis_small), no Jacobi rotations
@@ -842,7 +898,7 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
       }
       __syncwarp();
     }
-    if constexpr (K <= 6) {
+    if constexpr (K <= FASTK) {
       if (fast) {
         // V = S^T C (K x r coefficients in Ws), expanded layout
         constexpr int R1 = K - 1;

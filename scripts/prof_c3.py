@@ -12,9 +12,11 @@ shapes = {"c3": (131072, 1024, 4, 0.8, 1e-3, 5, 16384), "c1": (2000, 200, 3, 0.8
 m, n, r, rho, sigma, k, T = shapes[cfgname]
 seed = 1 if cfgname == "c2" else 0
 mode = rsm.Mode.M1 if cfgname == "c2" else rsm.Mode.M2
-M = rsm.generate(m, n, r, rho, sigma, seed)
 ctx = rsm.Context(0)
-ctx.load(M)
+if os.environ.get("DEVGEN", "1" if cfgname == "c4" else "0") == "1":
+    ctx.generate(m, n, r, rho, sigma, seed)  # device generator (config 4: 17 GB)
+else:
+    ctx.load(rsm.generate(m, n, r, rho, sigma, seed))
 cfg = rsm.RsmConfig(rank=r, mode=mode, block=k, plan=rsm.TrialPlan(T), seed=seed)
 for i in range(int(os.environ.get("REPS", "2"))):
     t0 = time.time()
