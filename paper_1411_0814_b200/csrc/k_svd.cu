@@ -504,17 +504,29 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
           }
           cc[u] = c;
         }
+        if (M2 && fast) {
+          // V = S^T C: the 4 columns' K values read once, then every output
+          // vector from registers (K <= 9 here)
+          double xs[4][9];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < 9; ++k) xs[u][k] = (k < K && cc[u] >= 0) ? vec[k * Lp + cc[u]] : 0.0;
+          for (int i = 0; i < rex; ++i) {
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+              const double w = k < K ? W[k * rex + i] : 0.0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) v[u] = fma(xs[u][k], w, v[u]);
+            }
+            emit_slices4(a.S, a.Wq, a.Kpad, a.npad, tl * rex + i, j0, v[0], v[1], v[2], v[3]);
+          }
+          continue;
+        }
         for (int i = 0; i < rex; ++i) {
           double v[4];
-          if (fast) {  // V = S^T C
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              double t = 0.0;
-              if (cc[u] >= 0)
-                for (int k = 0; k < K; ++k) t = fma(vec[k * Lp + cc[u]], W[k * rex + i], t);
-              v[u] = t;
-            }
-          } else {
+          {
             const int o = ord[i];
             const double sg = M2 ? sig[o] : 0.0;
             const double inv = sg > 0.0 ? 1.0 / sg : 0.0;
