@@ -173,6 +173,7 @@ __global__ void k_acc_emit(const int32_t* __restrict__ q, const int32_t* __restr
   t_q[pos] = qi;
   for (int t = 0; t < block; ++t) t_idx[pos * block + t] = idx[i * block + t];
   atomicMax(&st->qmax, qi);
+  atomicAdd(&st->qsum, (unsigned long long)qi);  // integer: order-independent
   if (pos == T - 1) st->attempted_done = a0 + (uint64_t)i + 1;
 }
 

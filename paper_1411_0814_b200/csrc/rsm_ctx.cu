@@ -103,6 +103,7 @@ struct View {
 struct SelResult {
   uint64_t attempted = 0, accepted = 0;
   int qmax = 0;
+  uint64_t qsum = 0;  // sum of the accepted trials' survivor counts
 };
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -445,6 +446,7 @@ SelResult select_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint
   r.attempted = attempted;
   r.accepted = acc;
   r.qmax = hs.qmax;
+  r.qsum = hs.qsum;
   return r;
 }
 
@@ -504,11 +506,9 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   const int64_t npad = ceil_div(n, 128) * 128;
   const int64_t cmw = npad / 32;
   const int K = (int)p->block;
-  // per-trial ell / top-vector count (harvest.cpp:44-50)
-  std::vector<int32_t> hq(Tacc > 0 ? Tacc : 1);
-  if (Tacc > 0)
-    ck(cudaMemcpyAsync(hq.data(), c->t_q.p, sizeof(int32_t) * Tacc, cudaMemcpyDeviceToHost, c->stream), "D2H q");
-  ck(cudaStreamSynchronize(c->stream), "sync");
+  // per-trial ell / top-vector count (harvest.cpp:44-50); the selection's
+  // state already carries the survivor-count sum and maximum, so no per-trial
+  // counts come back to the host
   int rex;
   if (m2) {
     rex = (int)p->rank;
@@ -525,7 +525,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   rsm_shard_range(Tacc, c->world, c->rank, &t_lo, &t_hi);
   const int64_t Tl = t_hi - t_lo;
   uint64_t z = 0;
-  for (int64_t t = 0; t < Tacc; ++t) z += m2 ? (uint64_t)(hq[t] - rex) : (uint64_t)p->ell;
+  z = m2 ? out.sel.qsum - (uint64_t)Tacc * (uint64_t)rex : (uint64_t)Tacc * (uint64_t)p->ell;
   out.z = z;
   c->G.ensure(sizeof(double) * n * n);
   c->colcnt.ensure(sizeof(int) * npad);
@@ -579,7 +579,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     if (i8) c->Wq.ensure((size_t)S8 * Kpad0 * npad);
     else c->Vtrial.ensure((size_t)tbytes * chunk);
     int64_t Lmax = m2 ? out.sel.qmax : 0;
-    if (!m2) for (int64_t t = t_lo; t < t_hi; ++t) Lmax = std::max<int64_t>(Lmax, hq[t]);
+    if (!m2) Lmax = out.sel.qmax;  // the largest survivor count over all accepted trials
     const int64_t Lpad = std::max<int64_t>(2, (Lmax + 1) & ~int64_t(1));
     const size_t fixed = rsmk::svd_smem_fixed(cmw, m2);
     const size_t vecb = sizeof(double) * (size_t)K * Lpad;

@@ -24,6 +24,7 @@ struct SelState {
   unsigned long long attempted_done;  // attempt id + 1 of the T-th acceptance, 0 = not yet
   int qmax;                           // largest survivor count among accepted trials
   int pad;
+  unsigned long long qsum;            // sum of the accepted trials' survivor counts (z)
 };
 
 struct SvdArgs {
