@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     // cells' outer products (walking only the hidden bits), which saves most
     // of the r(r+1)/2 FMAs per cell
     bool dense = false;
-    if constexpr (R > 4) dense = 2 * (int64_t)warp_sum_int(cnt) >= n;
+    if constexpr (R > 4) dense = !a.Apre && 2 * (int64_t)warp_sum_int(cnt) >= n;
+    const bool needA = !a.Apre;  // else the normal matrix comes from the tensor cores
     // branchless (so the loads of consecutive columns pipeline): a hidden
     // cell's basis row is scaled by 0 and its value selected away, so the NaN
     // stored there never enters arithmetic
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
       double v[R];
       vload(c, v);
       const double yc = k ? yraw : 0.0;
-      if (!dense) {
+      if (!dense && needA) {
         const double kf = k ? 1.0 : 0.0;
         double t[R];
 #pragma unroll
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(R <= 4 ? SU_MAXW * 32 : 384) k_solve_u(SolveUA
     };
     double A[NA], bv[R];
 #pragma unroll
-    for (int p = 0; p < NA; ++p) A[p] = dense ? Aall[p] - total(p) : total(p);
+    for (int p = 0; p < NA; ++p) A[p] = a.Apre ? a.Apre[row * NA + p] : (dense ? Aall[p] - total(p) : total(p));
 #pragma unroll
     for (int i = 0; i < R; ++i) bv[i] = total(NA + i);
     const int nj = (int)total(NA + R);
@@ -643,14 +644,16 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u, double& ss_prev, int64_t frow, int njr,
                     bool hidr) -> bool {
     int cnt = 0;
-    if (!WALK) {
+    if (a.Apre) {  // normal matrices from the tensor cores: only the count here
+      for (int w = lane; w < nwn; w += 32) cnt += __popc(wd[w]);
+    } else if (!WALK) {
       if (hidr) {
 #pragma unroll
         for (int p = 0; p < NA; ++p) acc[p] += lane == 0 ? Aall[p] : 0.0;
       }
       cnt = lane == 0 ? njr : 0;
     }
-    for (int w = lane; WALK && w < nwn; w += 32) {
+    for (int w = lane; WALK && !a.Apre && w < nwn; w += 32) {
       const int rem = (int)(n - (int64_t)w * 32);
       const unsigned valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
       const unsigned obs = wd[w] & valid;
@@ -692,7 +695,7 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
     warp_reduce_halving<NV>(acc, lane);
     double A[NA], bv[R];
 #pragma unroll
-    for (int p = 0; p < NA; ++p) A[p] = warp_total<NV>(acc, p);
+    for (int p = 0; p < NA; ++p) A[p] = a.Apre ? a.Apre[frow * NA + p] : warp_total<NV>(acc, p);
 #pragma unroll
     for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, NA + i);
     const int nj = (int)warp_total<NV>(acc, NA + R);

@@ -162,6 +162,7 @@ struct rsm_ctx {
   DevBuf sel_idx, sel_q, blockcnt, selstate, t_attempt, t_q, t_idx, t_cm, Vtrial,
       colcnt, svd_scr, svd_scr32, P, tiles, G, eX, eY, eZ, ePart, eW, eI, eD, Vhat, U, rowres,
       flagged, dsum, cnt64, Wq, tiles8, ugather;
+  DevBuf Apre, Bq;  // stage 5's tensor-core normal matrices and the basis-product digits
   DevBuf aux0, aux1, aux2, aux3;  // per-call utilities (rsm_sample, rsm_small_singular_vectors, rsm_gram_update)
   double* hsmall = nullptr;  // pinned host staging: eig stats [0,96), stage-5 scalars [96,100)
   int64_t tiles_n = -1;
@@ -847,7 +848,7 @@ struct SolveUOut {
 // the residual sum and the flagged-row count; row-sharded over ranks with
 // the shards gathered into `out` (detail/row_solve.hpp:12-36, solver.cpp:64-89)
 SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& outbuf, int64_t r,
-                     const double* ugiven = nullptr, bool defer = false) {
+                     const double* ugiven = nullptr, bool defer = false, bool unit_basis = false) {
   if (r < 1) fail(RSM_ERR_INVALID_CONFIG, "solve_u: rank must be positive");
   if (r > 8) fail(RSM_ERR_INVALID_CONFIG, "device row solver supports r <= 8");
   outbuf.ensure(sizeof(double) * v.m * r);
@@ -868,6 +869,28 @@ SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& out
   a.flagged = c->flagged.as<int>();
   a.r = (int)r;
   a.Ugiven = ugiven;
+  // the rows' normal matrices on the tensor cores (k_normal_i8.cu) unless
+  // RSM_NORMAL_TC=0; the row kernels then only form V_O^T y and the residual.
+  // Only for a basis with entries in [-1, 1] (decompose's orthonormal V-hat:
+  // the digit split of v_i v_j assumes |v_i v_j| <= 1); ALS and caller-given
+  // bases take the FP64 normal-matrix path.
+  static const bool normal_tc = [] {
+    const char* e = getenv("RSM_NORMAL_TC");
+    return !(e && atoi(e) == 0);
+  }();
+  if (normal_tc && unit_basis && hi > lo && v.n >= 32) {
+    const int na = (int)(r * (r + 1) / 2);
+    c->Apre.ensure(sizeof(double) * v.m * na);
+    c->Bq.ensure(rsmk::normal_i8_bq_bytes((int)r, v.n));
+    rsmk::NormalI8Args na8{};
+    na8.bits = v.bitsR; na8.m = v.m; na8.n = v.n; na8.nwp = v.nwp;
+    na8.V = basis; na8.r = (int)r;
+    na8.Bq = c->Bq.as<int8_t>();
+    na8.Apre = c->Apre.as<double>();
+    ck(rsmk::launch_normal_i8(na8, c->sms, c->stream), "normal matrices (tcgen05) launch");
+    c->launches += 2;
+    a.Apre = c->Apre.as<double>();
+  }
   if (hi > lo) {
     rsmk::launch_solve_u(a, c->stream);
     rsmk::launch_sum_rows(c->rowres.as<double>() + lo, hi - lo, c->dsum.as<double>(), c->stream);
@@ -963,7 +986,7 @@ void decompose_impl(rsm_ctx* c, const rsm_config* cfg, double* Uout, double* Vou
   record(c, 5);
   c->Vhat_n = 0;
   c->U_m = 0;
-  solve_rows(c, v, c->Vhat.as<double>(), c->U, r, nullptr, /*defer=*/true);
+  solve_rows(c, v, c->Vhat.as<double>(), c->U, r, nullptr, /*defer=*/true, /*unit_basis=*/true);
   record(c, 6);
   // oriented U is (v.m x r), oriented V is (v.n x r); the transpose swaps them
   double* hostU = tr ? Vout : Uout;
@@ -1178,7 +1201,8 @@ rsm_status rsm_ctx_destroy(rsm_ctx* c) {
                     &c->t_idx, &c->t_cm, &c->Vtrial, &c->colcnt, &c->svd_scr,
                     &c->svd_scr32, &c->P, &c->tiles, &c->G, &c->eX, &c->eY, &c->eZ, &c->ePart,
                     &c->eW, &c->eI, &c->eD, &c->Vhat, &c->U, &c->rowres, &c->flagged, &c->dsum,
-                    &c->cnt64, &c->Wq, &c->tiles8, &c->ugather, &c->aux0, &c->aux1, &c->aux2, &c->aux3};
+                    &c->cnt64, &c->Wq, &c->tiles8, &c->ugather, &c->aux0, &c->aux1, &c->aux2, &c->aux3,
+                    &c->Apre, &c->Bq};
   for (DevBuf* b : bufs) b->release();
   if (c->hstage) cudaFreeHost(c->hstage);
   if (c->hsmall) cudaFreeHost(c->hsmall);

@@ -118,6 +118,7 @@ struct SolveUArgs {
   int r;
   const double* Ugiven;  // non-null: rows' solutions given (m x r), only the residual pass
                          // counts (masked_residual_norm through the stage-5 arithmetic)
+  const double* Apre;    // non-null: rows' packed normal matrices (m x r(r+1)/2, k_normal_i8.cu)
 };
 
 // rsm_ctx.cu: message for rsm_last_error(NULL) from host-only entry points
@@ -174,6 +175,18 @@ size_t small_svd_scratch_doubles(int p, int q);
 void launch_small_svd(const double* S, int p, int q, int ell, double* scratch, double* zeta, double* sv,
                       cudaStream_t s);
 void launch_gram_update(double* G, int64_t n, const double* X, int64_t nvec, const double* G2, cudaStream_t s);
+// k_normal_i8.cu: stage 5's normal matrices on the tensor cores
+struct NormalI8Args {
+  const uint32_t* bits;  // m x nwp row-major mask words
+  int64_t m, n, nwp;
+  const double* V;       // n x r basis
+  int r;
+  int8_t* Bq;            // normal_i8_bq_bytes(r, n) scratch: the basis products' int8 digits
+  double* Apre;          // m x r(r+1)/2 packed upper normal matrices (output)
+  int b_resident;        // set by the launcher: B loaded once per CTA
+};
+size_t normal_i8_bq_bytes(int r, int64_t n);
+cudaError_t launch_normal_i8(const NormalI8Args& a, int sms, cudaStream_t s);
 // k_solve_u.cu
 void launch_solve_u(const SolveUArgs& a, cudaStream_t s);
 void launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s);
