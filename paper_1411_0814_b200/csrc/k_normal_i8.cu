@@ -44,8 +44,10 @@ namespace {
 
 constexpr int NS = 7;     // digits per q value
 constexpr int KS = 32;    // K per MMA (kind::i8)
+constexpr int KSUB = 4;   // MMAs per ring stage
+constexpr int SK = KS * KSUB;  // K (mask columns) per stage
 constexpr int NTH = 448;
-constexpr int NST = 8;    // ring stages
+constexpr int NST = 4;    // ring stages
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t* bar, unsigned count) {
@@ -129,16 +131,16 @@ __global__ void __launch_bounds__(NTH, 1)
     k_normal_i8(const __grid_constant__ CUtensorMap tmB, NormalI8Args a) {
   constexpr int NA = R * (R + 1) / 2;
   constexpr int N = 128 * HQ;
-  constexpr int A_STAGE = KS * 128;      // 4 KB
-  constexpr int B_STAGE = KS * 128 * HQ;  // 4 KB per half
+  constexpr int A_STAGE = 128 * SK;       // 128 rows x 128 K-bytes (16 KB)
+  constexpr int B_STAGE = SK * 128 * HQ;  // 128 K-rows x N bytes, [HQ][128][128]
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = sm;
   uint8_t* smB = sm + NST * A_STAGE;
-  // B resident (all K-steps loaded once) when it fits, else streamed per stage
+  // B resident (every K-stage loaded once) when it fits, else a ring
   const bool res = a.b_resident != 0;
-  const int nk0 = (int)((a.n + KS - 1) / KS);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smB + (res ? nk0 : NST) * B_STAGE);
+  const int nks = (int)((a.n + SK - 1) / SK);  // K-stages per tile
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + (res ? nks : NST) * B_STAGE);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;  // [2]: two TMEM accumulators, tiles alternate
   uint64_t* tempty = tfull + 2;   // [2]
@@ -146,7 +148,6 @@ __global__ void __launch_bounds__(NTH, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bres + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (a.m + 127) / 128;
-  const int nk = (int)((a.n + KS - 1) / KS);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mb_init(full + s, res ? 4 : 5);  // 4 builder warps (+ the B producer's expect_tx when streamed)
@@ -170,46 +171,40 @@ __global__ void __launch_bounds__(NTH, 1)
   const uint32_t tmem = *tslot;
 
   if (warp < 8) {
-    // ---------------- A builders (two groups of four warps, alternate K-steps) ----------------
+    // ---------------- A builders: two groups of four warps, alternate stages ----------------
     const int grp = warp >> 2, qtr = warp & 3;
-    int64_t gk0 = 0;  // global K-step index of the tile's first step (shared ring order)
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, gk0 += nk) {
+    int64_t gs0 = 0;  // global stage index of the tile's first stage (the ring's order)
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, gs0 += nks) {
       const int64_t row = tile * 128 + 32 * qtr + lane;
       const bool rv = row < a.m;
-      // the lane's row words in batches of 8 (two 16-byte loads; rows are nwp
-      // words, nwp a multiple of 4), the next batch in flight while this one
-      // is used (zero past n / m)
+      // four mask words per stage (one 16-byte load; rows are nwp = 4 nks words)
       const uint4* rw = reinterpret_cast<const uint4*>(a.bits + (rv ? row : 0) * a.nwp);
-      auto ld4 = [&](int w) { return (rv && w < a.nwp) ? __ldg(rw + (w >> 2)) : make_uint4(0, 0, 0, 0); };
-      uint4 n0 = ld4(0), n1 = ld4(4), c0w = n0, c1w = n1;
-      // this group's first step in the tile
-      for (int k = (int)((grp - (gk0 & 1)) & 1); k < nk; k += 2) {
-        if ((k & 7) < 2) {  // the group's first step in a batch of 8 words
-          c0w = n0;
-          c1w = n1;
-          const int nb = (k & ~7) + 8;
-          n0 = ld4(nb);
-          n1 = ld4(nb + 4);
-        }
-        const int q = k & 7;
-        const uint32_t word = q == 0 ? c0w.x : q == 1 ? c0w.y : q == 2 ? c0w.z : q == 3 ? c0w.w
-                            : q == 4 ? c1w.x : q == 5 ? c1w.y : q == 6 ? c1w.z : c1w.w;
-        const int64_t gk = gk0 + k;
-        const int st = (int)(gk % NST);
-        const unsigned ph = (unsigned)((gk / NST) & 1);
+      int ks = (int)((grp - (gs0 & 1)) & 1);  // this group's first stage of the tile
+      uint4 nx = (rv && ks < nks) ? __ldg(rw + ks) : make_uint4(0, 0, 0, 0);
+      const int ar = 32 * qtr + lane;
+      for (; ks < nks; ks += 2) {
+        const uint4 w4 = nx;
+        nx = (rv && ks + 2 < nks) ? __ldg(rw + ks + 2) : make_uint4(0, 0, 0, 0);
+        const int64_t gs = gs0 + ks;
+        const int st = (int)(gs % NST);
+        const unsigned ph = (unsigned)((gs / NST) & 1);
         mb_wait(empty + st, ph ^ 1u);
-        uint8_t* At = smA + st * A_STAGE;
-        // K-major, no swizzle: row (32 qtr + lane)'s 32 K-bytes are its own
-        // mask bits expanded to 0/1 bytes, two 16-byte core-matrix rows:
-        // core matrix (row / 8, chunk) at (row / 8) * 128 + chunk * 2048
-        const int ar = 32 * qtr + lane;
-        uint4 c0, c1;
-        c0.x = spread4(word & 0xF); c0.y = spread4((word >> 4) & 0xF);
-        c0.z = spread4((word >> 8) & 0xF); c0.w = spread4((word >> 12) & 0xF);
-        c1.x = spread4((word >> 16) & 0xF); c1.y = spread4((word >> 20) & 0xF);
-        c1.z = spread4((word >> 24) & 0xF); c1.w = spread4((word >> 28) & 0xF);
-        *reinterpret_cast<uint4*>(At + (ar >> 3) * 128 + (ar & 7) * 16) = c0;
-        *reinterpret_cast<uint4*>(At + 2048 + (ar >> 3) * 128 + (ar & 7) * 16) = c1;
+        // K-major, no swizzle: row ar's 128 K-bytes are its 4 words' bits as
+        // 0/1 bytes; core matrix (row / 8, 16-byte chunk c) at
+        // (row / 8) * 128 + c * 2048, row % 8 inside it
+        uint8_t* At = smA + st * A_STAGE + (ar >> 3) * 128 + (ar & 7) * 16;
+        const uint32_t wj[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t w = wj[j];
+          uint4 c0, c1;
+          c0.x = spread4(w & 0xF); c0.y = spread4((w >> 4) & 0xF);
+          c0.z = spread4((w >> 8) & 0xF); c0.w = spread4((w >> 12) & 0xF);
+          c1.x = spread4((w >> 16) & 0xF); c1.y = spread4((w >> 20) & 0xF);
+          c1.z = spread4((w >> 24) & 0xF); c1.w = spread4((w >> 28) & 0xF);
+          *reinterpret_cast<uint4*>(At + (2 * j) * 2048) = c0;
+          *reinterpret_cast<uint4*>(At + (2 * j + 1) * 2048) = c1;
+        }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
         if (lane == 0) mb_arrive(full + st);
@@ -218,12 +213,12 @@ __global__ void __launch_bounds__(NTH, 1)
   } else if (warp < 12) {
     // ---------------- epilogue: TMEM lane quarter warp % 4 -> FP64 ----------------
     const int qtr = warp & 3;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int64_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int64_t row = tile * 128 + 32 * qtr + lane;
       const bool rv = row < a.m;
-      // epilogue: TMEM lane quarter `warp` -> FP64 packed normal matrices
-      const int tb = (int)(((tile - blockIdx.x) / gridDim.x) & 1);  // this tile's accumulator
-      mb_wait(tfull + tb, (unsigned)((((tile - blockIdx.x) / gridDim.x) >> 1) & 1));
+      const int tb = (int)(it & 1);  // this tile's accumulator
+      mb_wait(tfull + tb, (unsigned)((it >> 1) & 1));
       tc_fence_after();
       double A[NA];
 #pragma unroll
@@ -246,8 +241,6 @@ __global__ void __launch_bounds__(NTH, 1)
               "=r"(v[30]), "=r"(v[31])
             : "r"(tmem + ((uint32_t)(32 * qtr) << 16) + (uint32_t)(tb * N + cb)));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        // column cb + j holds digit s = (cb+j) % NS of value p = (cb+j) / NS;
-        // digits are added small-first within each value
 #pragma unroll
         for (int j = 31; j >= 0; --j) {
           const int col = cb + j;
@@ -264,7 +257,7 @@ __global__ void __launch_bounds__(NTH, 1)
       }
     }
   } else if (warp == 12) {
-    // ---------------- MMA issuer ----------------
+    // ---------------- MMA issuer: KSUB MMAs (K = 32 each) per stage ----------------
     int st = 0;
     unsigned ph = 0;
     int64_t it = 0;  // this CTA's tile count: accumulator it & 1
@@ -274,17 +267,25 @@ __global__ void __launch_bounds__(NTH, 1)
       // the epilogue drained this accumulator's previous tile (two tiles ago)
       mb_wait(tempty + tb, (unsigned)(((it >> 1) & 1) ^ 1u));
       tc_fence_after();
-      for (int k = 0; k < nk; ++k) {
+      for (int ks = 0; ks < nks; ++ks) {
         mb_wait(full + st, ph);
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t ad = smem_desc_none(su32(smA + st * A_STAGE), 2048, 128);
-          const uint64_t bd = smem_desc(su32(smB + (res ? k : st) * B_STAGE), KS * 128, 1024);
-          asm volatile(
-              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-              " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(tb * N)),
-              "l"(ad), "l"(bd), "r"(idesc_n(N)), "r"(k > 0 ? 1u : 0u)
-              : "memory");
+          const unsigned abase = su32(smA + st * A_STAGE);
+          const unsigned bbase = su32(smB + (res ? ks : st) * B_STAGE);
+#pragma unroll
+          for (int i = 0; i < KSUB; ++i) {
+            // A: K chunks 2i, 2i+1 (LBO 2048 along K, SBO 128 along M);
+            // B: K-rows 32i.. of each 128-column half (LBO 16 KB between
+            // halves along N, SBO 1 KB between 8-row atoms)
+            const uint64_t ad = smem_desc_none(abase + (unsigned)(2 * i * 2048), 2048, 128);
+            const uint64_t bd = smem_desc(bbase + (unsigned)(i * KS * 128), SK * 128, 1024);
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(tb * N)),
+                "l"(ad), "l"(bd), "r"(idesc_n(N)), "r"((ks > 0 || i > 0) ? 1u : 0u)
+                : "memory");
+          }
           tc_commit(empty + st);
         }
         __syncwarp();
@@ -297,26 +298,26 @@ __global__ void __launch_bounds__(NTH, 1)
       __syncwarp();
     }
   } else {
-    // ---------------- B producer (TMA) ----------------
+    // ---------------- B producer (TMA): 128 K-rows x HQ halves per load ----------------
     if (lane == 0 && res) {
-      mb_expect_tx(bres, (unsigned)(nk * B_STAGE));
-      for (int k = 0; k < nk; ++k)
+      mb_expect_tx(bres, (unsigned)(nks * B_STAGE));
+      for (int ks = 0; ks < nks; ++ks)
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-            "%4}], [%5];\n" ::"r"(su32(smB + k * B_STAGE)),
-            "l"(&tmB), "r"(0), "r"(k * KS), "r"(0), "r"(su32(bres))
+            "%4}], [%5];\n" ::"r"(su32(smB + ks * B_STAGE)),
+            "l"(&tmB), "r"(0), "r"(ks * SK), "r"(0), "r"(su32(bres))
             : "memory");
     } else if (lane == 0) {
       int st = 0;
       unsigned ph = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int k = 0; k < nk; ++k) {
+        for (int ks = 0; ks < nks; ++ks) {
           mb_wait(empty + st, ph ^ 1u);
           mb_expect_tx(full + st, (unsigned)B_STAGE);
           asm volatile(
               "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
               "%4}], [%5];\n" ::"r"(su32(smB + st * B_STAGE)),
-              "l"(&tmB), "r"(0), "r"(k * KS), "r"(0), "r"(su32(full + st))
+              "l"(&tmB), "r"(0), "r"(ks * SK), "r"(0), "r"(su32(full + st))
               : "memory");
           if (++st == NST) {
             st = 0;
@@ -349,19 +350,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 template <int R, int HQ>
 cudaError_t launch_t(const NormalI8Args& a, int sms, cudaStream_t s) {
-  const int nk = (int)((a.n + KS - 1) / KS);
+  const int nks = (int)((a.n + SK - 1) / SK);
   NormalI8Args b = a;
-  const int stream_smem = 1024 + NST * (KS * 128 + KS * 128 * HQ) + 256;
-  const int res_smem = 1024 + NST * KS * 128 + nk * KS * 128 * HQ + 256;
+  const int stream_smem = 1024 + NST * (128 * SK + SK * 128 * HQ) + 256;
+  const int res_smem = 1024 + NST * 128 * SK + nks * SK * 128 * HQ + 256;
   b.b_resident = res_smem <= 200 * 1024 ? 1 : 0;
   const int SMEM = b.b_resident ? res_smem : stream_smem;
   auto fn = encode_fn();
   if (!fn) return cudaErrorInvalidValue;
   CUtensorMap mb;
-  const int64_t nr = ((a.n + KS - 1) / KS) * KS;  // rows of Bq (padded: zero digits)
+  const int64_t nr = ((a.n + SK - 1) / SK) * SK;  // rows of Bq (padded: zero digits)
   cuuint64_t dims[3] = {128, (cuuint64_t)nr, (cuuint64_t)HQ};
   cuuint64_t strides[2] = {128, (cuuint64_t)(128 * nr)};
-  cuuint32_t box[3] = {128, (cuuint32_t)KS, (cuuint32_t)HQ};
+  cuuint32_t box[3] = {128, (cuuint32_t)SK, (cuuint32_t)HQ};
   cuuint32_t es[3] = {1, 1, 1};
   if (fn(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(a.Bq), dims, strides, box, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -378,7 +379,7 @@ template <int R>
 cudaError_t launch_r(const NormalI8Args& a, int sms, cudaStream_t s) {
   constexpr int NA = R * (R + 1) / 2;
   constexpr int HQ = (NA * NS + 127) / 128;
-  const int64_t nr = ((a.n + KS - 1) / KS) * KS;
+  const int64_t nr = ((a.n + SK - 1) / SK) * SK;
   k_q_digits<R><<<(unsigned)std::min<int64_t>((a.n * NA + 255) / 256, 4096), 256, 0, s>>>(a.V, a.n, nr, a.Bq);
   return launch_t<R, HQ>(a, sms, s);
 }
@@ -389,7 +390,7 @@ cudaError_t launch_r(const NormalI8Args& a, int sms, cudaStream_t s) {
 size_t normal_i8_bq_bytes(int r, int64_t n) {
   const int na = r * (r + 1) / 2;
   const int hq = (na * NS + 127) / 128;
-  return (size_t)hq * (size_t)(((n + KS - 1) / KS) * KS) * 128;
+  return (size_t)hq * (size_t)(((n + SK - 1) / SK) * SK) * 128;
 }
 
 cudaError_t launch_normal_i8(const NormalI8Args& a, int sms, cudaStream_t s) {

@@ -878,7 +878,8 @@ SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& out
     const char* e = getenv("RSM_NORMAL_TC");
     return !(e && atoi(e) == 0);
   }();
-  if (normal_tc && unit_basis && hi > lo && v.n >= 32) {
+  // (from ~8k rows on: below that the extra launches cost more than they save)
+  if (normal_tc && unit_basis && hi > lo && v.n >= 32 && v.m >= 8192) {
     const int na = (int)(r * (r + 1) / 2);
     c->Apre.ensure(sizeof(double) * v.m * na);
     c->Bq.ensure(rsmk::normal_i8_bq_bytes((int)r, v.n));
