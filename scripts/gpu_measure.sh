@@ -8,4 +8,4 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 timeout 300 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches exit $?"
 timeout 300 python scripts/prof_c3.py c3 > gpurun_out/prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gram|k_svd_warp|k_solve_u|k_eig|k_select" -s 6 -c 6 -f -o gpurun_out/prof_full python scripts/prof_c3.py c3 > gpurun_out/ncu_full.log 2>&1; echo "ncu full exit $?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gram|k_svd_warp|k_solve_u|k_eig|k_select|k_normal" -s 7 -c 7 -f -o gpurun_out/prof_full python scripts/prof_c3.py c3 > gpurun_out/ncu_full.log 2>&1; echo "ncu full exit $?"
