@@ -554,6 +554,42 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       }
       __syncthreads();
       EIG_T(2);
+      // Probe round (first outer iteration): the filtered block cannot have
+      // converged yet, and the next filter needs only the top Ritz value for
+      // its damping interval -- a Rayleigh quotient of H by power iteration
+      // (a lower bound: the interval only widens) instead of the full b x b
+      // eigensolve, rotation and residuals. Subspace iteration depends on the
+      // span alone, so the CholQR basis carries on unrotated.
+      if (a.rr0_probe && !full && outer == 0 && outer + 1 < a.max_outer) {
+        if (tid < 32) {
+          const int l = tid;
+          double x = l < b ? 1.0 : 0.0;
+          double yv = 0.0;
+          for (int itp = 0; itp < 48; ++itp) {
+            yv = 0.0;
+            for (int j = 0; j < b; ++j) {
+              const double xj = __shfl_sync(0xffffffffu, x, j);
+              if (l < b) yv = fma(sh.H[l * BMAX + j], xj, yv);
+            }
+            const double nn = warp_sum(yv * yv);
+            x = nn > 0.0 ? yv * rsqrt(nn) : x;
+          }
+          yv = 0.0;
+          for (int j = 0; j < b; ++j) {
+            const double xj = __shfl_sync(0xffffffffu, x, j);
+            if (l < b) yv = fma(sh.H[l * BMAX + j], xj, yv);
+          }
+          const double te = warp_sum(x * yv);
+          if (l == 0) sh.theta[b - 1] = te;
+        }
+        __syncthreads();
+        const double te = sh.theta[b - 1];
+        if (lmax > 0.0 && !a.cnt) ub = fmin(ub, fmax(1.1 * lmax, 1.1 * te));
+        acut = te;
+        if (!(acut < 0.999 * ub)) acut = 0.999 * ub;
+        if (acut <= 0.0) acut = 1e-6 * ub;
+        continue;
+      }
       if (tid < 32) {
         const long long tj = clock64();
         const int sw = warp_jacobi_abs(sh.H, BMAX, sh.S, BMAX, b, sh.cs, sh.pairs, 60);

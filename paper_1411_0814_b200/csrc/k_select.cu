@@ -164,16 +164,23 @@ __global__ void k_acc_emit(const int32_t* __restrict__ q, const int32_t* __restr
     }
   }
   __syncthreads();
-  if (!f) return;
   const unsigned long long pos = st->acc_before + (unsigned long long)blockoff[blockIdx.x] +
                                  (unsigned long long)(ws[warp] + __popc(bal & ((1u << lane) - 1u)));
+  // survivor-count sum of the accepted trials that enter the first T: one
+  // 64-bit atomic per warp (integer sums: the order does not matter)
+  const unsigned qc = (f && pos < T) ? (unsigned)q[i] : 0u;
+  const unsigned qw = __reduce_add_sync(0xffffffffu, qc);
+  const unsigned qm = __reduce_max_sync(0xffffffffu, qc);
+  if (lane == 0 && qw) {
+    atomicAdd(&st->qsum, (unsigned long long)qw);
+    atomicMax(&st->qmax, (int)qm);
+  }
+  if (!f) return;
   if (pos >= T) return;
   t_attempt[pos] = a0 + (uint64_t)i;
   const int32_t qi = q[i];
   t_q[pos] = qi;
   for (int t = 0; t < block; ++t) t_idx[pos * block + t] = idx[i * block + t];
-  atomicMax(&st->qmax, qi);
-  atomicAdd(&st->qsum, (unsigned long long)qi);  // integer: order-independent
   if (pos == T - 1) st->attempted_done = a0 + (uint64_t)i + 1;
 }
 

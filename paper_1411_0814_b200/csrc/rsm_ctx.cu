@@ -765,6 +765,11 @@ EigLaunch solve_v_launch(rsm_ctx* c, int64_t n, int64_t r, double tol) {
     return e ? atoi(e) : 40;
   }();
   a.dmax = dmax;
+  static const int rr0_probe = [] {
+    const char* e = getenv("RSM_EIG_PROBE");
+    return e ? atoi(e) : 1;
+  }();
+  a.rr0_probe = rr0_probe;
   a.cnt = c->G_harvest ? c->colcnt.as<int>() : nullptr;
   a.zero_rows = c->eI.as<int>() + 7;
   rsmk::launch_zero_rows(a.G, n, a.cnt, c->eI.as<int>() + 7, c->stream);

@@ -104,6 +104,7 @@ struct EigArgs {
   const int* cnt;   // per-column trial counts when G = diag(cnt) - PSD (else null)
   double amp;       // Chebyshev filter amplification cap (degree choice)
   int dmax;         // and degree cap
+  int rr0_probe;     // first outer iteration: top Ritz value by power iteration only
 };
 
 struct SolveUArgs {
