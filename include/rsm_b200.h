@@ -181,6 +181,11 @@ rsm_status rsm_ctx_solve_u(rsm_ctx* ctx, const double* V, int64_t r, double* U /
 int rsm_ctx_stage_ms(rsm_ctx* ctx, double* ms, int cap);
 /* Kernel launches issued by the last decompose. */
 int64_t rsm_ctx_launch_count(rsm_ctx* ctx);
+/* Decompositions on this context that were re-run because the speculative
+ * selection (one chunk enqueued ahead of stages 2-5) did not
+ * reach the trial count or saw a support longer than stage 2 was sized for
+ * (diagnostic; the results are those of the re-run). */
+int64_t rsm_ctx_rerun_count(rsm_ctx* ctx);
 /* Bytes the last rsm_ctx_load copied host -> device: the values plus the
  * mask bit-packed on the host (rsm_ctx_load_device: 0). */
 int64_t rsm_ctx_last_load_h2d_bytes(rsm_ctx* ctx);

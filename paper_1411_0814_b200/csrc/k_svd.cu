@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
   uint32_t* rw = a.scratch_u32 + (size_t)blockIdx.x * 2 * a.mwp;  // column branch only
   uint32_t* rp = rw + a.mwp;
 
-  for (int64_t t = a.t_lo + blockIdx.x; t < a.t_hi; t += gridDim.x) {
+  const int64_t t_end = a.sel_acc ? min(a.t_hi, (int64_t)*a.sel_acc) : a.t_hi;
+  for (int64_t t = a.t_lo + blockIdx.x; t < t_end; t += gridDim.x) {
     const int64_t tl = t - a.t_lo;  // local index for outputs
     if (tid < K) idx[tid] = a.t_idx[t * K + tid];
     __syncthreads();
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
       warp0_popc_scan(cm, pre, a.cmw, &flags[0]);
       __syncthreads();
       L = flags[0];
+      if (L > a.Lcap) continue;  // speculative launch only (uniform: L is in shared memory)
       for (int64_t w = tid; w < a.cmw; w += nth) a.t_cm[tl * a.cmw + w] = cm[w];
       // gather S (K x L) row-major into vec (sampler.cpp:80-84)
       if (K >= 2 && K <= 9) {
@@ -327,6 +329,7 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
       warp0_popc_scan(rw, rp, a.mwp, &flags[0]);
       __syncthreads();
       L = flags[0];
+      if (L > a.Lcap) continue;  // speculative launch only (uniform: L is in shared memory)
       // gather S^T (K x L): vector j = column idx[j] over surviving rows
       if (K >= 2 && K <= 8) {
         switch (K) {
@@ -757,7 +760,8 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
   const int rex = a.rex, rp = (a.rex + 1) & ~1;
   const int64_t nwarps = (int64_t)gridDim.x * SVDW_WARPS;
 
-  for (int64_t t = a.t_lo + (int64_t)blockIdx.x * SVDW_WARPS + warp; t < a.t_hi; t += nwarps) {
+  const int64_t t_end = a.sel_acc ? min(a.t_hi, (int64_t)*a.sel_acc) : a.t_hi;
+  for (int64_t t = a.t_lo + (int64_t)blockIdx.x * SVDW_WARPS + warp; t < t_end; t += nwarps) {
     const int64_t tl = t - a.t_lo;
     const int myidx = lane < K ? a.t_idx[t * K + lane] : 0;
     int rows[K];
@@ -789,6 +793,7 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
       run += __shfl_sync(0xffffffffu, incl, 31);
     }
     const int L = run;
+    if (L > a.Lcap) continue;  // speculative launch only (see SvdArgs)
     __syncwarp();
     // gather S (K x L): lane = column within each 32-column word. Every
     // support cell is copied global -> shared by an asynchronous 8-byte copy
@@ -1055,6 +1060,45 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
 
 size_t svd_warp_smem(int K, int64_t Lpad, int64_t cmw) {
   return sizeof(double) * (size_t)SVDW_WARPS * (K * Lpad + 2 * K * K + 64 + 32 + cmw);
+}
+
+static const void* svd_warp_fn(int K) {
+  switch (K) {
+    case 2: return (const void*)k_svd_warp<2>;
+    case 3: return (const void*)k_svd_warp<3>;
+    case 4: return (const void*)k_svd_warp<4>;
+    case 5: return (const void*)k_svd_warp<5>;
+    case 6: return (const void*)k_svd_warp<6>;
+    case 7: return (const void*)k_svd_warp<7>;
+    case 8: return (const void*)k_svd_warp<8>;
+    case 9: return (const void*)k_svd_warp<9>;
+    default: return nullptr;
+  }
+}
+
+// speculative stage-2 bound: the largest even support length >= Lest for which
+// the warp kernel keeps the occupancy it has at Lest (the shared memory the
+// bound costs is then free); Lest itself when the warp kernel does not apply
+int64_t svd_warp_lcap(int K, int64_t Lest, int64_t cmw) {
+  Lest = std::max<int64_t>(2, (Lest + 1) & ~int64_t(1));
+  const void* fn = svd_warp_fn(K);
+  if (!fn || svd_warp_smem(K, Lest, cmw) > 200 * 1024) return Lest;
+  const int occ0 = occupancy(fn, SVDW_WARPS * 32, svd_warp_smem(K, Lest, cmw));
+  auto keeps = [&](int64_t L) {
+    const size_t sm = svd_warp_smem(K, L, cmw);
+    return sm <= 200 * 1024 && occupancy(fn, SVDW_WARPS * 32, sm) >= occ0;
+  };
+  int64_t lo = Lest, hi = Lest + 2;  // even lengths; lo keeps occ0
+  while (keeps(hi)) {
+    lo = hi;
+    hi *= 2;
+  }
+  while (hi - lo > 2) {
+    const int64_t mid = ((lo + hi) / 2) & ~int64_t(1);
+    if (keeps(mid)) lo = mid;
+    else hi = mid;
+  }
+  return lo;
 }
 
 bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s) {

@@ -104,6 +104,7 @@ struct SelResult {
   uint64_t attempted = 0, accepted = 0;
   int qmax = 0;
   uint64_t qsum = 0;  // sum of the accepted trials' survivor counts
+  bool spec = false;  // speculative: one chunk enqueued, outcome read after the caller's sync
 };
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -164,7 +165,12 @@ struct rsm_ctx {
       flagged, dsum, cnt64, Wq, tiles8, ugather;
   DevBuf Apre, Bq;  // stage 5's tensor-core normal matrices and the basis-product digits
   DevBuf aux0, aux1, aux2, aux3;  // per-call utilities (rsm_sample, rsm_small_singular_vectors, rsm_gram_update)
-  double* hsmall = nullptr;  // pinned host staging: eig stats [0,96), stage-5 scalars [96,100)
+  double* hsmall = nullptr;  // pinned host staging: eig stats [0,96), stage-5 scalars [96,100),
+                             // speculative selection state [104,109)
+  double spec_rate = 1.0;    // acceptance rate seen by the last full selection (sizes the speculative chunk)
+  int64_t spec_Lcap = 0;     // support bound of the last speculative stage-2 launch
+  int64_t spec_qhint = 0;    // largest support a failed speculation saw on this matrix
+  int64_t spec_reruns = 0;   // decompositions re-run after a failed speculation (tests read it)
   int64_t tiles_n = -1;
   int64_t tiles8_n = -1;  // tcgen05 stage-3 tile list valid for this npad
   int ntiles8 = 0;
@@ -361,6 +367,8 @@ void load_common(rsm_ctx* c, int64_t m, int64_t n, bool packed_on_host) {
   ck(cudaStreamSynchronize(c->stream), "sync");
   ck(cudaGetLastError(), "load kernels");
   c->loaded = true;
+  c->spec_qhint = 0;
+  c->spec_rate = 1.0;
 }
 
 // ------------------------------------------------------------- trial params
@@ -397,7 +405,13 @@ void check_device_params(const rsm_trial_params* p, const View& v) {
 }
 
 // ------------------------------------------------------------------ stage 1
-SelResult select_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint64_t T) {
+double* pinned_small(rsm_ctx* c);
+
+// spec = true: enqueue one chunk sized from the last observed acceptance rate
+// and return without synchronising, as if it accepted all T trials; the
+// selection state goes to pinned memory and decompose checks it after its one
+// synchronisation (spec_selection_ok)
+SelResult select_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint64_t T, bool spec = false) {
   if (T < 1) fail(RSM_ERR_INVALID_CONFIG, "trial count must be positive");
   check_device_params(p, v);
   const bool m2 = p->mode == RSM_MODE_M2;
@@ -414,7 +428,7 @@ SelResult select_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint
   const int64_t pool = m2 ? v.m : v.n;
   SelResult r;
   uint64_t attempted = 0, acc = 0;
-  double p_est = 1.0;
+  double p_est = spec ? std::min(1.0, std::max(1e-3, c->spec_rate)) : 1.0;
   rsmk::SelState hs{};
   while (acc < T && attempted < budget) {
     const uint64_t want = T - acc;
@@ -432,6 +446,15 @@ SelResult select_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint
                         c->selstate.as<rsmk::SelState>(), T, c->t_attempt.as<uint64_t>(),
                         c->t_q.as<int32_t>(), c->t_idx.as<int32_t>(), c->stream);
     c->launches += 4;
+    if (spec) {
+      static_assert(sizeof(rsmk::SelState) <= 5 * sizeof(double), "pinned slot");
+      ck(cudaMemcpyAsync(pinned_small(c) + 104, c->selstate.p, sizeof(rsmk::SelState), cudaMemcpyDeviceToHost,
+                         c->stream), "D2H");
+      r.attempted = chunk;
+      r.accepted = T;
+      r.spec = true;
+      return r;
+    }
     ck(cudaMemcpyAsync(&hs, c->selstate.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "select");
     ck(cudaGetLastError(), "select kernels");
@@ -448,14 +471,58 @@ SelResult select_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint
   r.accepted = acc;
   r.qmax = hs.qmax;
   r.qsum = hs.qsum;
+  if (attempted) c->spec_rate = (double)acc / (double)attempted;
   return r;
+}
+
+// after the stream sync: did the speculative chunk accept all T trials, with
+// every support within the bound the speculative stage-2 launch assumed? The
+// state is the same on every rank (the selection is replicated), so all ranks
+// take the same branch.
+bool spec_selection_ok(rsm_ctx* c, SelResult* r) {
+  rsmk::SelState hs;
+  std::memcpy(&hs, c->hsmall + 104, sizeof(hs));
+  if (!hs.attempted_done) {
+    c->spec_rate = std::max(1e-3, (double)hs.acc / (double)std::max<uint64_t>(r->attempted, 1));
+    return false;
+  }
+  if ((int64_t)hs.qmax > c->spec_Lcap) {
+    c->spec_qhint = hs.qmax;
+    return false;
+  }
+  r->attempted = hs.attempted_done;
+  r->qmax = hs.qmax;
+  r->qsum = hs.qsum;
+  r->spec = false;
+  return true;
 }
 
 // ------------------------------------------------------------ stages 2 + 3
 struct HarvestOut {
   SelResult sel;
   uint64_t z = 0;
+  int rex = 0;  // top vectors per trial
 };
+
+// support-length bound for a speculative stage-2 launch: K random rows (row
+// branch) or columns (column branch) under the loaded density keep a
+// binomial number of survivors; mean + 5 sd (a miss costs a re-run, about
+// T * 3e-7 per call for an i.i.d. mask; a wider bound costs the warp kernel
+// occupancy on every call), raised to what the warp kernel's
+// occupancy allows for free, and to the largest support a failed speculation
+// on this matrix saw
+int64_t spec_lcap(rsm_ctx* c, const View& v, bool m2, int K, int64_t cmw) {
+  const double pool = m2 ? (double)v.n : (double)v.m;
+  const double dens = (double)c->known / ((double)v.m * (double)v.n);
+  const double pk = std::pow(dens, K);
+  const double mean = pool * pk, sd = std::sqrt(pool * pk * (1.0 - pk));
+  int64_t L = (int64_t)std::ceil(mean + 5.0 * sd + 8.0);
+  L = std::max<int64_t>(L, c->spec_qhint);
+  L = std::min<int64_t>(L, (int64_t)pool);
+  if (m2) L = rsmk::svd_warp_lcap(K, L, cmw);
+  if (const char* e = getenv("RSM_SPEC_LCAP")) L = std::max<int64_t>(2, atoll(e));  // tests: force the fallback
+  return L;
+}
 
 void build_tiles(rsm_ctx* c, int64_t npad, int cpl) {
   if (c->tiles_n == npad && c->tiles_cpl == cpl) return;
@@ -496,11 +563,11 @@ int64_t ntiles_for(int64_t npad, int cpl) {
   return k;
 }
 
-HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint64_t T) {
+HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, uint64_t T, bool spec = false) {
   HarvestOut out;
   const bool m2 = p->mode == RSM_MODE_M2;
   record(c, 0);
-  out.sel = select_impl(c, v, p, T);
+  out.sel = select_impl(c, v, p, T, spec);
   record(c, 1);
   const int64_t Tacc = (int64_t)out.sel.accepted;
   const int64_t n = v.n;
@@ -513,7 +580,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
   int rex;
   if (m2) {
     rex = (int)p->rank;
-    if (p->ell > 0 && Tacc > 0 && p->ell < (int64_t)out.sel.qmax - p->rank)
+    if (!out.sel.spec && p->ell > 0 && Tacc > 0 && p->ell < (int64_t)out.sel.qmax - p->rank)
       fail(RSM_ERR_INVALID_CONFIG,
            "row-branch vectors_per_trial below survivors-rank harvests an implementation-defined "
            "null-space basis; the device path supports the adaptive default");
@@ -521,6 +588,7 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     rex = (int)(p->block - p->ell);
   }
   if (rex < 1 || rex > 16) fail(RSM_ERR_INVALID_CONFIG, "device path supports 1 <= block-vectors <= 16 top vectors");
+  out.rex = rex;
   // local trial range (trials shard over ranks, no communication needed)
   int64_t t_lo, t_hi;
   rsm_shard_range(Tacc, c->world, c->rank, &t_lo, &t_hi);
@@ -579,9 +647,11 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     c->t_cm.ensure(sizeof(uint32_t) * chunk * cmw);
     if (i8) c->Wq.ensure((size_t)S8 * Kpad0 * npad);
     else c->Vtrial.ensure((size_t)tbytes * chunk);
-    int64_t Lmax = m2 ? out.sel.qmax : 0;
-    if (!m2) Lmax = out.sel.qmax;  // the largest survivor count over all accepted trials
+    // the largest survivor count over all accepted trials; a speculative
+    // launch does not know it yet and sizes for a bound instead (spec_lcap)
+    const int64_t Lmax = out.sel.spec ? spec_lcap(c, v, m2, K, cmw) : out.sel.qmax;
     const int64_t Lpad = std::max<int64_t>(2, (Lmax + 1) & ~int64_t(1));
+    c->spec_Lcap = Lpad;
     const size_t fixed = rsmk::svd_smem_fixed(cmw, m2);
     const size_t vecb = sizeof(double) * (size_t)K * Lpad;
     const bool use_smem = fixed + vecb <= 200 * 1024;
@@ -624,6 +694,8 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
         a.scratch_u32 = c->svd_scr32.as<uint32_t>();
       }
       a.Lpad = Lpad;
+      a.Lcap = out.sel.spec ? Lpad : INT64_MAX;
+      a.sel_acc = out.sel.spec ? &c->selstate.as<rsmk::SelState>()->acc : nullptr;
       a.use_smem = use_smem ? 1 : 0;
       static const int svd_maxit = [] {
         const char* e = getenv("RSM_SVD_MAXIT");
@@ -979,27 +1051,53 @@ void decompose_impl(rsm_ctx* c, const rsm_config* cfg, double* Uout, double* Vou
   const bool tr = m < n;  // solver.cpp:130-140
   const View v = make_view(c, tr, cfg->mode == RSM_MODE_M1);
   const rsm_trial_params p = trial_params_impl(cfg, v.m, v.n);
-  HarvestOut h = harvest_impl(c, v, &p, cfg->trials);
-  rep->trials_attempted = h.sel.attempted;
-  rep->trials_accepted = h.sel.accepted;
-  rep->z = h.z;
-  // stages 4 and 5 are enqueued back to back: stage 5 needs only V-hat (on
-  // the device), so the host reads the eigensolver's status and the rank
-  // gate once, after the final synchronisation (a failed gate discards the
-  // stage-5 results and raises as the reference does)
+  // The whole decomposition is enqueued before the host looks at anything:
+  // the selection runs speculatively (one chunk, stage 2 sized for a support
+  // bound), stages 4 and 5 follow back to back (stage 5 needs only V-hat, on
+  // the device), and the host synchronises once. It then reads the selection
+  // state, the eigensolver's status and the rank gate; if the chunk did not
+  // reach T acceptances or a support outgrew the bound (both rare and
+  // replicated on every rank), the decomposition is re-run with the
+  // synchronous selection. A failed gate discards the stage-5 results and
+  // raises as the reference does. RSM_SPEC=0 runs the synchronous selection.
+  static const bool spec_on = [] {
+    const char* e = getenv("RSM_SPEC");
+    return !(e && atoi(e) == 0);
+  }();
   const int64_t r = cfg->rank;
-  const EigLaunch L = solve_v_launch(c, v.n, r, cfg->gram_rank_tol);
-  record(c, 5);
-  c->Vhat_n = 0;
-  c->U_m = 0;
-  solve_rows(c, v, c->Vhat.as<double>(), c->U, r, nullptr, /*defer=*/true, /*unit_basis=*/true);
-  record(c, 6);
   // oriented U is (v.m x r), oriented V is (v.n x r); the transpose swaps them
   double* hostU = tr ? Vout : Uout;
   double* hostV = tr ? Uout : Vout;
-  if (hostU) ck(cudaMemcpyAsync(hostU, c->U.p, sizeof(double) * v.m * r, cudaMemcpyDeviceToHost, c->stream), "D2H U");
-  if (hostV) ck(cudaMemcpyAsync(hostV, c->Vhat.p, sizeof(double) * v.n * r, cudaMemcpyDeviceToHost, c->stream), "D2H V");
-  ck(cudaStreamSynchronize(c->stream), "decompose");
+  HarvestOut h;
+  EigLaunch L;
+  for (bool spec = spec_on;; spec = false) {
+    h = harvest_impl(c, v, &p, cfg->trials, spec);
+    L = solve_v_launch(c, v.n, r, cfg->gram_rank_tol);
+    record(c, 5);
+    c->Vhat_n = 0;
+    c->U_m = 0;
+    solve_rows(c, v, c->Vhat.as<double>(), c->U, r, nullptr, /*defer=*/true, /*unit_basis=*/true);
+    record(c, 6);
+    if (hostU) ck(cudaMemcpyAsync(hostU, c->U.p, sizeof(double) * v.m * r, cudaMemcpyDeviceToHost, c->stream), "D2H U");
+    if (hostV) ck(cudaMemcpyAsync(hostV, c->Vhat.p, sizeof(double) * v.n * r, cudaMemcpyDeviceToHost, c->stream), "D2H V");
+    ck(cudaStreamSynchronize(c->stream), "decompose");
+    if (!h.sel.spec) break;
+    if (spec_selection_ok(c, &h.sel)) {
+      // the harvest's host-side checks that needed the selection outcome
+      if (p.mode == RSM_MODE_M2) {
+        if (p.ell > 0 && p.ell < (int64_t)h.sel.qmax - p.rank)
+          fail(RSM_ERR_INVALID_CONFIG,
+               "row-branch vectors_per_trial below survivors-rank harvests an implementation-defined "
+               "null-space basis; the device path supports the adaptive default");
+        h.z = h.sel.qsum - h.sel.accepted * (uint64_t)h.rex;
+      }
+      break;
+    }
+    ++c->spec_reruns;
+  }
+  rep->trials_attempted = h.sel.attempted;
+  rep->trials_accepted = h.sel.accepted;
+  rep->z = h.z;
   const SolveVOut sv = solve_v_finish(c, L, v.n, r, cfg->gram_rank_tol);
   rep->gram_rank = sv.gram_rank;
   rep->borderline_rank_gate = sv.borderline;
@@ -1413,6 +1511,8 @@ int rsm_ctx_stage_ms(rsm_ctx* c, double* ms, int cap) {
 }
 
 int64_t rsm_ctx_launch_count(rsm_ctx* c) { return c ? c->launches : 0; }
+
+int64_t rsm_ctx_rerun_count(rsm_ctx* c) { return c ? c->spec_reruns : 0; }
 
 int64_t rsm_ctx_last_load_h2d_bytes(rsm_ctx* c) { return c ? c->last_h2d : 0; }
 

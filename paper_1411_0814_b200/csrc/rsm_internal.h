@@ -52,6 +52,12 @@ struct SvdArgs {
   int use_smem;
   int max_outer;         // one-sided Jacobi rotations per trial (at most)
   int fast_basis;        // row branch, r = k - 1: top-r basis from the Gram (no Jacobi)
+  // speculative launch (decompose enqueues stages 2-5 before the selection's
+  // outcome is on the host): trials at or past *sel_acc and trials whose
+  // support exceeds Lcap are skipped; the host checks the selection state
+  // after its one synchronisation and re-runs when either happened
+  const unsigned long long* sel_acc;
+  int64_t Lcap;
 };
 
 struct GramArgs {
@@ -151,6 +157,7 @@ size_t svd_smem_fixed(int64_t cmw, bool m2);
 void launch_svd(const SvdArgs& a, bool m2, int grid, size_t smem, cudaStream_t s);
 int svd_occupancy(bool m2, size_t smem);
 bool launch_svd_warp(const SvdArgs& a, int sms, cudaStream_t s);  // row branch, k <= 9
+int64_t svd_warp_lcap(int K, int64_t Lest, int64_t cmw);
 // k_gram.cu
 int gram_cols_per_lane(int R);
 int gram_ctas_per_sm(int R);

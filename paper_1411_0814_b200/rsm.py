@@ -101,6 +101,7 @@ def lib():
         "rsm_ctx_solve_u": (i32, [_P, _P, i64, _P, C.POINTER(i64), C.POINTER(dbl)]),
         "rsm_ctx_stage_ms": (C.c_int, [_P, _P, C.c_int]),
         "rsm_ctx_launch_count": (i64, [_P]),
+        "rsm_ctx_rerun_count": (i64, [_P]),
         "rsm_ctx_last_load_h2d_bytes": (i64, [_P]),
         "rsm_ctx_solver_stats": (C.c_int, [_P, _P, C.c_int]),
         "rsm_make_trial_params": (i32, [C.POINTER(_Config), i64, i64, C.POINTER(_TrialParams)]),
@@ -141,7 +142,7 @@ def exported_symbols():
     return ["rsm_config_default", "rsm_last_error", "rsm_ctx_create", "rsm_ctx_destroy", "rsm_nccl_unique_id",
             "rsm_ctx_stream", "rsm_ctx_load", "rsm_ctx_load_device", "rsm_ctx_generate", "rsm_ctx_fetch_matrix", "rsm_ctx_decompose", "rsm_ctx_fetch_factors", "rsm_ctx_als",
             "rsm_ctx_select", "rsm_ctx_harvest_gram", "rsm_ctx_solve_v", "rsm_ctx_solve_u", "rsm_ctx_stage_ms",
-            "rsm_ctx_launch_count", "rsm_ctx_last_load_h2d_bytes", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_als", "rsm_harvest_gram", "rsm_solve_v",
+            "rsm_ctx_launch_count", "rsm_ctx_rerun_count", "rsm_ctx_last_load_h2d_bytes", "rsm_ctx_solver_stats", "rsm_make_trial_params", "rsm_decompose", "rsm_als", "rsm_harvest_gram", "rsm_solve_v",
             "rsm_solve_u", "rsm_masked_residual_norm", "rsm_generate", "rsm_generate_tracks", "rsm_load_matrix_csv",
             "rsm_save_matrix_csv", "rsm_dataset_checksum", "rsm_free", "rsm_fp64_peak_tflops",
             "rsm_dmma_peak_tflops", "rsm_shard_range", "rsm_host_group_create", "rsm_host_group_destroy",
@@ -450,6 +451,10 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().rsm_ctx_launch_count(self.h))
+
+    def rerun_count(self) -> int:
+        """decompositions re-run after a failed speculative selection (diagnostic)"""
+        return int(lib().rsm_ctx_rerun_count(self.h))
 
     def last_load_h2d_bytes(self) -> int:
         """Bytes the last host load copied to the device (values + packed mask)."""
