@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
@@ -43,11 +44,16 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(RSM_ERR_INTERNAL, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
+// bumped whenever any device buffer moves: a captured decompose graph holds
+// raw buffer addresses and is replayed only while this is unchanged
+std::atomic<uint64_t> g_buf_epoch{0};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   void ensure(size_t need) {
     if (need <= bytes) return;
+    ++g_buf_epoch;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -58,9 +64,34 @@ struct DevBuf {
   template <class T>
   T* as() const { return static_cast<T*>(p); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      ++g_buf_epoch;
+      cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
+  }
+};
+
+// decompose's device work as one CUDA graph (decompose_impl): the key is
+// everything the host-side enqueue reads; the rest is the host state the
+// captured call left behind, restored on every replay
+struct DecompGraph {
+  cudaGraphExec_t exec = nullptr;
+  bool keyed = false, broken = false;
+  int64_t rank = 0, block = 0, vpt = 0, min_dim = 0;
+  int32_t mode = 0;
+  uint64_t trials = 0, seed = 0, load_gen = 0, epoch = 0;
+  double tol = 0.0, spec_rate = 0.0;
+  int64_t qhint = 0;
+  // captured outcome
+  uint64_t attempted = 0, accepted = 0, z = 0;
+  int rex = 0, eig_b = 0, eig_grid = 0;
+  int64_t launches = 0, spec_Lcap = 0;
+  void drop() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    keyed = false;
   }
 };
 
@@ -147,6 +178,8 @@ struct rsm_ctx {
 
   // the loaded matrix as given
   bool loaded = false;
+  uint64_t load_gen = 0;  // bumped by every load (decompose graph key)
+  DecompGraph dgraph;
   int64_t m = 0, n = 0;
   unsigned long long known = 0;
   DevBuf Y, M8, bitsR, bitsC;
@@ -197,7 +230,16 @@ namespace {
 
 thread_local std::string g_err;
 
-void record(rsm_ctx* c, int i) { ck(cudaEventRecord(c->ev[i], c->stream), "cudaEventRecord"); }
+void record(rsm_ctx* c, int i) {
+  // inside a decompose graph capture the stage events become event-record
+  // nodes (External), so every replay re-records them
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  ck(cudaStreamIsCapturing(c->stream, &st), "cudaStreamIsCapturing");
+  if (st == cudaStreamCaptureStatusActive)
+    ck(cudaEventRecordWithFlags(c->ev[i], c->stream, cudaEventRecordExternal), "cudaEventRecord");
+  else
+    ck(cudaEventRecord(c->ev[i], c->stream), "cudaEventRecord");
+}
 
 // ---------------------------------------------------------------- collectives
 // Sum over ranks in place (FP64 or int32 elements): NCCL on the context
@@ -367,6 +409,7 @@ void load_common(rsm_ctx* c, int64_t m, int64_t n, bool packed_on_host) {
   ck(cudaStreamSynchronize(c->stream), "sync");
   ck(cudaGetLastError(), "load kernels");
   c->loaded = true;
+  ++c->load_gen;
   c->spec_qhint = 0;
   c->spec_rate = 1.0;
 }
@@ -1070,7 +1113,7 @@ void decompose_impl(rsm_ctx* c, const rsm_config* cfg, double* Uout, double* Vou
   double* hostV = tr ? Uout : Vout;
   HarvestOut h;
   EigLaunch L;
-  for (bool spec = spec_on;; spec = false) {
+  auto enqueue = [&](bool spec) {
     h = harvest_impl(c, v, &p, cfg->trials, spec);
     L = solve_v_launch(c, v.n, r, cfg->gram_rank_tol);
     record(c, 5);
@@ -1078,10 +1121,96 @@ void decompose_impl(rsm_ctx* c, const rsm_config* cfg, double* Uout, double* Vou
     c->U_m = 0;
     solve_rows(c, v, c->Vhat.as<double>(), c->U, r, nullptr, /*defer=*/true, /*unit_basis=*/true);
     record(c, 6);
+  };
+  auto fetch_and_sync = [&] {
     if (hostU) ck(cudaMemcpyAsync(hostU, c->U.p, sizeof(double) * v.m * r, cudaMemcpyDeviceToHost, c->stream), "D2H U");
     if (hostV) ck(cudaMemcpyAsync(hostV, c->Vhat.p, sizeof(double) * v.n * r, cudaMemcpyDeviceToHost, c->stream), "D2H V");
     ck(cudaStreamSynchronize(c->stream), "decompose");
-    if (!h.sel.spec) break;
+  };
+  // With the speculative selection the enqueue never waits on the device, so
+  // it is captured once as a CUDA graph and replayed: the first call with a
+  // key runs eagerly (and allocates), the second captures, later calls only
+  // launch the graph (single rank; RSM_GRAPH=0 disables).
+  static const bool graph_env = [] {
+    const char* e = getenv("RSM_GRAPH");
+    return !(e && atoi(e) == 0);
+  }();
+  DecompGraph& g = c->dgraph;
+  const bool graph_on = spec_on && graph_env && !c->coll && !g.broken;
+  bool done = false;
+  if (graph_on) {
+    const bool same = g.keyed && g.rank == cfg->rank && g.mode == cfg->mode && g.block == cfg->block &&
+                      g.vpt == cfg->vectors_per_trial && g.trials == cfg->trials && g.seed == cfg->seed &&
+                      g.tol == cfg->gram_rank_tol && g.min_dim == cfg->min_dim && g.load_gen == c->load_gen &&
+                      g.epoch == g_buf_epoch.load() && g.spec_rate == c->spec_rate && g.qhint == c->spec_qhint;
+    if (same && g.exec) {
+      ck(cudaGraphLaunch(g.exec, c->stream), "decompose graph launch");
+      h.sel.attempted = g.attempted;
+      h.sel.accepted = g.accepted;
+      h.sel.spec = true;
+      h.z = g.z;
+      h.rex = g.rex;
+      L.b = g.eig_b;
+      L.grid = g.eig_grid;
+      c->launches += g.launches;
+      c->spec_Lcap = g.spec_Lcap;
+      c->G_n = v.n;
+      c->G_harvest = true;
+      fetch_and_sync();
+      done = true;
+    } else if (same) {
+      const uint64_t e0 = g_buf_epoch.load();
+      const int64_t l0 = c->launches;
+      cudaGraph_t gr = nullptr;
+      ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed), "begin capture");
+      bool captured = true;
+      try {
+        enqueue(true);
+      } catch (...) {
+        captured = false;
+      }
+      const cudaError_t ce = cudaStreamEndCapture(c->stream, &gr);
+      cudaGetLastError();
+      cudaGraphExec_t ex = nullptr;
+      if (captured && ce == cudaSuccess && gr && g_buf_epoch.load() == e0 &&
+          cudaGraphInstantiate(&ex, gr, 0) == cudaSuccess) {
+        g.exec = ex;
+        g.attempted = h.sel.attempted;
+        g.accepted = h.sel.accepted;
+        g.z = h.z;
+        g.rex = h.rex;
+        g.eig_b = L.b;
+        g.eig_grid = L.grid;
+        g.launches = c->launches - l0;
+        g.spec_Lcap = c->spec_Lcap;
+        ck(cudaGraphLaunch(g.exec, c->stream), "decompose graph launch");
+        fetch_and_sync();
+        done = true;
+      } else {
+        cudaGetLastError();
+        g.broken = true;  // this context runs eagerly from now on
+        c->launches = l0;
+      }
+      if (gr) cudaGraphDestroy(gr);
+    } else {
+      g.drop();
+    }
+  }
+  if (!done) {
+    enqueue(spec_on);  // eager (first call with this key, a failed capture, or no graph)
+    fetch_and_sync();
+    if (graph_on && !g.keyed) {
+      g.keyed = true;
+      g.rank = cfg->rank; g.mode = cfg->mode; g.block = cfg->block; g.vpt = cfg->vectors_per_trial;
+      g.trials = cfg->trials; g.seed = cfg->seed; g.tol = cfg->gram_rank_tol; g.min_dim = cfg->min_dim;
+      g.load_gen = c->load_gen;
+      g.spec_rate = c->spec_rate;
+      g.qhint = c->spec_qhint;
+    }
+  }
+  if (graph_on && g.keyed) g.epoch = g_buf_epoch.load();
+  // the speculation's outcome: a miss re-runs with the synchronous selection
+  if (h.sel.spec) {
     if (spec_selection_ok(c, &h.sel)) {
       // the harvest's host-side checks that needed the selection outcome
       if (p.mode == RSM_MODE_M2) {
@@ -1091,9 +1220,11 @@ void decompose_impl(rsm_ctx* c, const rsm_config* cfg, double* Uout, double* Vou
                "null-space basis; the device path supports the adaptive default");
         h.z = h.sel.qsum - h.sel.accepted * (uint64_t)h.rex;
       }
-      break;
+    } else {
+      ++c->spec_reruns;
+      enqueue(false);
+      fetch_and_sync();
     }
-    ++c->spec_reruns;
   }
   rep->trials_attempted = h.sel.attempted;
   rep->trials_accepted = h.sel.accepted;
@@ -1307,6 +1438,7 @@ rsm_status rsm_ctx_destroy(rsm_ctx* c) {
                     &c->eW, &c->eI, &c->eD, &c->Vhat, &c->U, &c->rowres, &c->flagged, &c->dsum,
                     &c->cnt64, &c->Wq, &c->tiles8, &c->ugather, &c->aux0, &c->aux1, &c->aux2, &c->aux3,
                     &c->Apre, &c->Bq};
+  c->dgraph.drop();
   for (DevBuf* b : bufs) b->release();
   if (c->hstage) cudaFreeHost(c->hstage);
   if (c->hsmall) cudaFreeHost(c->hsmall);

@@ -88,3 +88,56 @@ def test_column_branch_speculation_matches_oracle():
     assert rep.trials_attempted == rep_o.trials_attempted and rep.z == rep_o.z
     assert rep.gram_rank == rep_o.gram_rank
     assert rel_fro(F.u @ F.v.T, U_o @ V_o.T) <= 1e-9
+
+
+# ---------------------------------------------------- decompose as one graph
+# (first call with a key eager, second captured, later calls replayed)
+
+def test_graph_replay_matches_eager_bitwise():
+    M = rsm.generate(2000, 200, 3, 0.8, 1e-3, 0)
+    cfg = rsm.RsmConfig(rank=3, mode=rsm.Mode.M2, block=4, plan=rsm.TrialPlan(2000), seed=0)
+    c = rsm.Context(0)
+    try:
+        c.load(M)
+        outs, stages, launches = [], [], []
+        for _ in range(4):
+            outs.append(c.decompose(cfg))
+            stages.append(c.stage_ms())
+            launches.append(c.launch_count())
+        for o in outs[1:]:
+            _same(outs[0], o)
+        assert len(set(launches)) == 1 and launches[0] > 0
+        for st in stages:  # replays re-record the stage events
+            assert st[6] > 0 and all(x >= 0 for x in st[:6])
+            assert abs(sum(st[:6]) - st[6]) <= 1e-3 * st[6] + 1e-3
+        assert stages[3] != stages[2] or stages[2] != stages[1]
+        # a new key (seed) after the graph: same as a fresh context's result
+        cfg2 = rsm.RsmConfig(rank=3, mode=rsm.Mode.M2, block=4, plan=rsm.TrialPlan(2000), seed=1)
+        a = c.decompose(cfg2)
+        b = _run(M, cfg2)
+        b[3].close()
+        _same(a, b)
+        # a reload invalidates the graph: results follow the new matrix
+        M3 = rsm.generate(2000, 200, 3, 0.8, 1e-3, 9)
+        c.load(M3)
+        for _ in range(3):
+            d = c.decompose(cfg)
+        e = _run(M3, cfg)
+        e[3].close()
+        _same(d, e)
+    finally:
+        c.close()
+
+
+def test_graph_replay_rank_gate_failure_raises_every_call():
+    M = rsm.generate_tracks(2048, 256, 32, 128, 1e-3, 0)
+    cfg = rsm.RsmConfig(rank=4, mode=rsm.Mode.M2, block=5, plan=rsm.TrialPlan(2048), seed=0)
+    c = rsm.Context(0)
+    try:
+        c.load(M)
+        for _ in range(4):
+            with pytest.raises(rsm.Error) as ei:
+                c.decompose(cfg)
+            assert ei.value.code == rsm.errc.insufficient_coverage
+    finally:
+        c.close()
