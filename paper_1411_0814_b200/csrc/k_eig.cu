@@ -245,57 +245,54 @@ __device__ void gram_partial(const EigArgs& a, const double* Xo, int nc, int ld,
 }
 
 // warp 0: Cholesky of the nc x nc matrix given packed (upper) in sh.red;
-// lower factor to sh.S and its reciprocal diagonal to sh.dinv. Lane i holds
-// row i in registers; column k of the factor is broadcast by shuffles.
+// lower factor to sh.S and its reciprocal diagonal to sh.dinv. Right-looking,
+// in place in shared memory with rolled loops: the routine runs a handful of
+// times per kernel, far apart, so its instructions are fetched cold each
+// time -- compact code beats a register-unrolled version (measured 3x).
 // Retries with a diagonal shift when the matrix is not numerically positive.
-__device__ __noinline__ void chol_small(int nc, EigShared& sh) {
+__device__ __noinline__ void chol_small(int nc, EigShared& sh, double shift0) {
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
+  double* L = sh.S;
   double tr = 0.0;
-  for (int k = 0; k < nc; ++k) tr += fabs(sh.red[k * nc - k * (k - 1) / 2]);
-  double shift = 0.0;
-  double a[BMAX];
+  for (int k = lane; k < nc; k += 32) tr += fabs(sh.red[k * nc - k * (k - 1) / 2]);
+  tr = warp_sum(tr);
+  double shift = shift0 * tr;
+#pragma unroll 1
   for (int attempt = 0; attempt < 4; ++attempt) {
-#pragma unroll
-    for (int j = 0; j < BMAX; ++j) {
-      double v = 0.0;
-      if (lane < nc && j < nc) {
-        const int i0 = lane < j ? lane : j, j0 = lane < j ? j : lane;
-        v = sh.red[i0 * nc - i0 * (i0 - 1) / 2 + (j0 - i0)] + (lane == j ? shift : 0.0);
-      }
-      a[j] = v;
+#pragma unroll 1
+    for (int e = lane; e < nc * nc; e += 32) {
+      const int i = e / nc, j = e - i * nc;
+      if (j <= i) L[i * BMAX + j] = sh.red[j * nc - j * (j - 1) / 2 + (i - j)] + (i == j ? shift : 0.0);
     }
+    __syncwarp();
     bool ok = true;
-#pragma unroll
-    for (int k = 0; k < BMAX; ++k) {
-      if (k < nc) {
-        const double d = __shfl_sync(0xffffffffu, a[k], k);
-        if (!(d > 0.0)) ok = false;
-        // one reciprocal square root per pivot on the dependent chain
-        const double inv = d > 0.0 ? rsqrt_fast(d) : 0.0;
-        const double l = d > 0.0 ? d * inv : 0.0;
-        if (lane == k) a[k] = l;
-        if (lane > k) a[k] *= inv;
-        // trailing update: a[j] -= L(lane,k) L(j,k) for k < j <= lane
-#pragma unroll
-        for (int j = k + 1; j < BMAX; ++j) {
-          const double ljk = __shfl_sync(0xffffffffu, a[k], j);
-          if (j < nc && j <= lane) a[j] = fma(-a[k], ljk, a[j]);
+#pragma unroll 1
+    for (int k = 0; k < nc; ++k) {
+      const double d = L[k * BMAX + k];
+      if (!(d > 0.0)) ok = false;
+      const double inv = d > 0.0 ? rsqrt_fast(d) : 0.0;
+      __syncwarp();
+      if (lane == 0) L[k * BMAX + k] = d > 0.0 ? d * inv : 0.0;
+      if (k + 1 + lane < nc) L[(k + 1 + lane) * BMAX + k] *= inv;
+      __syncwarp();
+      // trailing update L(i, j) -= L(i, k) L(j, k), k < j <= i
+      const int m = nc - k - 1;
+#pragma unroll 1
+      for (int e = lane; e < m * m; e += 32) {
+        const int ii = e / m, jj = e - ii * m;
+        if (jj <= ii) {
+          const int i = k + 1 + ii, j = k + 1 + jj;
+          L[i * BMAX + j] = fma(-L[i * BMAX + k], L[j * BMAX + k], L[i * BMAX + j]);
         }
       }
+      __syncwarp();
     }
+    if (blockIdx.x == 0 && lane == 0) sh.flag[3] += 1;  // attempts (statistics)
     if (__all_sync(0xffffffffu, ok)) break;
     shift = (shift == 0.0) ? 1e-14 * tr : shift * 100.0;
   }
-  if (lane < nc) {
-    double dg = 1.0;
-#pragma unroll
-    for (int j = 0; j < BMAX; ++j) {
-      if (j <= lane) sh.S[lane * BMAX + j] = a[j];
-      if (j == lane) dg = a[j];
-    }
-    sh.dinv[lane] = 1.0 / dg;
-  }
+  if (lane < nc) sh.dinv[lane] = 1.0 / L[lane * BMAX + lane];
   __syncwarp();
 }
 
@@ -334,7 +331,9 @@ __device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, double
   grid_reduce(a, grid, buf, P + 1, 0, pw, sh);
   long long t2 = clock64();
   buf ^= 1;
-  chol_small(nc, sh);
+  // the first pass after a filter (pc >= 0) meets a Gram conditioned up to
+  // the filter's amplification: it may start from the shift its retry would reach
+  chol_small(nc, sh, pc >= 0 ? a.shift0 : 0.0);
   __syncthreads();
   long long t3 = clock64();
   apply_rinv(X, Xo, nc, ld, row_lo, nr, sh);
@@ -356,13 +355,26 @@ __device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, double
   __syncthreads();
 }
 
+// CTA 0, thread 0, last: Ritz values, statistics and status straight into the
+// caller's pinned host block (no device->host copies on the stream):
+// [0, 32) w, [32, 64) dstat, [64, 68) istat
+__device__ void publish(const EigArgs& a) {
+  if (!a.hout) return;
+  for (int j = 0; j < a.b; ++j) a.hout[j] = a.w[j];
+  for (int i = 0; i < 32; ++i) a.hout[32 + i] = a.dstat[i];
+  int* hi = reinterpret_cast<int*>(a.hout + 64);
+  for (int i = 0; i < 8; ++i) hi[i] = a.istat[i];
+}
+
 }  // namespace
 
 template <int NC>
 __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   cg::grid_group grid = cg::this_grid();
+  const long long t_start = clock64();
   __shared__ EigShared sh;
-  if (blockIdx.x == 0 && threadIdx.x < 8) a.dstat[16 + threadIdx.x] = 0.0;
+  if (blockIdx.x == 0 && threadIdx.x < 16) a.dstat[16 + threadIdx.x] = 0.0;
+  if (threadIdx.x == 0) sh.flag[3] = 0;
   extern __shared__ __align__(16) double dyn[];
   const int tid = threadIdx.x;
   const int64_t n = a.n;
@@ -380,6 +392,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       a.istat[3] = 0;
       a.istat[4] = 0;
       for (int i = 0; i < 16; ++i) a.dstat[i] = 0.0;
+      publish(a);
     }
     return;
   }
@@ -393,12 +406,6 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   double* gdyn = dyn + 4 * own;
   const double* gs = nullptr;
   double* xs = gdyn + (a.gres ? (((int64_t)a.rows_per_cta * n + 1) & ~int64_t(1)) : 0);
-  if (a.gres) {
-    const int64_t tot = (int64_t)(row_hi - row_lo) * n;
-    const double* src = a.G + (int64_t)row_lo * n;
-    for (int64_t e = tid; e < tot; e += ET) gdyn[e] = __ldg(src + e);
-    gs = gdyn;
-  }
   unsigned xphase = 0;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&sh.xbar)),
@@ -406,6 +413,37 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  if (a.gres) {
+    // the CTA's rows of G (written by the previous kernel): one bulk copy on
+    // the iterate's mbarrier when n is even (16-byte rows), else a plain loop
+    const int64_t tot = (int64_t)(row_hi - row_lo) * n;
+    const double* src = a.G + (int64_t)row_lo * n;
+    if ((n & 1) == 0 && tot > 0) {
+      const unsigned bar = (unsigned)__cvta_generic_to_shared(&sh.xbar);
+      if (tid == 0) {
+        const unsigned bytes = (unsigned)(tot * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                (unsigned)__cvta_generic_to_shared(gdyn)),
+            "l"(src), "r"(bytes), "r"(bar)
+            : "memory");
+      }
+      unsigned done = 0;
+      do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(xphase)
+            : "memory");
+      } while (!done);
+      xphase ^= 1u;
+    } else {
+      for (int64_t e = tid; e < tot; e += ET) gdyn[e] = __ldg(src + e);
+      __syncthreads();
+    }
+    gs = gdyn;
+  }
 
   // ---- ub: an upper bound of the spectrum ----
   // With the accumulator's structure G = diag(count) - sum E V V^T E^T (a PSD
@@ -453,7 +491,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   }
   __syncthreads();
   // the random start block is well conditioned: one CholQR orthonormalises it
-  if (!full) cholqr(a, grid, X, Xo, b, ld, pcol, row_lo, nr, buf, pw, sh);
+  if (!full && a.init_cq) cholqr(a, grid, X, Xo, b, ld, pcol, row_lo, nr, buf, pw, sh);
 
   double acut = 0.5 * ub;
   double maxres = 0.0, lmax = 0.0;
@@ -462,6 +500,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   // [3] small eigensolve, [4] rotate+residual, [5] setup before the loop
   long long tacc[6] = {0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
+  const long long t_setup = tlast - t_start;  // G rows to smem, ub, initial CholQR
   const bool tme = blockIdx.x == 0 && tid == 0;
   long long jac_sweeps = 0, jac_cyc = 0, mv_cyc = 0, sync_cyc = 0;
 #define EIG_T(i)                          \
@@ -565,7 +604,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
           const int l = tid;
           double x = l < b ? 1.0 : 0.0;
           double yv = 0.0;
-          for (int itp = 0; itp < 48; ++itp) {
+          for (int itp = 0; itp < a.probe_its; ++itp) {
             yv = 0.0;
             for (int j = 0; j < b; ++j) {
               const double xj = __shfl_sync(0xffffffffu, x, j);
@@ -686,6 +725,7 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     if (acut <= 0.0) acut = 1e-6 * ub;
   }
   if (status == 1 && maxres <= 1e-9 * ub) status = 0;  // converged to a looser bound
+  const long long t_loop_end = clock64();
   // ---- outputs, sign-fixed (solver.cpp:47-60): each column's largest-
   // magnitude entry made positive, the first index winning ties. Per-CTA
   // candidates (signed value, row) -> partials, one grid sync, every CTA
@@ -703,15 +743,29 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       *pslot(a, buf, pw, r + tid) = nr > 0 ? (double)arg : -1.0;
     }
     grid.sync();
-    if (tid < r) {
-      const int nc = (int)gridDim.x;
-      double best = -1.0, val = 0.0;
-      for (int cta = 0; cta < nc; ++cta) {
-        const double x = a.part[((size_t)buf * pw + tid) * nc + cta];
-        const double id = a.part[((size_t)buf * pw + r + tid) * nc + cta];
-        if (id >= 0.0 && fabs(x) > best) { best = fabs(x); val = x; }
+    {
+      // warp j scans column j's candidates: lane l takes a contiguous run of
+      // CTAs (first maximum within it), then an arg-max butterfly in which the
+      // lower CTA index wins ties -- the first index over the whole column
+      const int warp = tid >> 5, lane = tid & 31;
+      const int nc = (int)gridDim.x, per = (nc + 31) / 32;
+      for (int j = warp; j < r; j += ET / 32) {
+        double best = -1.0, val = 0.0;
+        int at = nc;
+        for (int cta = lane * per; cta < nc && cta < (lane + 1) * per; ++cta) {
+          const double x = a.part[((size_t)buf * pw + j) * nc + cta];
+          const double id = a.part[((size_t)buf * pw + r + j) * nc + cta];
+          if (id >= 0.0 && fabs(x) > best) { best = fabs(x); val = x; at = cta; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+          const double v2 = __shfl_xor_sync(0xffffffffu, val, o);
+          const int a2 = __shfl_xor_sync(0xffffffffu, at, o);
+          if (b2 > best || (b2 == best && a2 < at)) { best = b2; val = v2; at = a2; }
+        }
+        if (lane == 0) flip[j] = val < 0.0 ? -1.0 : 1.0;
       }
-      flip[tid] = val < 0.0 ? -1.0 : 1.0;
     }
     __syncthreads();
     for (int q = tid; q < nr * r; q += ET) {
@@ -732,6 +786,12 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
     a.dstat[10] = (double)jac_cyc;
     a.dstat[11] = (double)mv_cyc;
     a.dstat[12] = (double)sync_cyc;
+    a.dstat[20] = (double)sync_cyc;  // grid syncs before the filter's matvecs
+    a.dstat[21] = (double)t_setup;
+    a.dstat[22] = (double)(clock64() - t_loop_end);  // sign fix + outputs
+    a.dstat[23] = (double)(clock64() - t_start);
+    a.dstat[24] = (double)sh.flag[3];
+    publish(a);
   }
 #undef EIG_T
 }

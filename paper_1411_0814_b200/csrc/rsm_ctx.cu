@@ -216,7 +216,7 @@ struct rsm_ctx {
 
   cudaEvent_t ev[8] = {};
   double stage_ms[8] = {};
-  double solver_stats[24] = {};  // eig: outer its, matvecs, lambda_max, ub, max residual, block, grid
+  double solver_stats[32] = {};  // eig: outer its, matvecs, lambda_max, ub, max residual, block, grid
   int64_t launches = 0;
   // held by the one-shot calls (rsm_decompose, rsm_solve_u, ...) from the load
   // through the last device->host copy: those share one context per device, and
@@ -885,16 +885,28 @@ EigLaunch solve_v_launch(rsm_ctx* c, int64_t n, int64_t r, double tol) {
     return e ? atoi(e) : 1;
   }();
   a.rr0_probe = rr0_probe;
+  static const int init_cq = [] {
+    const char* e = getenv("RSM_EIG_INITCQ");
+    return e ? atoi(e) : 0;
+  }();
+  a.init_cq = init_cq;
+  static const double shift0 = [] {
+    const char* e = getenv("RSM_EIG_SHIFT0");
+    return e ? atof(e) : 1e-14;
+  }();
+  a.shift0 = shift0;
+  static const int probe_its = [] {
+    const char* e = getenv("RSM_EIG_PROBE_ITS");
+    return e ? std::max(1, atoi(e)) : 16;
+  }();
+  a.probe_its = probe_its;
   a.cnt = c->G_harvest ? c->colcnt.as<int>() : nullptr;
   a.zero_rows = c->eI.as<int>() + 7;
   rsmk::launch_zero_rows(a.G, n, a.cnt, c->eI.as<int>() + 7, c->stream);
   ++c->launches;
+  a.hout = pinned_small(c);  // the kernel writes its scalars to pinned host memory itself
   ck(rsmk::launch_eig(a, grid, c->stream), "cooperative eig launch");  // sign fix included
   c->launches += 1;
-  double* hs = pinned_small(c);
-  ck(cudaMemcpyAsync(hs, c->eW.p, sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream), "D2H");
-  ck(cudaMemcpyAsync(hs + 32, c->eD.p, sizeof(double) * 32, cudaMemcpyDeviceToHost, c->stream), "D2H");
-  ck(cudaMemcpyAsync(hs + 64, c->eI.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
   EigLaunch L;
   L.b = b;
   L.grid = grid;
@@ -923,7 +935,7 @@ SolveVOut solve_v_finish(rsm_ctx* c, const EigLaunch& L, int64_t n, int64_t r, d
   c->solver_stats[13] = dstat[9];   // Rayleigh-Ritz Jacobi sweeps (total)
   c->solver_stats[14] = dstat[10];  // and their cycles
   c->solver_stats[15] = dstat[11];  // filter matvec cycles (CTA 0)
-  for (int i = 0; i < 8; ++i) c->solver_stats[16 + i] = dstat[16 + i];  // CholQR sub-phase cycles
+  for (int i = 0; i < 16; ++i) c->solver_stats[16 + i] = dstat[16 + i];  // CholQR sub-phases, tail, counters
   if (istat[0] == 3)  // certified: more than r eigenvalues at or below tol * lambda_max
     fail(RSM_ERR_INSUFFICIENT_COVERAGE,
          "rank gate failed: constraint coverage below n-r; raise the trial count or epsilon");
@@ -1649,7 +1661,7 @@ int64_t rsm_ctx_rerun_count(rsm_ctx* c) { return c ? c->spec_reruns : 0; }
 int64_t rsm_ctx_last_load_h2d_bytes(rsm_ctx* c) { return c ? c->last_h2d : 0; }
 
 int rsm_ctx_solver_stats(rsm_ctx* c, double* out, int cap) {
-  const int k = std::min(cap, 24);
+  const int k = std::min(cap, 32);
   for (int i = 0; i < k; ++i) out[i] = c->solver_stats[i];
   return k;
 }

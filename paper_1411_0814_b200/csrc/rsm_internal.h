@@ -111,6 +111,10 @@ struct EigArgs {
   double amp;       // Chebyshev filter amplification cap (degree choice)
   int dmax;         // and degree cap
   int rr0_probe;     // first outer iteration: top Ritz value by power iteration only
+  double* hout;      // pinned host block for w / dstat / istat (see k_eig.cu publish), or null
+  int init_cq;       // CholQR of the random start block (0: the first filter takes it as is)
+  double shift0;     // relative diagonal shift of the first CholQR pass after a filter
+  int probe_its;     // power iterations of the probe round
 };
 
 struct SolveUArgs {

@@ -461,11 +461,12 @@ class Context:
         return int(lib().rsm_ctx_last_load_h2d_bytes(self.h))
 
     def solver_stats(self) -> dict:
-        buf = (C.c_double * 24)()
-        k = lib().rsm_ctx_solver_stats(self.h, C.cast(buf, C.c_void_p), 24)
+        buf = (C.c_double * 32)()
+        k = lib().rsm_ctx_solver_stats(self.h, C.cast(buf, C.c_void_p), 32)
         keys = ["outer", "matvecs", "lambda_max", "ub", "max_residual", "block", "grid", "cyc_filter",
                 "cyc_cholqr", "cyc_rr", "cyc_eig", "cyc_rotate", "cyc_setup", "jac_sweeps", "cyc_jacobi", "cyc_matvec", "cyc_cq_gram", "cyc_cq_reduce", "cyc_cq_chol",
-                "cyc_cq_apply", "cyc_x4", "cyc_x5", "cyc_x6", "cyc_x7"]
+                "cyc_cq_apply", "cyc_sync", "cyc_setup_all", "cyc_tail", "cyc_kernel", "chol_attempts",
+                "cyc_probe", "x26", "x27", "x28", "x29", "x30", "x31"]
         return dict(zip(keys, buf[:k]))
 
 

@@ -47,6 +47,60 @@ __device__ __noinline__ void chol_v1(const double* red, int nc, double* S, doubl
   __syncwarp();
 }
 
+// rolled, in shared memory (k_eig.cu chol_small since round 2)
+__device__ __noinline__ void chol_v2(const double* red, int nc, double* L, double* dinv) {
+  const int lane = threadIdx.x;
+#pragma unroll 1
+  for (int e = lane; e < nc * nc; e += 32) {
+    const int i = e / nc, j = e - i * nc;
+    if (j <= i) L[i * BMAX + j] = red[j * nc - j * (j - 1) / 2 + (i - j)];
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int k = 0; k < nc; ++k) {
+    const double d = L[k * BMAX + k];
+    const double inv = d > 0.0 ? rsqrt_fast(d) : 0.0;
+    __syncwarp();
+    if (lane == 0) L[k * BMAX + k] = d > 0.0 ? d * inv : 0.0;
+    if (k + 1 + lane < nc) L[(k + 1 + lane) * BMAX + k] *= inv;
+    __syncwarp();
+    const int m = nc - k - 1;
+#pragma unroll 1
+    for (int e = lane; e < m * m; e += 32) {
+      const int ii = e / m, jj = e - ii * m;
+      if (jj <= ii) {
+        const int i = k + 1 + ii, j = k + 1 + jj;
+        L[i * BMAX + j] = fma(-L[i * BMAX + k], L[j * BMAX + k], L[i * BMAX + j]);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane < nc) dinv[lane] = 1.0 / L[lane * BMAX + lane];
+  __syncwarp();
+}
+
+__global__ void bench2(double* out, long long* cyc) {
+  __shared__ double red[200], S[BMAX * BMAX], dinv[BMAX];
+  const int lane = threadIdx.x;
+  const int nc = 10;
+  for (int p = lane; p < nc * (nc + 1) / 2; p += 32) red[p] = 0.01 * ((p * 37) % 11);
+  if (lane < nc) red[lane * nc - lane * (lane - 1) / 2] = nc + lane;
+  __syncwarp();
+  long long t0 = clock64();
+  chol_v1(red, nc, S, dinv);
+  long long t1 = clock64();
+  chol_v1(red, nc, S, dinv);
+  long long t2 = clock64();
+  chol_v2(red, nc, S, dinv);
+  long long t3 = clock64();
+  chol_v2(red, nc, S, dinv);
+  long long t4 = clock64();
+  if (lane == 0) {
+    cyc[0] = t1 - t0; cyc[1] = t2 - t1; cyc[2] = t3 - t2; cyc[3] = t4 - t3;
+    out[0] = S[5 * BMAX + 3] + dinv[2];
+  }
+}
+
 __global__ void bench(double* out, long long* cyc) {
   __shared__ double red[200], S[BMAX * BMAX], dinv[BMAX], H[BMAX * BMAX], V[BMAX * BMAX];
   const int lane = threadIdx.x;
@@ -81,5 +135,10 @@ int main() {
   cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
   printf("chol_small(11): %lld cycles; jacobi_reg<10>: %lld cycles, %lld sweeps (%s)\n", h[0], h[1], h[2],
          cudaGetErrorString(cudaGetLastError()));
+  long long h2[4];
+  bench2<<<1, 32>>>(o, c);
+  cudaMemcpy(h2, c, sizeof(h2), cudaMemcpyDeviceToHost);
+  printf("chol(10) unrolled/shuffle: first %lld, second %lld; rolled/smem: first %lld, second %lld cycles\n", h2[0],
+         h2[1], h2[2], h2[3]);
   return 0;
 }
