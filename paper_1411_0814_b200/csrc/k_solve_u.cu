@@ -815,6 +815,229 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_fused(SolveUArgs a) {
   }
 }
 
+// Row solver for precomputed normal matrices (a.Apre from k_normal_i8.cu,
+// r <= 4, n even): per row only V_O^T y, the observed count and the direct
+// residual remain, so a warp keeps ONE staged row: row k+1 arrives in the
+// warp's buffer by TMA (values; its mask words into one of two small word
+// buffers) and is accumulated while the residual of row k -- staged one row
+// earlier and still in L2 -- is formed from global loads in the same column
+// loop (every V-hat read in shared memory serves both rows). Half the row
+// buffers of k_solve_u_fused, so 16 warps per SM instead of 11 (V-hat stays
+// in shared memory), and the per-row reduction carries R + 2 values instead of
+// the normal matrix's. Same arithmetic per cell as k_solve_u_fused (the
+// residual, the selects and the FMA order are identical), same results.
+template <int R>
+__global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_pre(SolveUArgs a) {
+  constexpr int NP = (R + 1) / 2;
+  constexpr int NA = R * (R + 1) / 2;
+  constexpr int NV = pow2_at_least(R + 2);  // b, count, previous row's residual
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int nwarps = blockDim.x >> 5;
+  const int nwn = (int)((n + 31) >> 5);
+  const int64_t mwd = ((a.nwp + 3) & ~int64_t(3)) / 2;  // one row's mask words, in doubles (16-byte multiple)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);  // [SU_MAXW]
+  double2* Vp = reinterpret_cast<double2*>(sm + SU_MAXW);
+  double* wb = sm + SU_MAXW + 2 * NP * n;
+  const int64_t bufd = n + 2 * mwd;  // values, then two mask-word slots
+  double* ybuf = wb + warp * bufd;
+  auto mbuf = [&](int s) { return reinterpret_cast<uint32_t*>(ybuf + n + s * mwd); };
+  if (threadIdx.x < nwarps)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + threadIdx.x)), "r"(1));
+  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  for (int64_t e = threadIdx.x; e < NP * n; e += blockDim.x) {
+    const int64_t p = e / n, c = e % n;
+    const double x0 = a.V[c * R + 2 * p];
+    const double x1 = (2 * p + 1 < R) ? a.V[c * R + 2 * p + 1] : 0.0;
+    Vp[e] = make_double2(x0, x1);
+  }
+  __syncthreads();
+  auto vload = [&](int64_t c, double* v) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double2 t = Vp[p * n + c];
+      v[2 * p] = t.x;
+      if (2 * p + 1 < R) v[2 * p + 1] = t.y;
+    }
+  };
+  const uint32_t ybytes = (uint32_t)(n * 8), wbytes = (uint32_t)(a.nwp * 4);
+  const unsigned bar = smem_u32(bars + warp);
+  auto issue = [&](int64_t row, int slot) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(ybytes + wbytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              smem_u32(ybuf)),
+          "l"(a.Y + row * n), "r"(ybytes), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              smem_u32(mbuf(slot))),
+          "l"(a.bitsR + row * a.nwp), "r"(wbytes), "r"(bar)
+          : "memory");
+    }
+  };
+  auto prefetch_l2 = [&](int64_t row) {
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.Y + row * n), "r"(ybytes) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.bitsR + row * a.nwp), "r"(wbytes)
+                   : "memory");
+    }
+  };
+  unsigned phase = 0u;
+  auto wait_buf = [&]() {
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar), "r"(phase)
+          : "memory");
+    } while (!done);
+    phase ^= 1u;
+  };
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t nw = (int64_t)gridDim.x * nwarps;
+  const int64_t r0 = a.row_lo + gw;
+  if (r0 >= a.row_hi) return;
+  const int64_t nrows = (a.row_hi - r0 + nw - 1) / nw;  // this warp's rows: r0 + k nw
+  const int nfull = (int)(n >> 5);
+  const bool tail = (int64_t)nfull * 32 + lane < n;
+  auto accum_b = [&](double* acc, const double* v, double yraw, bool k) {
+    const double yc = k ? yraw : 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[i] = fma(yc, v[i], acc[i]);
+  };
+  auto resid = [&](double& ss, const double* v, const double* nu, double yraw, bool k) {
+    double d = yraw;
+#pragma unroll
+    for (int q = 0; q < R; ++q) d = fma(nu[q], v[q], d);
+    d = k ? d : 0.0;
+    ss = fma(d, d, ss);
+  };
+  // count, one reduction of b / count / the previous row's residual, solve
+  auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u, double& ss_prev, int64_t frow) -> bool {
+    int cnt = 0;
+    for (int w = lane; w < nwn; w += 32) cnt += __popc(wd[w]);
+    acc[R] = (double)cnt;
+    acc[R + 1] = ss_prev;
+    warp_reduce_halving<NV>(acc, lane);
+    double A[NA], bv[R];
+    const double* ap = a.Apre + frow * NA;
+    if constexpr (NA % 2 == 0) {
+#pragma unroll
+      for (int p = 0; p < NA / 2; ++p) {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(ap) + p);
+        A[2 * p] = t.x;
+        A[2 * p + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < NA; ++p) A[p] = __ldg(ap + p);
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, i);
+    const int nj = (int)warp_total<NV>(acc, R);
+    ss_prev = warp_total<NV>(acc, R + 1);
+    const bool fl = row_solve<R>(A, bv, nj, u);
+    if (a.Ugiven) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) u[q] = a.Ugiven[frow * R + q];
+      return false;
+    }
+    return fl;
+  };
+  // row 0: accumulation pass alone
+  double u[R];
+  bool flagged;
+  issue(r0, 0);
+  {
+    wait_buf();
+    const uint32_t* wd = mbuf(0);
+    double acc[NV];
+#pragma unroll
+    for (int p = 0; p < NV; ++p) acc[p] = 0.0;
+#pragma unroll 4
+    for (int w = 0; w < nfull; ++w) {
+      const int64_t c = w * 32 + lane;
+      double v[R];
+      vload(c, v);
+      accum_b(acc, v, ybuf[c], (wd[w] >> lane) & 1u);
+    }
+    if (tail) {
+      const int64_t c = (int64_t)nfull * 32 + lane;
+      double v[R];
+      vload(c, v);
+      accum_b(acc, v, ybuf[c], (wd[nfull] >> lane) & 1u);
+    }
+    double none = 0.0;
+    flagged = finish(acc, wd, u, none, r0);
+  }
+  for (int64_t k = 0; k < nrows; ++k) {
+    const int64_t row = r0 + k * nw;
+    const uint32_t* wd = mbuf((int)(k & 1));
+    const uint32_t* wn = mbuf((int)((k + 1) & 1));
+    const double* yg = a.Y + row * n;  // row k: staged one row ago, read back through L2
+    const bool has_next = k + 1 < nrows;
+    if (has_next) issue(row + nw, (int)((k + 1) & 1));  // the buffer is free: row k was accumulated
+    if (k + 2 < nrows) prefetch_l2(r0 + (k + 2) * nw);
+    double nu[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) nu[q] = -u[q];
+    double ss = 0.0;
+    double acc[NV];
+#pragma unroll
+    for (int p = 0; p < NV; ++p) acc[p] = 0.0;
+    if (has_next) {
+      wait_buf();
+#pragma unroll 4
+      for (int w = 0; w < nfull; ++w) {
+        const int64_t c = w * 32 + lane;
+        double v[R];
+        vload(c, v);
+        resid(ss, v, nu, __ldg(yg + c), (wd[w] >> lane) & 1u);
+        accum_b(acc, v, ybuf[c], (wn[w] >> lane) & 1u);
+      }
+      if (tail) {
+        const int64_t c = (int64_t)nfull * 32 + lane;
+        double v[R];
+        vload(c, v);
+        resid(ss, v, nu, __ldg(yg + c), (wd[nfull] >> lane) & 1u);
+        accum_b(acc, v, ybuf[c], (wn[nfull] >> lane) & 1u);
+      }
+    } else {
+#pragma unroll 4
+      for (int w = 0; w < nfull; ++w) {
+        const int64_t c = w * 32 + lane;
+        double v[R];
+        vload(c, v);
+        resid(ss, v, nu, __ldg(yg + c), (wd[w] >> lane) & 1u);
+      }
+      if (tail) {
+        const int64_t c = (int64_t)nfull * 32 + lane;
+        double v[R];
+        vload(c, v);
+        resid(ss, v, nu, __ldg(yg + c), (wd[nfull] >> lane) & 1u);
+      }
+    }
+    if (lane < R) {
+      double uk = 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == lane) uk = u[q];
+      a.U[row * R + lane] = uk;
+    }
+    if (lane == 0 && flagged) atomicAdd(a.flagged, 1);
+    if (has_next) flagged = finish(acc, wn, u, ss, row + nw);  // ss: row k's residual, summed
+    else ss = warp_sum(ss);
+    if (lane == 0) a.rowres[row] = ss;
+    __syncwarp();  // every lane is done with the word slot the next issue overwrites
+  }
+}
+
 // deterministic single-CTA sum of n doubles (fixed strided order + tree)
 __global__ void k_sum_rows(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
   __shared__ double part[1024];
@@ -896,6 +1119,25 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
     if constexpr (R <= 4) {
       constexpr int NA = R * (R + 1) / 2;
       const size_t wgram = sizeof(double) * (((size_t)((a.n + 31) / 32) * NA + 1) & ~(size_t)1);
+      // tensor-core normal matrices: one staged row per warp (k_solve_u_pre)
+      static const bool pre_on = [] {
+        const char* e = getenv("RSM_SU_PRE");
+        return !(e && atoi(e) == 0);
+      }();
+      const size_t mwd = (size_t)((a.nwp + 3) & ~int64_t(3)) / 2;
+      const size_t per_warp1 = sizeof(double) * ((size_t)a.n + 2 * mwd);
+      const size_t headp = sizeof(double) * SU_MAXW;
+      if (a.Apre && bulk && pre_on && headp + vbytes + 8 * per_warp1 <= 227 * 1024 - 1024) {
+        int w = (int)std::min<size_t>(SU_MAXW, (227 * 1024 - 1024 - headp - vbytes) / per_warp1);
+        if (w < 1) w = 1;
+        const size_t smem = headp + vbytes + (size_t)w * per_warp1;
+        const int64_t rows = a.row_hi - a.row_lo;
+        int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
+        if (blocks < 1) blocks = 1;
+        ensure_smem((const void*)k_solve_u_pre<R>, smem);
+        k_solve_u_pre<R><<<(unsigned)blocks, w * 32, smem, s>>>(a);
+        return;
+      }
       if (bulk && !fused_off && head + vbytes + wgram + 8 * per_warp <= cap) {
         const size_t capw = 227 * 1024 - 1024;  // the kernel has no static shared memory
         int w = (int)std::min<size_t>(SU_MAXW, (capw - head - vbytes - wgram) / per_warp);
