@@ -906,17 +906,21 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_pre(SolveUArgs a) {
   const int64_t nrows = (a.row_hi - r0 + nw - 1) / nw;  // this warp's rows: r0 + k nw
   const int nfull = (int)(n >> 5);
   const bool tail = (int64_t)nfull * 32 + lane < n;
+  const unsigned lbit = 1u << lane;
+  // predicated on the mask bit (no selects): a hidden cell's NaN never
+  // enters an executed instruction, and skipping adds nothing the selected-zero
+  // form would (acc + 0 * v == acc, ss + 0 * 0 == ss)
   auto accum_b = [&](double* acc, const double* v, double yraw, bool k) {
-    const double yc = k ? yraw : 0.0;
+    if (k) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) acc[i] = fma(yc, v[i], acc[i]);
+      for (int i = 0; i < R; ++i) acc[i] = fma(yraw, v[i], acc[i]);
+    }
   };
   auto resid = [&](double& ss, const double* v, const double* nu, double yraw, bool k) {
     double d = yraw;
 #pragma unroll
     for (int q = 0; q < R; ++q) d = fma(nu[q], v[q], d);
-    d = k ? d : 0.0;
-    ss = fma(d, d, ss);
+    if (k) ss = fma(d, d, ss);
   };
   // count, one reduction of b / count / the previous row's residual, solve
   auto finish = [&](double (&acc)[NV], const uint32_t* wd, double* u, double& ss_prev, int64_t frow) -> bool {
@@ -993,13 +997,45 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_pre(SolveUArgs a) {
     for (int p = 0; p < NV; ++p) acc[p] = 0.0;
     if (has_next) {
       wait_buf();
-#pragma unroll 4
-      for (int w = 0; w < nfull; ++w) {
-        const int64_t c = w * 32 + lane;
+      // running pointers (immediate offsets in the unrolled body)
+      const double* yp = yg + lane;
+      const double* yb = ybuf + lane;
+      const double2* vq = Vp + lane;
+      // groups of four words: both rows' mask words by one 16-byte load each
+      const int nq = nfull >> 2;
+      for (int g = 0; g < nq; ++g) {
+        const uint4 md = reinterpret_cast<const uint4*>(wd)[g];
+        const uint4 mn = reinterpret_cast<const uint4*>(wn)[g];
+        const unsigned dw[4] = {md.x, md.y, md.z, md.w}, nw4[4] = {mn.x, mn.y, mn.z, mn.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double v[R];
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            const double2 t = vq[p * n + 32 * j];
+            v[2 * p] = t.x;
+            if (2 * p + 1 < R) v[2 * p + 1] = t.y;
+          }
+          resid(ss, v, nu, __ldg(yp + 32 * j), (dw[j] & lbit) != 0u);
+          accum_b(acc, v, yb[32 * j], (nw4[j] & lbit) != 0u);
+        }
+        yp += 128;
+        yb += 128;
+        vq += 128;
+      }
+      for (int w = nq << 2; w < nfull; ++w) {
         double v[R];
-        vload(c, v);
-        resid(ss, v, nu, __ldg(yg + c), (wd[w] >> lane) & 1u);
-        accum_b(acc, v, ybuf[c], (wn[w] >> lane) & 1u);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const double2 t = vq[p * n];
+          v[2 * p] = t.x;
+          if (2 * p + 1 < R) v[2 * p + 1] = t.y;
+        }
+        resid(ss, v, nu, __ldg(yp), (wd[w] >> lane) & 1u);
+        accum_b(acc, v, *yb, (wn[w] >> lane) & 1u);
+        yp += 32;
+        yb += 32;
+        vq += 32;
       }
       if (tail) {
         const int64_t c = (int64_t)nfull * 32 + lane;
