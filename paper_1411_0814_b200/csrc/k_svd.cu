@@ -23,6 +23,7 @@
 // popcount prefix (the compact-index map stage 3 needs), and the per-column
 // trial counts (the identity's diagonal) with integer atomics.
 #include <algorithm>
+#include <type_traits>
 
 #include "rsm_internal.h"
 #include "rsm_dev.cuh"
@@ -800,22 +801,41 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     // (cp.async), so all of a trial's K x L loads are in flight at once and
     // the warp waits for them once (one memory round trip per trial)
     {
-      const unsigned sb = (unsigned)__cvta_generic_to_shared(S) + 8u * (unsigned)lane;  // + 8 c per cell
+      // four words per step: their support words and prefixes by one 16-byte
+      // shared-memory load each (cmw is a multiple of 4; words past n are 0),
+      // the copies' global addresses as immediate offsets of K running row
+      // pointers
+      const unsigned sb = (unsigned)__cvta_generic_to_shared(S);
+      const unsigned Lp8 = 8u * (unsigned)Lp;
       const double* yrow[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) yrow[i] = a.Y + (int64_t)rows[i] * a.n + lane;
+      int* cc = a.colcnt + lane;
       const uint32_t below = (1u << lane) - 1u;
-      for (int w = 0; 32 * (int64_t)w < a.n; ++w) {
-        const uint32_t word = cm[w];
-        if ((word >> lane) & 1u) {  // support bits exist only for j < n
-          const unsigned dst = sb + 8u * (unsigned)((int)pre[w] + __popc(word & below) - lane);
+      const uint32_t lbit = 1u << lane;
+      auto cell = [&](auto J, uint32_t word, uint32_t p) {
+        constexpr int OFF = decltype(J)::value;
+        if (word & lbit) {  // support bits exist only for j < n
+          unsigned dst = sb + 8u * (p + (unsigned)__popc(word & below));
 #pragma unroll
-          for (int i = 0; i < K; ++i)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * (unsigned)(i * Lp)),
-                         "l"(yrow[i] + 32 * (int64_t)w)
+          for (int i = 0; i < K; ++i) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1+%2], 8;\n" ::"r"(dst), "l"(yrow[i]), "n"(OFF * 256)
                          : "memory");
-          atomicAdd(a.colcnt + 32 * (int64_t)w + lane, 1);
+            dst += Lp8;
+          }
+          atomicAdd(cc + 32 * OFF, 1);
         }
+      };
+      for (int w = 0; w < (int)a.cmw; w += 4) {
+        const uint4 c4 = *reinterpret_cast<const uint4*>(cm + w);
+        const uint4 p4 = *reinterpret_cast<const uint4*>(pre + w);
+        cell(std::integral_constant<int, 0>{}, c4.x, p4.x);
+        cell(std::integral_constant<int, 1>{}, c4.y, p4.y);
+        cell(std::integral_constant<int, 2>{}, c4.z, p4.z);
+        cell(std::integral_constant<int, 3>{}, c4.w, p4.w);
+#pragma unroll
+        for (int i = 0; i < K; ++i) yrow[i] += 128;
+        cc += 128;
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -928,29 +948,48 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
         const int lmax = L > 0 ? L - 1 : 0;
         if (a.Wq) {
           // int8 digit slices (k_gram_i8.cu): lane = 4 consecutive columns
-          for (int64_t j0 = 4 * lane; j0 < a.npad; j0 += 128) {
-            double v[4][R1];
+          // V = S^T C first in compact form, in place over rows 0..r-1 of S
+          // (each support column once: L of them, not npad), then expanded
+          for (int c = lane; c < L; c += 32) {
+            double x[K], t[R1];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int64_t j = j0 + u;
-              const uint32_t word = cm[j >> 5], bit = 1u << (j & 31);
-              const bool in = (word & bit) != 0;
-              int c = (int)pre[j >> 5] + __popc(word & (bit - 1u));
-              c = c < lmax ? c : lmax;
-              double x[K];
+            for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
 #pragma unroll
-              for (int i = 0; i < K; ++i) x[i] = S[i * Lp + c];
+            for (int p = 0; p < R1; ++p) {
+              double acc = 0.0;
 #pragma unroll
-              for (int p = 0; p < R1; ++p) {
-                double t = 0.0;
-#pragma unroll
-                for (int i = 0; i < K; ++i) t = fma(x[i], cf[i][p], t);
-                v[u][p] = in ? t : 0.0;
-              }
+              for (int i = 0; i < K; ++i) acc = fma(x[i], cf[i][p], acc);
+              t[p] = acc;
             }
 #pragma unroll
-            for (int p = 0; p < R1; ++p)
-              emit_slices4(a.S, a.Wq, a.Kpad, a.npad, tl * rex + p, j0, v[0][p], v[1][p], v[2][p], v[3][p]);
+            for (int p = 0; p < R1; ++p) S[p * Lp + c] = t[p];
+          }
+          __syncwarp();
+          const int64_t sstride = a.Kpad * a.npad;
+          int8_t* wq = a.Wq + tl * rex * a.npad + 4 * lane;
+          const int sh0 = (4 * lane) & 31;  // bit of the lane's first column within its word
+          for (int64_t j0 = 4 * lane; j0 < a.npad; j0 += 128, wq += 128) {
+            double v[4][R1];
+            const uint32_t word = cm[j0 >> 5];
+            int c0 = (int)pre[j0 >> 5] + __popc(word & ((1u << sh0) - 1u));
+            const uint32_t nib = (word >> sh0) & 15u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const bool in = (nib >> u) & 1u;
+              const int c = c0 < lmax ? c0 : lmax;
+#pragma unroll
+              for (int p = 0; p < R1; ++p) {
+                const double t = S[p * Lp + c];
+                v[u][p] = in ? t : 0.0;
+              }
+              c0 += in ? 1 : 0;
+            }
+            int8_t* wp = wq;
+#pragma unroll
+            for (int p = 0; p < R1; ++p) {
+              emit_slices4_at(a.S, wp, sstride, v[0][p], v[1][p], v[2][p], v[3][p]);
+              wp += a.npad;
+            }
           }
           __syncwarp();
           continue;

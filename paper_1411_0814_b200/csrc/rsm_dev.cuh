@@ -560,6 +560,32 @@ __device__ __forceinline__ void emit_slices4_t(int8_t* W, int64_t Kpad, int64_t 
   }
 }
 
+// The same with the address arithmetic hoisted: p = W + krow * npad + j0 (slice
+// 0), sstride = Kpad * npad bytes between slices (one 64-bit add per store).
+template <int S>
+__device__ __forceinline__ void emit_slices4_at_t(int8_t* p, int64_t sstride, double v0, double v1, double v2,
+                                                  double v3) {
+  const unsigned long long z0 = digits_i8<S>(v0), z1 = digits_i8<S>(v1), z2 = digits_i8<S>(v2),
+                           z3 = digits_i8<S>(v3);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int b = S - 1 - s;  // byte of digit a[s]
+    const int sh = b < 4 ? 0 : 32;
+    const unsigned q = (unsigned)(b & 3);
+    const unsigned t01 = __byte_perm((unsigned)(z0 >> sh), (unsigned)(z1 >> sh), q | ((4u + q) << 4));
+    const unsigned t23 = __byte_perm((unsigned)(z2 >> sh), (unsigned)(z3 >> sh), q | ((4u + q) << 4));
+    *reinterpret_cast<uint32_t*>(p) = __byte_perm(t01, t23, 0x5410);
+    p += sstride;
+  }
+}
+
+__device__ __forceinline__ void emit_slices4_at(int S, int8_t* p, int64_t sstride, double v0, double v1, double v2,
+                                                double v3) {
+  if (S == 5) emit_slices4_at_t<5>(p, sstride, v0, v1, v2, v3);
+  else if (S == 7) emit_slices4_at_t<7>(p, sstride, v0, v1, v2, v3);
+  else emit_slices4_at_t<6>(p, sstride, v0, v1, v2, v3);
+}
+
 __device__ __forceinline__ void emit_slices4(int S, int8_t* W, int64_t Kpad, int64_t npad, int64_t krow,
                                              int64_t j0, double v0, double v1, double v2, double v3) {
   if (S == 5) emit_slices4_t<5>(W, Kpad, npad, krow, j0, v0, v1, v2, v3);
