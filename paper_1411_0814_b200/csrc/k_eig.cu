@@ -244,56 +244,145 @@ __device__ void gram_partial(const EigArgs& a, const double* Xo, int nc, int ld,
   }
 }
 
-// warp 0: Cholesky of the nc x nc matrix given packed (upper) in sh.red;
-// lower factor to sh.S and its reciprocal diagonal to sh.dinv. Right-looking,
-// in place in shared memory with rolled loops: the routine runs a handful of
-// times per kernel, far apart, so its instructions are fetched cold each
-// time -- compact code beats a register-unrolled version (measured 3x).
+// Whole CTA (ET = 16 x 16 threads): Cholesky of the nc x nc matrix (nc <= 16)
+// given packed (upper) in sh.red; lower factor to sh.S and its reciprocal
+// diagonal to sh.dinv. Thread (i, j) keeps L(i, j) in a register; per step the
+// pivot's reciprocal square root and the scaled column go through sh.cs (two
+// CTA barriers), then every thread updates its own entry -- the arithmetic
+// and its order per entry are those of the right-looking loop (pivot d *
+// rsqrt(d), column * rsqrt(d), fma(-L(i,k), L(j,k), L(i,j)) for k ascending).
 // Retries with a diagonal shift when the matrix is not numerically positive.
-__device__ __noinline__ void chol_small(int nc, EigShared& sh, double shift0) {
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  double* L = sh.S;
+// (One warp working in shared memory took ~9 k cycles per 10 x 10 factor:
+// index divisions and three warp barriers per step.)
+__device__ void chol_cta(int nc, EigShared& sh, double shift0) {
+  const int tid = threadIdx.x, i = tid >> 4, j = tid & 15;
+  const bool live = i < nc && j <= i;
   double tr = 0.0;
-  for (int k = lane; k < nc; k += 32) tr += fabs(sh.red[k * nc - k * (k - 1) / 2]);
-  tr = warp_sum(tr);
+  for (int k = 0; k < nc; ++k) tr += fabs(sh.red[k * nc - k * (k - 1) / 2]);
   double shift = shift0 * tr;
+  const double a0 = live ? sh.red[j * nc - j * (j - 1) / 2 + (i - j)] : 0.0;
+  double l = 0.0;
 #pragma unroll 1
   for (int attempt = 0; attempt < 4; ++attempt) {
-#pragma unroll 1
-    for (int e = lane; e < nc * nc; e += 32) {
-      const int i = e / nc, j = e - i * nc;
-      if (j <= i) L[i * BMAX + j] = sh.red[j * nc - j * (j - 1) / 2 + (i - j)] + (i == j ? shift : 0.0);
-    }
-    __syncwarp();
+    l = a0 + ((live && i == j) ? shift : 0.0);
     bool ok = true;
 #pragma unroll 1
     for (int k = 0; k < nc; ++k) {
-      const double d = L[k * BMAX + k];
-      if (!(d > 0.0)) ok = false;
-      const double inv = d > 0.0 ? rsqrt_fast(d) : 0.0;
-      __syncwarp();
-      if (lane == 0) L[k * BMAX + k] = d > 0.0 ? d * inv : 0.0;
-      if (k + 1 + lane < nc) L[(k + 1 + lane) * BMAX + k] *= inv;
-      __syncwarp();
-      // trailing update L(i, j) -= L(i, k) L(j, k), k < j <= i
-      const int m = nc - k - 1;
-#pragma unroll 1
-      for (int e = lane; e < m * m; e += 32) {
-        const int ii = e / m, jj = e - ii * m;
-        if (jj <= ii) {
-          const int i = k + 1 + ii, j = k + 1 + jj;
-          L[i * BMAX + j] = fma(-L[i * BMAX + k], L[j * BMAX + k], L[i * BMAX + j]);
-        }
+      if (i == k && j == k) {
+        const double d = l;
+        ok = d > 0.0;
+        const double inv = ok ? rsqrt_fast(d) : 0.0;
+        l = ok ? d * inv : 0.0;
+        sh.cs[0] = inv;
       }
-      __syncwarp();
+      __syncthreads();
+      if (live && j == k && i > k) {
+        l *= sh.cs[0];
+        sh.cs[1 + i] = l;
+      }
+      __syncthreads();
+      if (live && j > k) l = fma(-sh.cs[1 + i], sh.cs[1 + j], l);
     }
-    if (blockIdx.x == 0 && lane == 0) sh.flag[3] += 1;  // attempts (statistics)
-    if (__all_sync(0xffffffffu, ok)) break;
+    if (blockIdx.x == 0 && tid == 0) sh.flag[3] += 1;  // attempts (statistics)
+    if (__syncthreads_and(ok ? 1 : 0)) break;
     shift = (shift == 0.0) ? 1e-14 * tr : shift * 100.0;
   }
-  if (lane < nc) sh.dinv[lane] = 1.0 / L[lane * BMAX + lane];
-  __syncwarp();
+  if (live) sh.S[i * BMAX + j] = l;
+  if (live && i == j) sh.dinv[i] = 1.0 / l;
+  __syncthreads();
+}
+
+// Whole CTA: cyclic Jacobi on the symmetric K x K matrix A (sh.H, leading
+// dimension BMAX, K <= 16) with the absolute threshold 16 eps ||A||_F
+// (warp_jacobi_abs's; LAPACK-level absolute eigenvalue accuracy). Thread
+// (i, j) keeps A(i, j) and V(i, j) in registers with shared-memory copies the
+// others read. Round-robin ordering: each step the Kp/2 pair threads form
+// their rotations (Rutishauser's formulas, two rsqrt and no division), then
+// every thread applies J^T A J and V J to its own entry from four (two)
+// neighbours: three CTA barriers per step instead of one warp's ~1.9 k cycles
+// of shuffles. The four products are summed (t1 + t4) + (t2 + t3), symmetric
+// in (i, j), so A stays exactly symmetric. On return A's diagonal holds the
+// eigenvalues and V (sh.S) the vectors in matching column order. Returns the
+// sweep count.
+__device__ int jacobi_cta(double* A, double* V, int K, EigShared& sh, int max_sweeps) {
+  const int tid = threadIdx.x, i = tid >> 4, j = tid & 15;
+  const int Kp = (K + 1) & ~1;
+  const bool live = i < K && j < K;
+  double a = live ? A[i * BMAX + j] : 0.0;
+  double v = (i == j) ? 1.0 : 0.0;
+  double* cs = sh.cs;      // [2 * BMAX]: c_i, sigma_i of index i's rotation
+  int* part = sh.pairs;    // [BMAX]: partner of index i (itself: no rotation)
+  {
+    double f = warp_sum(a * a);
+    if ((tid & 31) == 0) sh.red2[tid >> 5] = f;
+    V[i * BMAX + j] = v;
+    __syncthreads();
+    f = 0.0;
+    for (int w = 0; w < ET / 32; ++w) f += sh.red2[w];
+    cs[2 * BMAX] = fmax(16.0 * 2.220446049250313e-16 * sqrt(f), 1e-300);
+    __syncthreads();
+  }
+  const double thr = cs[2 * BMAX];
+  if (K < 2) return 0;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (!__syncthreads_or((live && i < j && fabs(a) > thr) ? 1 : 0)) break;
+#pragma unroll 1
+    for (int step = 0; step < Kp - 1; ++step) {
+      if (tid < Kp / 2) {
+        const int x = (tid == 0) ? 0 : ((tid - 1 + step) % (Kp - 1)) + 1;
+        const int y = ((Kp - 2 - tid + step) % (Kp - 1)) + 1;
+        const int p = x < y ? x : y, q = x < y ? y : x;
+        double c = 1.0, sn = 0.0;
+        if (q < K) {
+          const double off = A[p * BMAX + q];
+          if (fabs(off) > thr) {
+            const double dd = A[q * BMAX + q] - A[p * BMAX + p], ee = 2.0 * off;
+            const double r2 = fma(dd, dd, ee * ee);
+            const double rr = r2 * rsqrt_fast(r2);
+            const double w = rr + fabs(dd);
+            const double g = rsqrt_fast(2.0 * rr * w);
+            c = w * g;
+            sn = (dd >= 0.0 ? ee : -ee) * g;
+          }
+          part[p] = sn != 0.0 ? q : p;
+          part[q] = sn != 0.0 ? p : q;
+          cs[2 * p] = c;
+          cs[2 * p + 1] = -sn;  // x_p' = c x_p - s x_q
+          cs[2 * q] = c;
+          cs[2 * q + 1] = sn;   // x_q' = s x_p + c x_q
+        } else {
+          part[p] = p;
+          cs[2 * p] = 1.0;
+          cs[2 * p + 1] = 0.0;
+        }
+      }
+      __syncthreads();
+      double an = a, vn = v;
+      if (live) {
+        const int pi = part[i], pj = part[j];
+        const double ci = cs[2 * i], si = cs[2 * i + 1], cj = cs[2 * j], sj = cs[2 * j + 1];
+        if (pi != i || pj != j) {
+          const double t1 = __dmul_rn(__dmul_rn(ci, cj), a);
+          const double t2 = __dmul_rn(__dmul_rn(ci, sj), A[i * BMAX + pj]);
+          const double t3 = __dmul_rn(__dmul_rn(si, cj), A[pi * BMAX + j]);
+          const double t4 = __dmul_rn(__dmul_rn(si, sj), A[pi * BMAX + pj]);
+          an = __dadd_rn(__dadd_rn(t1, t4), __dadd_rn(t2, t3));
+          if (j == pi && i != j) an = 0.0;  // the rotated pair's off-diagonal entry
+        }
+        if (pj != j) vn = fma(cj, v, sj * V[i * BMAX + pj]);
+      }
+      __syncthreads();
+      if (live) {
+        A[i * BMAX + j] = an;
+        V[i * BMAX + j] = vn;
+      }
+      a = an;
+      v = vn;
+      __syncthreads();
+    }
+  }
+  return sweep;
 }
 
 // X(own rows) <- X R^{-1}, R = L^T with L in sh.S (smem copy and global)
@@ -333,8 +422,7 @@ __device__ void cholqr(const EigArgs& a, cg::grid_group& grid, double* X, double
   buf ^= 1;
   // the first pass after a filter (pc >= 0) meets a Gram conditioned up to
   // the filter's amplification: it may start from the shift its retry would reach
-  chol_small(nc, sh, pc >= 0 ? a.shift0 : 0.0);
-  __syncthreads();
+  chol_cta(nc, sh, pc >= 0 ? a.shift0 : 0.0);
   long long t3 = clock64();
   apply_rinv(X, Xo, nc, ld, row_lo, nr, sh);
   if (tme) {
@@ -629,28 +717,29 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
         if (acut <= 0.0) acut = 1e-6 * ub;
         continue;
       }
-      if (tid < 32) {
+      {
         const long long tj = clock64();
-        const int sw = warp_jacobi_abs(sh.H, BMAX, sh.S, BMAX, b, sh.cs, sh.pairs, 60);
+        const int sw = jacobi_cta(sh.H, sh.S, b, sh, 60);
         if (tme) {
           jac_sweeps += sw;
           jac_cyc += clock64() - tj;
         }
-        if (tid == 0) {
-          // ascending order: selection sort of eigenpairs
-          for (int i = 0; i < b; ++i) sh.theta[i] = sh.H[i * BMAX + i];
-          for (int i = 0; i < b; ++i) {
-            int mn = i;
-            for (int j = i + 1; j < b; ++j)
-              if (sh.theta[j] < sh.theta[mn]) mn = j;
-            if (mn != i) {
-              double t = sh.theta[i]; sh.theta[i] = sh.theta[mn]; sh.theta[mn] = t;
-              for (int k = 0; k < b; ++k) {
-                t = sh.S[k * BMAX + i]; sh.S[k * BMAX + i] = sh.S[k * BMAX + mn]; sh.S[k * BMAX + mn] = t;
-              }
-            }
+        // ascending order (ties: the lower index first, as a stable selection
+        // sort): eigenpair j moves to its rank
+        const int i = tid >> 4, j = tid & 15;
+        if (tid < b) {
+          const double th = sh.H[tid * BMAX + tid];
+          int rank = 0;
+          for (int k = 0; k < b; ++k) {
+            const double tk = sh.H[k * BMAX + k];
+            rank += (tk < th || (tk == th && k < tid)) ? 1 : 0;
           }
+          sh.theta[rank] = th;
+          sh.pairs[tid] = rank;
         }
+        const double x = (i < b && j < b) ? sh.S[i * BMAX + j] : 0.0;
+        __syncthreads();
+        if (i < b && j < b) sh.S[i * BMAX + sh.pairs[j]] = x;
       }
       __syncthreads();
     }
