@@ -85,12 +85,15 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// 1/sqrt(v) to ~1 ulp: single-precision seed and two Newton steps (relative
-// error 2^-22 -> 2^-43 -> rounding) when v is inside float range, else the
-// library rsqrt (a long software sequence)
+// 1/sqrt(v) to ~1 ulp: the hardware's double-precision seed (rsqrt.approx.f64 =
+// MUFU.RSQ64H on the high word, relative error ~2^-22) and two Newton steps
+// (2^-43 -> rounding) for normal v; else the library rsqrt (a long software
+// sequence). The float-seeded form (two F64<->F32 conversions around
+// MUFU.RSQ) measured 131 cycles per dependent call (scripts/micro/dp_latency.cu).
 __device__ __forceinline__ double rsqrt_fast(double v) {
-  if (v > 1e-30 && v < 1e30) {
-    double r = (double)rsqrtf((float)v);
+  if (v > 1e-300 && v < 1e300) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(r) : "d"(v));
     const double hv = 0.5 * v;
     r = r * fma(-hv * r, r, 1.5);
     r = r * fma(-hv * r, r, 1.5);
