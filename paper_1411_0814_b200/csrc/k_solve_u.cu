@@ -21,6 +21,7 @@
 // sum (y - u.v)^2 from the row still in shared memory, never by the
 // cancelling ||y||^2 - u^T b shortcut.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "rsm_internal.h"
@@ -1074,6 +1075,223 @@ __global__ void __launch_bounds__(SU_MAXW * 32) k_solve_u_pre(SolveUArgs a) {
   }
 }
 
+// k_solve_u_pre without row staging, for a V-hat that leaves no room for row
+// buffers (config 4: n = 2048, r = 8 -- 128 KB of basis planes): both rows of
+// the fused column loop come straight from global memory (row k+1 from DRAM,
+// pulled toward L2 by a bulk prefetch two rows ahead; row k, read one
+// iteration earlier, from L2), eight words of each row in flight per lane.
+// Every V-hat read in shared memory serves the residual of row k and the
+// accumulation of row k+1 -- the two-pass kernel read the basis twice per row,
+// and at r = 8 those reads (64 B per cell per pass) are what bounds it. Every
+// lane sees every mask word, so the observed count needs no reduction; the
+// warp reduction carries V_O^T y and the previous row's residual only. Same
+// per-cell arithmetic as k_solve_u_pre. Needs a.Apre (k_normal_i8.cu).
+template <int R>
+__global__ void __launch_bounds__(384) k_solve_u_preg(SolveUArgs a) {
+  constexpr int NP = (R + 1) / 2;
+  constexpr int NA = R * (R + 1) / 2;
+  constexpr int NV = pow2_at_least(R + 1);  // b, previous row's residual
+  constexpr int UB = 8;
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int nwarps = blockDim.x >> 5;
+  double2* Vp = reinterpret_cast<double2*>(sm);
+  for (int64_t e = threadIdx.x; e < NP * n; e += blockDim.x) {
+    const int64_t p = e / n, c = e % n;
+    const double x0 = a.V[c * R + 2 * p];
+    const double x1 = (2 * p + 1 < R) ? a.V[c * R + 2 * p + 1] : 0.0;
+    Vp[e] = make_double2(x0, x1);
+  }
+  __syncthreads();
+  const uint32_t ybytes = (uint32_t)(n * 8), wbytes = (uint32_t)(a.nwp * 4);
+  auto prefetch_l2 = [&](int64_t row) {
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.Y + row * n), "r"(ybytes) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.bitsR + row * a.nwp), "r"(wbytes)
+                   : "memory");
+    }
+  };
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t nw = (int64_t)gridDim.x * nwarps;
+  const int64_t r0 = a.row_lo + gw;
+  if (r0 >= a.row_hi) return;
+  const int64_t nrows = (a.row_hi - r0 + nw - 1) / nw;  // this warp's rows: r0 + k nw
+  const int nfull = (int)(n >> 5);
+  const bool has_tail = (int64_t)nfull * 32 < n;
+  const bool tail = (int64_t)nfull * 32 + lane < n;
+  const unsigned lbit = 1u << lane;
+  auto vload = [&](const double2* vq, double* v) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double2 t = vq[p * n];
+      v[2 * p] = t.x;
+      if (2 * p + 1 < R) v[2 * p + 1] = t.y;
+    }
+  };
+  // predicated on the mask bit: a hidden cell's NaN never enters an executed
+  // instruction (as k_solve_u_pre)
+  auto accum_b = [&](double* acc, const double* v, double yraw, bool k) {
+    if (k) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) acc[i] = fma(yraw, v[i], acc[i]);
+    }
+  };
+  auto resid = [&](double& ss, const double* v, const double* nu, double yraw, bool k) {
+    double d = yraw;
+#pragma unroll
+    for (int q = 0; q < R; ++q) d = fma(nu[q], v[q], d);
+    if (k) ss = fma(d, d, ss);
+  };
+  auto finish = [&](double (&acc)[NV], int cnt, double* u, double& ss_prev, int64_t frow) -> bool {
+    double A[NA], bv[R];
+    const double* ap = a.Apre + frow * NA;
+#pragma unroll
+    for (int p = 0; p < NA; ++p) A[p] = __ldg(ap + p);  // in flight during the reduction
+    acc[R] = ss_prev;
+    warp_reduce_halving<NV>(acc, lane);
+#pragma unroll
+    for (int i = 0; i < R; ++i) bv[i] = warp_total<NV>(acc, i);
+    ss_prev = warp_total<NV>(acc, R);
+    const bool fl = row_solve<R>(A, bv, cnt, u);
+    if (a.Ugiven) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) u[q] = a.Ugiven[frow * R + q];
+      return false;
+    }
+    return fl;
+  };
+  // one row alone: ACC = accumulation pass (row 0), else residual pass (last row)
+  auto single = [&](auto ACC, const double* y, const uint32_t* wd, double* acc, const double* nu, double& ss,
+                    int& cnt) {
+    constexpr bool kAcc = decltype(ACC)::value;
+    const double* yp = y + lane;
+    const double2* vq = Vp + lane;
+    int w = 0;
+    for (; w + UB <= nfull; w += UB) {
+      const uint4 m0 = __ldg(reinterpret_cast<const uint4*>(wd + w));
+      const uint4 m1 = __ldg(reinterpret_cast<const uint4*>(wd + w + 4));
+      const unsigned bw[UB] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+      double yv[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) yv[u] = __ldg(yp + 32 * u);
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        double v[R];
+        vload(vq + 32 * u, v);
+        if (kAcc) {
+          cnt += __popc(bw[u]);
+          accum_b(acc, v, yv[u], (bw[u] & lbit) != 0u);
+        } else {
+          resid(ss, v, nu, yv[u], (bw[u] & lbit) != 0u);
+        }
+      }
+      yp += 32 * UB;
+      vq += 32 * UB;
+    }
+    for (; w < nfull + (has_tail ? 1 : 0); ++w) {
+      const unsigned word = __ldg(wd + w);
+      if (kAcc) cnt += __popc(word);
+      if (w < nfull || tail) {
+        double v[R];
+        vload(vq, v);
+        const bool k = (word & lbit) != 0u;
+        const double yraw = k ? __ldg(yp) : 0.0;
+        if (kAcc) accum_b(acc, v, yraw, k);
+        else resid(ss, v, nu, yraw, k);
+      }
+      yp += 32;
+      vq += 32;
+    }
+  };
+  double u[R];
+  bool flagged;
+  {
+    double acc[NV];
+#pragma unroll
+    for (int p = 0; p < NV; ++p) acc[p] = 0.0;
+    double none = 0.0;
+    int cnt = 0;
+    if (nrows > 1) prefetch_l2(r0 + nw);
+    single(std::true_type{}, a.Y + r0 * n, a.bitsR + r0 * a.nwp, acc, nullptr, none, cnt);
+    flagged = finish(acc, cnt, u, none, r0);
+  }
+  for (int64_t k = 0; k < nrows; ++k) {
+    const int64_t row = r0 + k * nw;
+    const bool has_next = k + 1 < nrows;
+    if (k + 2 < nrows) prefetch_l2(r0 + (k + 2) * nw);
+    const double* yk = a.Y + row * n;
+    const uint32_t* wd = a.bitsR + row * a.nwp;
+    double nu[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) nu[q] = -u[q];
+    double ss = 0.0;
+    double acc[NV];
+#pragma unroll
+    for (int p = 0; p < NV; ++p) acc[p] = 0.0;
+    int cnt = 0;
+    if (has_next) {
+      const double* yn = yk + nw * n;
+      const uint32_t* wn = wd + nw * a.nwp;
+      const double* ypk = yk + lane;
+      const double* ypn = yn + lane;
+      const double2* vq = Vp + lane;
+      int w = 0;
+      for (; w + UB <= nfull; w += UB) {
+        const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(wd + w));
+        const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(wd + w + 4));
+        const uint4 n0 = __ldg(reinterpret_cast<const uint4*>(wn + w));
+        const uint4 n1 = __ldg(reinterpret_cast<const uint4*>(wn + w + 4));
+        const unsigned dw[UB] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        const unsigned nwd[UB] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+        double yvn[UB], yvk[UB];
+#pragma unroll
+        for (int q = 0; q < UB; ++q) yvn[q] = __ldg(ypn + 32 * q);  // DRAM / L2 (prefetched)
+#pragma unroll
+        for (int q = 0; q < UB; ++q) yvk[q] = __ldg(ypk + 32 * q);  // L2
+#pragma unroll
+        for (int q = 0; q < UB; ++q) {
+          double v[R];
+          vload(vq + 32 * q, v);
+          cnt += __popc(nwd[q]);
+          resid(ss, v, nu, yvk[q], (dw[q] & lbit) != 0u);
+          accum_b(acc, v, yvn[q], (nwd[q] & lbit) != 0u);
+        }
+        ypk += 32 * UB;
+        ypn += 32 * UB;
+        vq += 32 * UB;
+      }
+      for (; w < nfull + (has_tail ? 1 : 0); ++w) {
+        const unsigned wdk = __ldg(wd + w), wdn = __ldg(wn + w);
+        cnt += __popc(wdn);
+        if (w < nfull || tail) {
+          double v[R];
+          vload(vq, v);
+          const bool kk = (wdk & lbit) != 0u, kn = (wdn & lbit) != 0u;
+          resid(ss, v, nu, kk ? __ldg(ypk) : 0.0, kk);
+          accum_b(acc, v, kn ? __ldg(ypn) : 0.0, kn);
+        }
+        ypk += 32;
+        ypn += 32;
+        vq += 32;
+      }
+    } else {
+      single(std::false_type{}, yk, wd, acc, nu, ss, cnt);
+    }
+    if (lane < R) {
+      double uk = 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == lane) uk = u[q];
+      a.U[row * R + lane] = uk;
+    }
+    if (lane == 0 && flagged) atomicAdd(a.flagged, 1);
+    if (has_next) flagged = finish(acc, cnt, u, ss, row + nw);  // ss: row k's residual, summed
+    else ss = warp_sum(ss);
+    if (lane == 0) a.rowres[row] = ss;
+  }
+}
+
 // deterministic single-CTA sum of n doubles (fixed strided order + tree)
 __global__ void k_sum_rows(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
   __shared__ double part[1024];
@@ -1200,6 +1418,20 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
     else launch_solve_u_k<R, true, 2>(a, head + vbytes, per_warp, sms, s);
   } else if (head + vbytes <= cap) {
     // V-hat alone fills shared memory: rows are read from global
+    static const bool preg_on = [] {
+      const char* e = getenv("RSM_SU_PREG");
+      return !(e && atoi(e) == 0);
+    }();
+    if (a.Apre && bulk && preg_on) {
+      // tensor-core normal matrices: fused residual/accumulation loop (k_solve_u_preg)
+      const int w = 12;
+      const int64_t rows = a.row_hi - a.row_lo;
+      int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
+      if (blocks < 1) blocks = 1;
+      ensure_smem((const void*)k_solve_u_preg<R>, vbytes);
+      k_solve_u_preg<R><<<(unsigned)blocks, w * 32, vbytes, s>>>(a);
+      return;
+    }
     launch_solve_u_k<R, true, 0>(a, head + vbytes, 0, sms, s);
   } else {
     if (bulk) launch_solve_u_k<R, false, 1>(a, head, per_warp, sms, s);
