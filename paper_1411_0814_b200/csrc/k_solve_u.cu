@@ -1121,6 +1121,16 @@ __global__ void __launch_bounds__(384) k_solve_u_preg(SolveUArgs a) {
   const bool has_tail = (int64_t)nfull * 32 < n;
   const bool tail = (int64_t)nfull * 32 + lane < n;
   const unsigned lbit = 1u << lane;
+  // L2 residency: a row's first read (as row k+1) asks L2 to keep its lines,
+  // the second (as row k, one iteration later) releases them
+  uint64_t pol_keep, pol_drop;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
+  auto ld_hint = [](const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+  };
   auto vload = [&](const double2* vq, double* v) {
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -1212,14 +1222,14 @@ __global__ void __launch_bounds__(384) k_solve_u_preg(SolveUArgs a) {
     for (int p = 0; p < NV; ++p) acc[p] = 0.0;
     double none = 0.0;
     int cnt = 0;
-    if (nrows > 1) prefetch_l2(r0 + nw);
+    if ((a.pf & 3) && nrows > 1) prefetch_l2(r0 + nw);
     single(std::true_type{}, a.Y + r0 * n, a.bitsR + r0 * a.nwp, acc, nullptr, none, cnt);
     flagged = finish(acc, cnt, u, none, r0);
   }
   for (int64_t k = 0; k < nrows; ++k) {
     const int64_t row = r0 + k * nw;
     const bool has_next = k + 1 < nrows;
-    if (k + 2 < nrows) prefetch_l2(r0 + (k + 2) * nw);
+    if ((a.pf & 3) && k + 2 < nrows) prefetch_l2(r0 + (k + 2) * nw);
     const double* yk = a.Y + row * n;
     const uint32_t* wd = a.bitsR + row * a.nwp;
     double nu[R];
@@ -1246,9 +1256,9 @@ __global__ void __launch_bounds__(384) k_solve_u_preg(SolveUArgs a) {
         const unsigned nwd[UB] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
         double yvn[UB], yvk[UB];
 #pragma unroll
-        for (int q = 0; q < UB; ++q) yvn[q] = __ldg(ypn + 32 * q);  // DRAM / L2 (prefetched)
+        for (int q = 0; q < UB; ++q) yvn[q] = a.pf & 4 ? ld_hint(ypn + 32 * q, pol_keep) : __ldg(ypn + 32 * q);  // DRAM
 #pragma unroll
-        for (int q = 0; q < UB; ++q) yvk[q] = __ldg(ypk + 32 * q);  // L2
+        for (int q = 0; q < UB; ++q) yvk[q] = a.pf & 4 ? ld_hint(ypk + 32 * q, pol_drop) : __ldg(ypk + 32 * q);  // L2
 #pragma unroll
         for (int q = 0; q < UB; ++q) {
           double v[R];
@@ -1424,12 +1434,24 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
     }();
     if (a.Apre && bulk && preg_on) {
       // tensor-core normal matrices: fused residual/accumulation loop (k_solve_u_preg)
-      const int w = 12;
+      static const int w = [] {
+        const char* e = getenv("RSM_SU_PREG_W");
+        return e ? std::max(1, std::min(12, atoi(e))) : 12;
+      }();
+      static const int pf = [] {
+        // bit 2: L2 eviction hints on the two reads of a row (config 4: 8.3 -> 8.1 ms);
+        // bits 0-1: bulk L2 prefetch two rows ahead (measured slower: 8.5 ms, the
+        // prefetched rows push the rows awaiting their second read out of L2)
+        const char* e = getenv("RSM_SU_PF");
+        return e ? atoi(e) : 4;
+      }();
+      SolveUArgs b = a;
+      b.pf = pf;
       const int64_t rows = a.row_hi - a.row_lo;
       int64_t blocks = std::min<int64_t>((rows + w - 1) / w, (int64_t)sms);
       if (blocks < 1) blocks = 1;
       ensure_smem((const void*)k_solve_u_preg<R>, vbytes);
-      k_solve_u_preg<R><<<(unsigned)blocks, w * 32, vbytes, s>>>(a);
+      k_solve_u_preg<R><<<(unsigned)blocks, w * 32, vbytes, s>>>(b);
       return;
     }
     launch_solve_u_k<R, true, 0>(a, head + vbytes, 0, sms, s);

@@ -130,6 +130,7 @@ struct SolveUArgs {
   const double* Ugiven;  // non-null: rows' solutions given (m x r), only the residual pass
                          // counts (masked_residual_norm through the stage-5 arithmetic)
   const double* Apre;    // non-null: rows' packed normal matrices (m x r(r+1)/2, k_normal_i8.cu)
+  int pf;                // k_solve_u_preg: rows ahead pulled toward L2 by a bulk prefetch (0: none)
 };
 
 // rsm_ctx.cu: message for rsm_last_error(NULL) from host-only entry points
