@@ -109,3 +109,35 @@ def test_solve_u_wide_rows(m, n, r):
     R = np.where(M.mask != 0, np.nan_to_num(M.values) - U_o @ V.T, 0.0)
     ss_o = float(np.sum(R * R))
     assert abs(ss - ss_o) <= 1e-10 * ss_o
+
+
+@pytest.mark.parametrize("n", [2048, 2050])
+def test_fused_global_row_solver_matches_two_pass(n):
+    # config 4's stage-5 layout (V-hat fills shared memory, tensor-core normal
+    # matrices): the fused residual/accumulation kernel (k_solve_u_preg) against
+    # the two-pass kernel (RSM_SU_PREG=0) and the FP64 normal matrices
+    # (RSM_NORMAL_TC=0) on the same decomposition, with and without a column
+    # tail (n % 32 != 0); odd row counts per warp
+    code = (
+        "import sys, numpy as np\n"
+        "from paper_1411_0814_b200 import rsm\n"
+        f"ctx = rsm.Context(0); ctx.generate(8531, {n}, 8, 0.9, 1e-3, 3)\n"
+        "cfg = rsm.RsmConfig(rank=8, mode=rsm.Mode.M2, block=9, plan=rsm.TrialPlan(6000), seed=3)\n"
+        "F, rep = ctx.decompose(cfg)\n"
+        "np.save(sys.argv[1], np.concatenate([(F.u @ F.v.T[:, :64]).ravel(), [rep.e, rep.underdetermined_rows]]))\n")
+    outs = []
+    for extra in ({}, {"RSM_SU_PREG": "0"}, {"RSM_NORMAL_TC": "0"}):
+        env = dict(os.environ)
+        env["PYTHONPATH"] = ROOT + os.pathsep + env.get("PYTHONPATH", "")
+        env.update(extra)
+        path = os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ".",
+                            f"_preg_{n}_{len(outs)}.npy")
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=300)
+        outs.append(np.load(path))
+        os.remove(path)
+    a, b, c = outs
+    assert a[-1] == b[-1] == c[-1] == 0
+    assert abs(a[-2] - 1e-3) < 1e-4
+    for o in (b, c):
+        assert np.linalg.norm(a[:-2] - o[:-2]) <= 1e-11 * np.linalg.norm(a[:-2])
+        assert abs(a[-2] - o[-2]) <= 1e-10 * a[-2]
