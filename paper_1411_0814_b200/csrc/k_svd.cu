@@ -491,6 +491,34 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
     // outside the column support; rp = rex rounded up to even
     const int rex = a.rex, rp = (a.rex + 1) & ~1;
     if (a.Wq) {
+      if (M2 && fast) {
+        // V = S^T C once per SUPPORT column (L of them, not npad), in place
+        // over the first rex = K - 1 rows of the staged submatrix; the
+        // expansion below then only looks values up. Four columns per thread
+        // per pass, so each coefficient read serves four columns.
+        for (int64_t c0 = 4 * (int64_t)tid; c0 < L; c0 += 4 * (int64_t)nth) {
+          double xs[4][9];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < 9; ++k) xs[u][k] = (k < K && c0 + u < L) ? vec[k * Lp + c0 + u] : 0.0;
+          for (int i = 0; i < rex; ++i) {
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+              const double w = k < K ? W[k * rex + i] : 0.0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) v[u] = fma(xs[u][k], w, v[u]);
+            }
+            // row i < K - 1 of these columns is not read again by this thread
+            // (xs holds them) nor by any other (columns are disjoint)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c0 + u < L) vec[i * Lp + c0 + u] = v[u];
+          }
+        }
+        __syncthreads();
+      }
       // int8 digit slices for the tensor-core stage 3 (k_gram_i8.cu): rows
       // tl * rex + i, zero outside the support, four columns per thread
       for (int64_t j0 = 4 * (int64_t)tid; j0 < a.npad; j0 += 4 * (int64_t)nth) {
@@ -509,22 +537,14 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
           cc[u] = c;
         }
         if (M2 && fast) {
-          // V = S^T C: the 4 columns' K values read once, then every output
-          // vector from registers (K <= 9 here)
-          double xs[4][9];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int k = 0; k < 9; ++k) xs[u][k] = (k < K && cc[u] >= 0) ? vec[k * Lp + cc[u]] : 0.0;
+          int8_t* wp = a.Wq + (tl * rex) * a.npad + j0;
+          const int64_t sstride = a.Kpad * a.npad;
           for (int i = 0; i < rex; ++i) {
-            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            double v[4];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) {
-              const double w = k < K ? W[k * rex + i] : 0.0;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) v[u] = fma(xs[u][k], w, v[u]);
-            }
-            emit_slices4(a.S, a.Wq, a.Kpad, a.npad, tl * rex + i, j0, v[0], v[1], v[2], v[3]);
+            for (int u = 0; u < 4; ++u) v[u] = cc[u] >= 0 ? vec[i * Lp + cc[u]] : 0.0;
+            emit_slices4_at(a.S, wp, sstride, v[0], v[1], v[2], v[3]);
+            wp += a.npad;
           }
           continue;
         }
