@@ -1498,14 +1498,61 @@ __global__ void k_sum_final(const double* __restrict__ part, int np, double* __r
   *out = s;
 }
 
-// out[0] = sum of v[0..n); out must have room for 2 + SUMP doubles (partials)
-void launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s) {
+// both levels in one launch: the block that arrives last (arrival counter, 0
+// on entry) adds the SUMP partials in index order -- the same fixed order as
+// k_sum_final, whichever block that is
+__global__ void k_sum_part_final(const double* __restrict__ v, int64_t n, double* __restrict__ part,
+                                 double* __restrict__ out, unsigned* __restrict__ counter) {
+  __shared__ double red[256];
+  __shared__ bool last;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+  double s = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += v[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = red[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    // lane l loads partials l and l + 32 (SUMP = 64); lane 0 adds them in index order
+    const volatile double* pv = part;
+    const double a0 = pv[threadIdx.x], a1 = pv[threadIdx.x + 32];
+    double t = 0.0;
+    for (int i = 0; i < 32; ++i) t += __shfl_sync(0xffffffffu, a0, i);
+    for (int i = 0; i < 32; ++i) t += __shfl_sync(0xffffffffu, a1, i);
+    if (threadIdx.x == 0) {
+      *out = t;
+      *counter = 0u;
+    }
+  }
+}
+
+// out[0] = sum of v[0..n); out must have room for 2 + SUMP doubles (partials).
+// counter (optional): a device word that is 0 on entry -- the two-level sum
+// then runs as one launch (the last block to arrive finishes it)
+int launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s, unsigned* counter) {
   if (n <= 32768) {
     k_sum_rows<<<1, 1024, 0, s>>>(v, n, out);
-    return;
+    return 1;
+  }
+  if (counter) {
+    static_assert(SUMP == 64, "k_sum_part_final's final pass");
+    k_sum_part_final<<<SUMP, 256, 0, s>>>(v, n, out + 2, out, counter);
+    return 1;
   }
   k_sum_part<<<SUMP, 256, 0, s>>>(v, n, out + 2);
   k_sum_final<<<1, 1, 0, s>>>(out + 2, SUMP, out);
+  return 2;
 }
 
 }  // namespace rsmk

@@ -1026,8 +1026,9 @@ SolveUOut solve_rows(rsm_ctx* c, const View& v, const double* basis, DevBuf& out
   }
   if (hi > lo) {
     rsmk::launch_solve_u(a, c->stream);
-    rsmk::launch_sum_rows(c->rowres.as<double>() + lo, hi - lo, c->dsum.as<double>(), c->stream);
-    c->launches += 2;
+    // flagged[1] (zeroed above) is the sum kernel's arrival counter
+    c->launches += 1 + rsmk::launch_sum_rows(c->rowres.as<double>() + lo, hi - lo, c->dsum.as<double>(), c->stream,
+                                             reinterpret_cast<unsigned*>(c->flagged.as<int>() + 1));
   } else {
     ck(cudaMemsetAsync(c->dsum.p, 0, sizeof(double), c->stream), "memset");
   }

@@ -202,7 +202,8 @@ size_t normal_i8_bq_bytes(int r, int64_t n);
 cudaError_t launch_normal_i8(const NormalI8Args& a, int sms, cudaStream_t s);
 // k_solve_u.cu
 void launch_solve_u(const SolveUArgs& a, cudaStream_t s);
-void launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s);
+// returns the launches made
+int launch_sum_rows(const double* v, int64_t n, double* out, cudaStream_t s, unsigned* counter = nullptr);
 void launch_residual(const double* Y, const uint32_t* bitsR, int64_t m, int64_t n, int64_t nwp,
                      const double* U, const double* V, int r, double* rowres, cudaStream_t s);
 
