@@ -582,18 +582,23 @@ __device__ __forceinline__ void emit_slices4_at_t(int8_t* p, int64_t sstride, do
   }
 }
 
+// digit counts other than the default (RSM_I8_SLICES experiments): out of line,
+// so the callers' loops hold one copy of the emission code, not three
+static __device__ __noinline__ void emit_slices4_at_other(int S, int8_t* p, int64_t sstride, double v0, double v1,
+                                                   double v2, double v3) {
+  if (S == 5) emit_slices4_at_t<5>(p, sstride, v0, v1, v2, v3);
+  else emit_slices4_at_t<7>(p, sstride, v0, v1, v2, v3);
+}
+
 __device__ __forceinline__ void emit_slices4_at(int S, int8_t* p, int64_t sstride, double v0, double v1, double v2,
                                                 double v3) {
-  if (S == 5) emit_slices4_at_t<5>(p, sstride, v0, v1, v2, v3);
-  else if (S == 7) emit_slices4_at_t<7>(p, sstride, v0, v1, v2, v3);
-  else emit_slices4_at_t<6>(p, sstride, v0, v1, v2, v3);
+  if (S == kGramSlices) emit_slices4_at_t<kGramSlices>(p, sstride, v0, v1, v2, v3);
+  else emit_slices4_at_other(S, p, sstride, v0, v1, v2, v3);
 }
 
 __device__ __forceinline__ void emit_slices4(int S, int8_t* W, int64_t Kpad, int64_t npad, int64_t krow,
                                              int64_t j0, double v0, double v1, double v2, double v3) {
-  if (S == 5) emit_slices4_t<5>(W, Kpad, npad, krow, j0, v0, v1, v2, v3);
-  else if (S == 7) emit_slices4_t<7>(W, Kpad, npad, krow, j0, v0, v1, v2, v3);
-  else emit_slices4_t<6>(W, Kpad, npad, krow, j0, v0, v1, v2, v3);
+  emit_slices4_at(S, W + krow * npad + j0, Kpad * npad, v0, v1, v2, v3);
 }
 
 }  // namespace rsmd
