@@ -989,26 +989,30 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
           int8_t* wq = a.Wq + tl * rex * a.npad + 4 * lane;
           const int sh0 = (4 * lane) & 31;  // bit of the lane's first column within its word
           for (int64_t j0 = 4 * lane; j0 < a.npad; j0 += 128, wq += 128) {
-            double v[4][R1];
             const uint32_t word = cm[j0 >> 5];
             int c0 = (int)pre[j0 >> 5] + __popc(word & ((1u << sh0) - 1u));
             const uint32_t nib = (word >> sh0) & 15u;
+            int cu[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const bool in = (nib >> u) & 1u;
-              const int c = c0 < lmax ? c0 : lmax;
-#pragma unroll
-              for (int p = 0; p < R1; ++p) {
-                const double t = S[p * Lp + c];
-                v[u][p] = in ? t : 0.0;
-              }
-              c0 += in ? 1 : 0;
+              cu[u] = c0 < lmax ? c0 : lmax;
+              c0 += (nib >> u) & 1u;
             }
+            // the vector loop stays rolled: one copy of the digit emission in
+            // the instruction stream (the kernel is fetch-sensitive)
             int8_t* wp = wq;
-#pragma unroll
+            const double* sp = S;
+#pragma unroll 1
             for (int p = 0; p < R1; ++p) {
-              emit_slices4_at(a.S, wp, sstride, v[0][p], v[1][p], v[2][p], v[3][p]);
+              double v[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const double t = sp[cu[u]];
+                v[u] = ((nib >> u) & 1u) ? t : 0.0;
+              }
+              emit_slices4_at(a.S, wp, sstride, v[0], v[1], v[2], v[3]);
               wp += a.npad;
+              sp += Lp;
             }
           }
           __syncwarp();
