@@ -881,22 +881,40 @@ __global__ void __launch_bounds__(SVDW_WARPS * 32) k_svd_warp(SvdArgs a) {
     }
     bool fast = false;
     for (int it = 0;; ++it) {
-#pragma unroll
-      for (int p = 0; p < P; ++p) g[p] = warp_sum(g[p]);
+      bool reduced = false;
       if constexpr (K <= FASTK) {
         if (it == 0 && rex == K - 1 && a.fast_basis) {
           // r = k - 1: an orthonormal basis of the top-r subspace straight
-          // from the Gram (see topr_basis_small), no Jacobi rotations
-          if (lane == 0) {
+          // from the Gram (see topr_basis_small), no Jacobi rotations. Only one
+          // lane needs the Gram: a halving reduction (~NH shuffles instead of
+          // 5 P) leaves each total in one lane, which stores it.
+          constexpr int NH = P <= 16 ? 16 : (P <= 32 ? 32 : 64);
+          constexpr int PL = NH > 32 ? NH / 32 : 1, LPV = NH < 32 ? 32 / NH : 1;
+          double h[NH];
 #pragma unroll
-            for (int p = 0; p < P; ++p) Gs[p] = g[p];
-            Gs[K * K - 1] = topr_basis_small<K>(Gs, Ws) ? 1.0 : 0.0;
+          for (int p = 0; p < NH; ++p) h[p] = p < P ? g[p] : 0.0;
+          warp_reduce_halving<NH>(h, lane);
+          if (lane % LPV == 0) {
+#pragma unroll
+            for (int q = 0; q < PL; ++q) {
+              const int j = (lane / LPV) * PL + q;
+              if (j < P) Gs[j] = h[q];
+            }
           }
+          __syncwarp();
+          if (lane == 0) Gs[K * K - 1] = topr_basis_small<K>(Gs, Ws) ? 1.0 : 0.0;
           __syncwarp();
           fast = Gs[K * K - 1] != 0.0;
           __syncwarp();
           if (fast) break;
+#pragma unroll
+          for (int p = 0; p < P; ++p) g[p] = Gs[p];  // the Jacobi path wants the totals in every lane
+          reduced = true;
         }
+      }
+      if (!reduced) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) g[p] = warp_sum(g[p]);
       }
       bool big = false;
       {
