@@ -610,25 +610,32 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       d = d < 2 ? 2 : (d > a.dmax ? a.dmax : d);
       double sigma = e / (0.0 - c);
       const double tau = 2.0 / sigma;
-      grid.sync();  // X complete
-      matvec<NC>(a, X, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
-      ++matvecs;
-      for (int q = tid; q < nr * ld; q += ET) {
-        const int j = q % ld;
-        const double y = (j == pcol) ? Zo[q] / ub : (Zo[q] - c * Xo[q]) * (sigma / e);
-        Yo[q] = y;
-        Y[(int64_t)row_lo * ld + q] = y;
-      }
-      for (int it = 2; it <= d; ++it) {
+      // one loop for all d filter steps (a single inlined copy of the matvec:
+      // the kernel is large enough for instruction fetch to show): step 1
+      // forms Y = (G X - c X) sigma / e from X, step it > 1 the three-term
+      // recurrence from Y and X; the block rotates (X, Y, Z) <- (Y, Z, X)
+      // after every step but the first
+#pragma unroll 1
+      for (int it = 1; it <= d; ++it) {
         const long long t0 = clock64();
-        grid.sync();  // Y complete
+        grid.sync();  // the iterate (X at step 1, Y after) is complete
         const long long t1 = clock64();
-        matvec<NC>(a, Y, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
-        if (tme) {
+        const bool first = it == 1;
+        matvec<NC>(a, first ? X : Y, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
+        if (tme && !first) {
           sync_cyc += t1 - t0;
           mv_cyc += clock64() - t1;
         }
         ++matvecs;
+        if (first) {
+          for (int q = tid; q < nr * ld; q += ET) {
+            const int j = q % ld;
+            const double y = (j == pcol) ? Zo[q] / ub : (Zo[q] - c * Xo[q]) * (sigma / e);
+            Yo[q] = y;
+            Y[(int64_t)row_lo * ld + q] = y;
+          }
+          continue;
+        }
         const double sigma2 = 1.0 / (tau - sigma);
         for (int q = tid; q < nr * ld; q += ET) {
           const int j = q % ld;
@@ -645,8 +652,9 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
       { double* t = X; X = Y; Y = t; t = Xo; Xo = Yo; Yo = t; }
       __syncthreads();
       EIG_T(0);
-      cholqr(a, grid, X, Xo, b, ld, pcol, row_lo, nr, buf, pw, sh);
-      cholqr(a, grid, X, Xo, b, ld, -1, row_lo, nr, buf, pw, sh);
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass)  // CholQR2 (one inlined copy)
+        cholqr(a, grid, X, Xo, b, ld, pass == 0 ? pcol : -1, row_lo, nr, buf, pw, sh);
       EIG_T(1);
     }
     // ---- Rayleigh-Ritz ----
