@@ -601,32 +601,49 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
   } while (0)
   EIG_T(5);
   for (; outer < a.max_outer; ++outer) {
-    if (!full) {
-      // ---- Chebyshev filter of degree d on [acut, ub], normalised at 0 ----
-      const double e = 0.5 * (ub - acut), c = 0.5 * (ub + acut);
-      const double x0 = fabs(c / e);
-      const double growth = x0 + sqrt(x0 * x0 - 1.0);
-      int d = (int)floor(log(a.amp) / log(growth));
-      d = d < 2 ? 2 : (d > a.dmax ? a.dmax : d);
-      double sigma = e / (0.0 - c);
-      const double tau = 2.0 / sigma;
-      // one loop for all d filter steps (a single inlined copy of the matvec:
-      // the kernel is large enough for instruction fetch to show): step 1
-      // forms Y = (G X - c X) sigma / e from X, step it > 1 the three-term
-      // recurrence from Y and X; the block rotates (X, Y, Z) <- (Y, Z, X)
-      // after every step but the first
+    {
+      // ---- Chebyshev filter of degree d on [acut, ub], normalised at 0, then
+      // CholQR2 and the Rayleigh-Ritz product, as ONE loop over matvec steps
+      // (a single inlined copy of the matvec: the kernel is large enough for
+      // instruction fetch to show): step 1 forms Y = (G X - c X) sigma / e
+      // from X, steps 2..d the three-term recurrence from Y and X (the block
+      // rotates (X, Y, Z) <- (Y, Z, X) after each), step d + 1 is Z = G X of
+      // the re-orthonormalised block. full: no filter, d = 0 ----
+      double e = 1.0, c = 0.0, sigma = 0.0, tau = 0.0;
+      int d = 0;
+      if (!full) {
+        e = 0.5 * (ub - acut);
+        c = 0.5 * (ub + acut);
+        const double x0 = fabs(c / e);
+        const double growth = x0 + sqrt(x0 * x0 - 1.0);
+        d = (int)floor(log(a.amp) / log(growth));
+        d = d < 2 ? 2 : (d > a.dmax ? a.dmax : d);
+        sigma = e / (0.0 - c);
+        tau = 2.0 / sigma;
+      }
 #pragma unroll 1
-      for (int it = 1; it <= d; ++it) {
+      for (int it = 1; it <= d + 1; ++it) {
+        const bool first = it == 1, rr = it == d + 1;
+        if (rr && !full) {
+          // filtered block is in Y
+          { double* t = X; X = Y; Y = t; t = Xo; Xo = Yo; Yo = t; }
+          __syncthreads();
+          EIG_T(0);
+#pragma unroll 1
+          for (int pass = 0; pass < 2; ++pass)  // CholQR2 (one inlined copy)
+            cholqr(a, grid, X, Xo, b, ld, pass == 0 ? pcol : -1, row_lo, nr, buf, pw, sh);
+          EIG_T(1);
+        }
         const long long t0 = clock64();
-        grid.sync();  // the iterate (X at step 1, Y after) is complete
+        grid.sync();  // the iterate (X at steps 1 and d + 1, Y between) is complete
         const long long t1 = clock64();
-        const bool first = it == 1;
-        matvec<NC>(a, first ? X : Y, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
-        if (tme && !first) {
+        matvec<NC>(a, (first || rr) ? X : Y, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
+        if (tme && !first && !rr) {
           sync_cyc += t1 - t0;
           mv_cyc += clock64() - t1;
         }
         ++matvecs;
+        if (rr) break;
         if (first) {
           for (int q = tid; q < nr * ld; q += ET) {
             const int j = q % ld;
@@ -648,19 +665,8 @@ __global__ void __launch_bounds__(ET, 1) k_eig(EigArgs a) {
         t = Xo; Xo = Yo; Yo = Zo; Zo = t;
         sigma = sigma2;
       }
-      // filtered block is in Y
-      { double* t = X; X = Y; Y = t; t = Xo; Xo = Yo; Yo = t; }
-      __syncthreads();
-      EIG_T(0);
-#pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass)  // CholQR2 (one inlined copy)
-        cholqr(a, grid, X, Xo, b, ld, pass == 0 ? pcol : -1, row_lo, nr, buf, pw, sh);
-      EIG_T(1);
     }
     // ---- Rayleigh-Ritz ----
-    grid.sync();  // X complete
-    matvec<NC>(a, X, Z, Zo, ld, ld, row_lo, row_hi, gs, xs, sh, xphase);
-    ++matvecs;
     {
       const int P = b * (b + 1) / 2;
       for (int p = tid; p < P + 2; p += ET) {
