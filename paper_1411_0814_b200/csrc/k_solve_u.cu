@@ -1302,6 +1302,243 @@ __global__ void __launch_bounds__(384) k_solve_u_preg(SolveUArgs a) {
   }
 }
 
+// Stage 5 on the FP64 tensor cores (mma.m8n8k4.f64), for precomputed normal
+// matrices (a.Apre), r <= 8, n a multiple of 32. A warp owns 8 rows at a time;
+// lane l sits in row g = l / 4 of the block with k = l % 4.
+//   pass 1, b = V_O^T y: D(8 rows x 8) += A(8 x 4) B(4 x 8) per step with A
+//     the masked values and B four basis rows (columns j >= r are zero). The
+//     contraction order is free, so lane k of a row takes the four CONTIGUOUS
+//     columns 4k..4k+3 of every 16-column group (two 16-byte loads: a row's
+//     128 bytes per warp instruction pair) and step q uses column 4k + q of
+//     each lane;
+//   the 8 rows are solved at once (each 4-lane group holds its row's b, count
+//     and normal matrix; no reduction anywhere: the MMA did it);
+//   pass 2, the residual: an 8 x 8 tile of U V^T per MMA (A = the rows' u, B =
+//     eight basis rows), each lane then holds two adjacent predictions of its
+//     row and reads the matching 16 bytes of Y (through L2: the block was read
+//     by pass 1 moments ago; evict_last there, evict_first here).
+// ~360 warp instructions per row instead of ~1370, and V-hat's shared-memory
+// reads drop to 8 B per row-column. V-hat sits in shared memory with an odd
+// row stride (5 or 9 doubles) so both fragment patterns are conflict-free.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// TEAM warps share an 8-row block, each taking 1/TEAM of its columns: the
+// bytes a warp holds between its two passes (and so the L2 footprint of all
+// warps' blocks, which must stay below L2's capacity for the second read to
+// hit) shrink by TEAM while the warps in flight stay. The team's partial b,
+// counts and residuals meet in shared memory across a named barrier and are
+// added in team order; every team warp solves the block's rows (same inputs,
+// same result).
+template <int R, int UW, int TEAM>
+__global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma(SolveUArgs a) {
+  constexpr int RS = R <= 4 ? 5 : 9;
+  constexpr int NA = R * (R + 1) / 2;
+  constexpr int NK = (R + 3) / 4;
+  // UW: mask words (32 columns each) per unrolled step, 2 UW KB of a block in flight per warp
+  extern __shared__ __align__(16) double Vs[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, k = lane & 3;
+  const int64_t n = a.n;
+  const int nwarps = blockDim.x >> 5;
+  for (int64_t e = threadIdx.x; e < n * R; e += blockDim.x) {
+    const int64_t c = e / R;
+    const int j = (int)(e % R);
+    Vs[c * RS + j] = a.V[e];
+  }
+  __syncthreads();
+  uint64_t pol_keep, pol_drop;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
+  auto ld2 = [](const double* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;\n" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+  };
+  const int nwn = (int)(n >> 5) / TEAM;  // this warp's mask words per row (n % (32 TEAM) == 0)
+  const int team = warp / TEAM, tw = warp % TEAM, nteams = nwarps / TEAM;
+  const int64_t wbase = (int64_t)tw * nwn;  // first word of this warp's column range
+  // exchange areas behind V-hat: per team and team warp, 8 rows x 8 partial b, 8 counts, 8 residuals
+  double* xb = Vs + (((int64_t)n * RS + 1) & ~int64_t(1)) + (int64_t)(team * TEAM) * 80;
+  const int64_t rows = a.row_hi - a.row_lo;
+  const int64_t nblk = (rows + 7) / 8;
+  const int64_t stride = (int64_t)gridDim.x * nteams;
+  for (int64_t bi = (int64_t)blockIdx.x * nteams + team; bi < nblk; bi += stride) {
+    const int64_t row = a.row_lo + bi * 8 + g;
+    const bool valid = row < a.row_hi;
+    const int64_t rowc = valid ? row : a.row_hi - 1;  // a partial block re-reads its last row
+    const double* yr = a.Y + rowc * n + 32 * wbase;
+    const uint32_t* wr = a.bitsR + rowc * a.nwp + wbase;
+    // ---- pass 1: b = V_O^T y, observed count ----
+    // four independent accumulator pairs (step q of every group feeds pair q):
+    // the MMAs of a group do not wait on one another
+    double dq[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    int cnt = 0;
+    {
+      const double* yp = yr + 4 * k;
+      const double* vp = Vs + (int64_t)(32 * wbase + 4 * k) * RS + g;
+      int w = 0;
+      for (; w + UW <= nwn; w += UW) {
+        unsigned word[UW];
+        double2 y[UW][2][2];
+#pragma unroll
+        for (int u = 0; u < UW; ++u) word[u] = __ldg(wr + w + u);
+#pragma unroll
+        for (int u = 0; u < UW; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            y[u][h][0] = ld2(yp + 32 * u + 16 * h, pol_keep);
+            y[u][h][1] = ld2(yp + 32 * u + 16 * h + 2, pol_keep);
+          }
+#pragma unroll
+        for (int u = 0; u < UW; ++u) {
+          cnt += __popc(word[u]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const unsigned bits = (word[u] >> (16 * h + 4 * k)) & 15u;
+            const double yq[4] = {y[u][h][0].x, y[u][h][0].y, y[u][h][1].x, y[u][h][1].y};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double aq = ((bits >> q) & 1u) ? yq[q] : 0.0;  // a hidden cell's NaN is selected away
+              const double bq = g < R ? vp[(int64_t)(32 * u + 16 * h + q) * RS] : 0.0;
+              dmma(dq[q][0], dq[q][1], aq, bq);
+            }
+          }
+        }
+        yp += 32 * UW;
+        vp += (int64_t)32 * UW * RS;
+      }
+      for (; w < nwn; ++w) {
+        const unsigned word = __ldg(wr + w);
+        cnt += __popc(word);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 y0 = ld2(yp + 16 * h, pol_keep), y1 = ld2(yp + 16 * h + 2, pol_keep);
+          const unsigned bits = (word >> (16 * h + 4 * k)) & 15u;
+          const double yq[4] = {y0.x, y0.y, y1.x, y1.y};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double aq = ((bits >> q) & 1u) ? yq[q] : 0.0;
+            const double bq = g < R ? vp[(int64_t)(16 * h + q) * RS] : 0.0;
+            dmma(dq[q][0], dq[q][1], aq, bq);
+          }
+        }
+        yp += 32;
+        vp += (int64_t)32 * RS;
+      }
+    }
+    double d0 = (dq[0][0] + dq[1][0]) + (dq[2][0] + dq[3][0]);
+    double d1 = (dq[0][1] + dq[1][1]) + (dq[2][1] + dq[3][1]);
+    if constexpr (TEAM > 1) {
+      double* mine = xb + tw * 80;
+      mine[g * 8 + 2 * k] = d0;
+      mine[g * 8 + 2 * k + 1] = d1;
+      if (k == 0) mine[64 + g] = (double)cnt;
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "r"(32 * TEAM) : "memory");
+      d0 = 0.0;
+      d1 = 0.0;
+      double c = 0.0;
+#pragma unroll
+      for (int t = 0; t < TEAM; ++t) {
+        d0 += xb[t * 80 + g * 8 + 2 * k];
+        d1 += xb[t * 80 + g * 8 + 2 * k + 1];
+        c += xb[t * 80 + 64 + g];
+      }
+      cnt = (int)c;
+    }
+    // ---- the rows' solves: lane (g, k) holds b[g][2k], b[g][2k + 1] ----
+    double bv[R], A[NA], u[R];
+    const double* ap = a.Apre + rowc * NA;
+#pragma unroll
+    for (int p = 0; p < NA; ++p) A[p] = __ldg(ap + p);
+#pragma unroll
+    for (int j = 0; j < R; ++j) bv[j] = __shfl_sync(0xffffffffu, (j & 1) ? d1 : d0, (lane & ~3) + (j >> 1));
+    bool flagged = row_solve<R>(A, bv, cnt, u);
+    if (a.Ugiven) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) u[q] = a.Ugiven[rowc * R + q];
+      flagged = false;
+    }
+    // ---- pass 2: direct residual from 8 x 8 tiles of U V^T ----
+    double ua[NK];
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+      double x = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * kk + q < R && q == k) x = u[4 * kk + q];
+      ua[kk] = x;
+    }
+    double ss = 0.0;
+    {
+      const double* yp = yr + 2 * k;
+      const double* vp = Vs + (int64_t)(32 * wbase + g) * RS + k;
+      auto tiles = [&](unsigned word, const double2* y, const double* vq) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < NK; ++kk) {
+            const double bq = (4 * kk + k < R) ? vq[(int64_t)(8 * t) * RS + 4 * kk] : 0.0;
+            dmma(p0, p1, ua[kk], bq);
+          }
+          const unsigned bits = (word >> (8 * t + 2 * k)) & 3u;
+          if (bits & 1u) {
+            const double d = y[t].x - p0;
+            ss = fma(d, d, ss);
+          }
+          if (bits & 2u) {
+            const double d = y[t].y - p1;
+            ss = fma(d, d, ss);
+          }
+        }
+      };
+      int w = 0;
+      for (; w + UW <= nwn; w += UW) {
+        unsigned word[UW];
+        double2 y[UW][4];
+#pragma unroll
+        for (int u = 0; u < UW; ++u) word[u] = __ldg(wr + w + u);
+#pragma unroll
+        for (int u = 0; u < UW; ++u)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) y[u][t] = ld2(yp + 32 * u + 8 * t, pol_drop);
+#pragma unroll
+        for (int u = 0; u < UW; ++u) tiles(word[u], y[u], vp + (int64_t)(32 * u) * RS);
+        yp += 32 * UW;
+        vp += (int64_t)32 * UW * RS;
+      }
+      for (; w < nwn; ++w) {
+        const unsigned word = __ldg(wr + w);
+        double2 y[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) y[t] = ld2(yp + 8 * t, pol_drop);
+        tiles(word, y, vp);
+        yp += 32;
+        vp += (int64_t)32 * RS;
+      }
+    }
+    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+    if constexpr (TEAM > 1) {
+      if (k == 0) xb[tw * 80 + 72 + g] = ss;
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "r"(32 * TEAM) : "memory");
+      ss = 0.0;
+#pragma unroll
+      for (int t = 0; t < TEAM; ++t) ss += xb[t * 80 + 72 + g];
+    }
+    if (valid && k == 0 && tw == 0) {
+      a.rowres[row] = ss;
+#pragma unroll
+      for (int q = 0; q < R; ++q) a.U[row * R + q] = u[q];
+      if (flagged) atomicAdd(a.flagged, 1);
+    }
+  }
+}
+
 // deterministic single-CTA sum of n doubles (fixed strided order + tree)
 __global__ void k_sum_rows(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
   __shared__ double part[1024];
@@ -1378,6 +1615,52 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
     const char* e = getenv("RSM_SOLVE_U_FUSED");
     return e && atoi(e) == 0;
   }();
+  // FP64 tensor-core kernel: tensor-core normal matrices, n a multiple of 32,
+  // warps per SM limited so the 8-row blocks awaiting their second read
+  // (8 n doubles per warp) stay inside L2
+  static const int mma_mode = [] {
+    const char* e = getenv("RSM_SU_MMA");
+    return e ? atoi(e) : 1;
+  }();
+  if (a.Apre && mma_mode && (a.n % 32) == 0) {
+    constexpr int RS = R <= 4 ? 5 : 9;
+    const size_t vs = sizeof(double) * (size_t)a.n * RS;
+    if (vs <= 200 * 1024) {
+      static const int wenv = [] {
+        const char* e = getenv("RSM_SU_MMA_W");
+        return e ? atoi(e) : 0;
+      }();
+      const int64_t rows = a.row_hi - a.row_lo;
+      const int64_t nblk = (rows + 7) / 8;
+      if (mma_mode == 1 ? (a.n <= 1024) : true) {
+        // all the warps the register file holds; TEAM warps per 8-row block so the blocks awaiting
+        // their second read (8 n doubles per team) fit the L2 budget
+        constexpr int WALL = R <= 4 ? 16 : 8;
+        static const int tenv = [] {
+          const char* e = getenv("RSM_SU_MMA_TEAM");
+          return e ? atoi(e) : 0;
+        }();
+        int team = 1;
+        while (team < 4 && (double)(WALL / team) * sms * 8.0 * a.n * 8.0 > 80.0 * 1024 * 1024) team *= 2;
+        if (tenv > 0) team = tenv;
+        if ((a.n / 32) % team != 0 || WALL % team != 0) team = 1;
+        const int wt = wenv > 0 ? std::max(team, (std::min(WALL, wenv) / team) * team) : WALL;
+        const size_t smem = vs + 16 + sizeof(double) * 80 * (size_t)wt;
+        const int64_t tb = (nblk + wt / team - 1) / (wt / team);
+        const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tb, (int64_t)sms));
+#define RSM_MMA_LAUNCH(T)                                              \
+  {                                                                    \
+    ensure_smem((const void*)k_solve_u_mma<R, 4, T>, smem);            \
+    k_solve_u_mma<R, 4, T><<<gb, wt * 32, smem, s>>>(a);               \
+  }
+        if (team == 4) RSM_MMA_LAUNCH(4)
+        else if (team == 2) RSM_MMA_LAUNCH(2)
+        else RSM_MMA_LAUNCH(1)
+#undef RSM_MMA_LAUNCH
+        return;
+      }
+    }
+  }
   if (head + vbytes + 8 * per_warp <= cap) {
     // V-hat and >= 8 warps of staged rows
     if constexpr (R <= 4) {
