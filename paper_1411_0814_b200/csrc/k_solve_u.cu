@@ -1326,6 +1326,9 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+#ifndef RSM_SU_MMA_PFD
+#define RSM_SU_MMA_PFD 2
+#endif
 // TEAM warps share an 8-row block, each taking 1/TEAM of its columns: the
 // bytes a warp holds between its two passes (and so the L2 footprint of all
 // warps' blocks, which must stay below L2's capacity for the second read to
@@ -1338,6 +1341,7 @@ __global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma
   constexpr int RS = R <= 4 ? 5 : 9;
   constexpr int NA = R * (R + 1) / 2;
   constexpr int NK = (R + 3) / 4;
+  constexpr int PFD = RSM_SU_MMA_PFD;  // pass 1: steps prefetched ahead
   // UW: mask words (32 columns each) per unrolled step, 2 UW KB of a block in flight per warp
   extern __shared__ __align__(16) double Vs[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1382,6 +1386,14 @@ __global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma
       const double* vp = Vs + (int64_t)(32 * wbase + 4 * k) * RS + g;
       int w = 0;
       for (; w + UW <= nwn; w += UW) {
+        // pull the lines of the step PFD steps ahead toward L2 (no registers
+        // held): a row's 16-column group is one 128-byte line, lane k takes
+        // groups k, k + 4, ...
+        if (w + UW * (PFD + 1) <= nwn) {
+#pragma unroll
+          for (int j = 0; j < (2 * UW) / 4; ++j)
+            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(yp - 4 * k + 32 * UW * PFD + 16 * (k + 4 * j)));
+        }
         unsigned word[UW];
         double2 y[UW][2][2];
 #pragma unroll
@@ -1632,7 +1644,7 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
       }();
       const int64_t rows = a.row_hi - a.row_lo;
       const int64_t nblk = (rows + 7) / 8;
-      if (mma_mode == 1 ? (a.n <= 1024) : true) {
+      {
         // all the warps the register file holds; TEAM warps per 8-row block so the blocks awaiting
         // their second read (8 n doubles per team) fit the L2 budget
         constexpr int WALL = R <= 4 ? 16 : 8;
