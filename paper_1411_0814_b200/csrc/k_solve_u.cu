@@ -1308,15 +1308,16 @@ __global__ void __launch_bounds__(384) k_solve_u_preg(SolveUArgs a) {
 //   pass 1, b = V_O^T y: D(8 rows x 8) += A(8 x 4) B(4 x 8) per step with A
 //     the masked values and B four basis rows (columns j >= r are zero). The
 //     contraction order is free, so lane k of a row takes the four CONTIGUOUS
-//     columns 4k..4k+3 of every 16-column group (two 16-byte loads: a row's
-//     128 bytes per warp instruction pair) and step q uses column 4k + q of
-//     each lane;
+//     columns 4k..4k+3 of every 16-column group (one 256-bit load, LDG.256:
+//     a row's whole 128-byte line per warp instruction) and step q uses
+//     column 4k + q of each lane;
 //   the 8 rows are solved at once (each 4-lane group holds its row's b, count
 //     and normal matrix; no reduction anywhere: the MMA did it);
 //   pass 2, the residual: an 8 x 8 tile of U V^T per MMA (A = the rows' u, B =
-//     eight basis rows), each lane then holds two adjacent predictions of its
-//     row and reads the matching 16 bytes of Y (through L2: the block was read
-//     by pass 1 moments ago; evict_last there, evict_first here).
+//     eight basis rows chosen so that two tiles give a lane the predictions of
+//     the same four contiguous columns), read against one 256-bit load of Y
+//     (through L2: the block was read by pass 1 moments ago; evict_last there,
+//     evict_first here).
 // ~360 warp instructions per row instead of ~1370, and V-hat's shared-memory
 // reads drop to 8 B per row-column. V-hat sits in shared memory with an odd
 // row stride (5 or 9 doubles) so both fragment patterns are conflict-free.
@@ -1357,9 +1358,14 @@ __global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma
   uint64_t pol_keep, pol_drop;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
-  auto ld2 = [](const double* p, uint64_t pol) {
-    double2 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;\n" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  // one 256-bit load (LDG.256, sm_100): a lane's four contiguous columns; the four lanes of a
+  // row cover one whole 128-byte line per instruction
+  struct double4v { double x, y, z, w; };
+  auto ld4 = [](const double* p, uint64_t pol) {
+    double4v v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;\n"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p), "l"(pol));
     return v;
   };
   const int nwn = (int)(n >> 5) / TEAM;  // this warp's mask words per row (n % (32 TEAM) == 0)
@@ -1395,23 +1401,20 @@ __global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma
             asm volatile("prefetch.global.L2 [%0];\n" ::"l"(yp - 4 * k + 32 * UW * PFD + 16 * (k + 4 * j)));
         }
         unsigned word[UW];
-        double2 y[UW][2][2];
+        double4v y[UW][2];
 #pragma unroll
         for (int u = 0; u < UW; ++u) word[u] = __ldg(wr + w + u);
 #pragma unroll
         for (int u = 0; u < UW; ++u)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            y[u][h][0] = ld2(yp + 32 * u + 16 * h, pol_keep);
-            y[u][h][1] = ld2(yp + 32 * u + 16 * h + 2, pol_keep);
-          }
+          for (int h = 0; h < 2; ++h) y[u][h] = ld4(yp + 32 * u + 16 * h, pol_keep);
 #pragma unroll
         for (int u = 0; u < UW; ++u) {
           cnt += __popc(word[u]);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const unsigned bits = (word[u] >> (16 * h + 4 * k)) & 15u;
-            const double yq[4] = {y[u][h][0].x, y[u][h][0].y, y[u][h][1].x, y[u][h][1].y};
+            const double yq[4] = {y[u][h].x, y[u][h].y, y[u][h].z, y[u][h].w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const double aq = ((bits >> q) & 1u) ? yq[q] : 0.0;  // a hidden cell's NaN is selected away
@@ -1428,9 +1431,9 @@ __global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma
         cnt += __popc(word);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const double2 y0 = ld2(yp + 16 * h, pol_keep), y1 = ld2(yp + 16 * h + 2, pol_keep);
+          const double4v y4 = ld4(yp + 16 * h, pol_keep);
           const unsigned bits = (word >> (16 * h + 4 * k)) & 15u;
-          const double yq[4] = {y0.x, y0.y, y1.x, y1.y};
+          const double yq[4] = {y4.x, y4.y, y4.z, y4.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const double aq = ((bits >> q) & 1u) ? yq[q] : 0.0;
@@ -1486,24 +1489,37 @@ __global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma
     }
     double ss = 0.0;
     {
-      const double* yp = yr + 2 * k;
-      const double* vp = Vs + (int64_t)(32 * wbase + g) * RS + k;
-      auto tiles = [&](unsigned word, const double2* y, const double* vq) {
+      // the columns of a tile are free too: of a 16-column group, tile 0 takes columns
+      // {4j, 4j + 1} and tile 1 {4j + 2, 4j + 3} (j = 0..3), so lane k's two predictions of
+      // each tile are its four contiguous columns 4k..4k+3: one 256-bit load per group
+      const double* yp = yr + 4 * k;
+      const double* vp = Vs + (int64_t)(32 * wbase + 4 * (g >> 1) + (g & 1)) * RS + k;
+      auto tiles = [&](unsigned word, const double4v* y, const double* vq) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          double p0 = 0.0, p1 = 0.0;
+        for (int h = 0; h < 2; ++h) {
+          double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
           for (int kk = 0; kk < NK; ++kk) {
-            const double bq = (4 * kk + k < R) ? vq[(int64_t)(8 * t) * RS + 4 * kk] : 0.0;
-            dmma(p0, p1, ua[kk], bq);
+            const double b0 = (4 * kk + k < R) ? vq[(int64_t)(16 * h) * RS + 4 * kk] : 0.0;
+            const double b1 = (4 * kk + k < R) ? vq[(int64_t)(16 * h + 2) * RS + 4 * kk] : 0.0;
+            dmma(p0, p1, ua[kk], b0);
+            dmma(p2, p3, ua[kk], b1);
           }
-          const unsigned bits = (word >> (8 * t + 2 * k)) & 3u;
+          const unsigned bits = (word >> (16 * h + 4 * k)) & 15u;
           if (bits & 1u) {
-            const double d = y[t].x - p0;
+            const double d = y[h].x - p0;
             ss = fma(d, d, ss);
           }
           if (bits & 2u) {
-            const double d = y[t].y - p1;
+            const double d = y[h].y - p1;
+            ss = fma(d, d, ss);
+          }
+          if (bits & 4u) {
+            const double d = y[h].z - p2;
+            ss = fma(d, d, ss);
+          }
+          if (bits & 8u) {
+            const double d = y[h].w - p3;
             ss = fma(d, d, ss);
           }
         }
@@ -1511,13 +1527,13 @@ __global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma
       int w = 0;
       for (; w + UW <= nwn; w += UW) {
         unsigned word[UW];
-        double2 y[UW][4];
+        double4v y[UW][2];
 #pragma unroll
         for (int u = 0; u < UW; ++u) word[u] = __ldg(wr + w + u);
 #pragma unroll
         for (int u = 0; u < UW; ++u)
 #pragma unroll
-          for (int t = 0; t < 4; ++t) y[u][t] = ld2(yp + 32 * u + 8 * t, pol_drop);
+          for (int h = 0; h < 2; ++h) y[u][h] = ld4(yp + 32 * u + 16 * h, pol_drop);
 #pragma unroll
         for (int u = 0; u < UW; ++u) tiles(word[u], y[u], vp + (int64_t)(32 * u) * RS);
         yp += 32 * UW;
@@ -1525,9 +1541,9 @@ __global__ void __launch_bounds__((R <= 4 && UW <= 4) ? 512 : 256) k_solve_u_mma
       }
       for (; w < nwn; ++w) {
         const unsigned word = __ldg(wr + w);
-        double2 y[4];
+        double4v y[2];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) y[t] = ld2(yp + 8 * t, pol_drop);
+        for (int h = 0; h < 2; ++h) y[h] = ld4(yp + 16 * h, pol_drop);
         tiles(word, y, vp);
         yp += 32;
         vp += (int64_t)32 * RS;
@@ -1634,7 +1650,7 @@ static void launch_solve_u_r(const SolveUArgs& a, cudaStream_t s) {
     const char* e = getenv("RSM_SU_MMA");
     return e ? atoi(e) : 1;
   }();
-  if (a.Apre && mma_mode && (a.n % 32) == 0) {
+  if (a.Apre && mma_mode && (a.n % 32) == 0 && ((uintptr_t)a.Y % 32) == 0) {
     constexpr int RS = R <= 4 ? 5 : 9;
     const size_t vs = sizeof(double) * (size_t)a.n * RS;
     if (vs <= 200 * 1024) {
