@@ -214,6 +214,8 @@ constexpr int svd_cta_threads() { return M2 ? 128 : 512; }
 
 template <int K>
 __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C);
+template <int K>
+__device__ __noinline__ bool perp_basis_small(const double* Gsm, double* Q, int ldq);
 
 __device__ __forceinline__ bool it_fast(const int* flags) { return flags[3] != 0; }
 
@@ -228,6 +230,20 @@ __device__ __noinline__ bool topr_basis_rt(int K, const double* Gsm, double* C) 
     case 7: return topr_basis_small<7>(Gsm, C);
     case 8: return topr_basis_small<8>(Gsm, C);
     case 9: return topr_basis_small<9>(Gsm, C);
+    default: return false;
+  }
+}
+
+// runtime-K dispatch of perp_basis_small (column-branch CTA kernel, K = l <= 8)
+__device__ __noinline__ bool perp_basis_rt(int K, const double* Gsm, double* Q, int ldq) {
+  switch (K) {
+    case 2: return perp_basis_small<2>(Gsm, Q, ldq);
+    case 3: return perp_basis_small<3>(Gsm, Q, ldq);
+    case 4: return perp_basis_small<4>(Gsm, Q, ldq);
+    case 5: return perp_basis_small<5>(Gsm, Q, ldq);
+    case 6: return perp_basis_small<6>(Gsm, Q, ldq);
+    case 7: return perp_basis_small<7>(Gsm, Q, ldq);
+    case 8: return perp_basis_small<8>(Gsm, Q, ldq);
     default: return false;
   }
 }
@@ -409,6 +425,23 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
         }
         __syncthreads();
         if (flags[3]) break;
+      } else if (!M2 && it == 0 && a.fast_basis && a.rex == K - 1 && K >= 2 && K <= 8) {
+        // column branch, r = l - 1: the right singular vectors of the q x l
+        // submatrix are the eigenvectors of this l x l Gram, and stage 3
+        // consumes only the projector on the top r of them = I - u u^T with u
+        // the smallest eigenvector. Any orthonormal basis of u-perp serves
+        // (perp_basis_small: inverse iteration + Householder complement, one
+        // lane, no Jacobi sweeps and no rotation passes over the vectors)
+        if (tid == 0) {
+          int p = 0;
+          for (int i = 0; i < K; ++i)
+            for (int j = i; j < K; ++j) Tmp[p++] = gram[i * KMAX + j];
+          flags[3] = perp_basis_rt(K, Tmp, Vacc, KMAX) ? 1 : 0;
+          if (flags[3])
+            for (int i = 0; i < K; ++i) ord[i] = i;
+        }
+        __syncthreads();
+        if (flags[3]) break;
       } else if (it == 0 && tid == 0) {
         flags[3] = 0;
       }
@@ -476,7 +509,7 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
     }
     const bool fast = M2 && it_fast(flags);
     // descending singular values, ties by index (stable)
-    if (tid == 0 && !fast) {
+    if (tid == 0 && !it_fast(flags)) {
       for (int i = 0; i < K; ++i) ord[i] = i;
       for (int i = 1; i < K; ++i) {
         const int x = ord[i];
@@ -752,6 +785,108 @@ __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C) {
     }
 #pragma unroll
     for (int j = 0; j < R; ++j) C[i * R + j] = c[j];
+  }
+  return true;
+}
+
+// Column branch, r = l - 1: an orthonormal basis of the top-r right singular
+// subspace of the q x K submatrix A from its K x K Gram G = A^T A (packed upper
+// g). That subspace is u-perp, u the eigenvector of G's smallest eigenvalue: u
+// by the same regularised-Cholesky inverse iteration as topr_basis_small, then
+// the Householder reflection H with H u = -+e_K, whose first K - 1 columns are
+// the basis. Q (K x K, leading dimension ldq) gets those columns and u as its
+// last one. Returns false (the caller runs the one-sided Jacobi) when the
+// inverse iteration has not converged to 1e-14 in 16 steps (lambda_K /
+// lambda_{K-1} above ~0.1: no clear gap); with a gap the eigenvector's error
+// eps * lambda_1 / (lambda_{K-1} - lambda_K) is at rounding level.
+template <int K>
+__device__ __noinline__ bool perp_basis_small(const double* Gsm, double* Q, int ldq) {
+  constexpr int P = K * (K + 1) / 2;
+  auto gat = [&](int i, int j) {
+    const int lo = i < j ? i : j, hi = i < j ? j : i;
+    return Gsm[lo * K - lo * (lo - 1) / 2 + (hi - lo)];
+  };
+  double tr = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) tr += gat(i, i);
+  if (!(tr > 0.0)) return false;
+  double L[P], Li[K];
+  auto li = [](int i, int j) { return i * (i + 1) / 2 + j; };
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double d = gat(j, j);
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= L[li(j, k)] * L[li(j, k)];
+    d = fmax(d, 1e-30 * tr);
+    Li[j] = rsqrt_fast(d);
+    L[li(j, j)] = d * Li[j];
+#pragma unroll
+    for (int i = j + 1; i < K; ++i) {
+      double v = gat(i, j);
+#pragma unroll
+      for (int k = 0; k < j; ++k) v -= L[li(i, k)] * L[li(j, k)];
+      L[li(i, j)] = v * Li[j];
+    }
+  }
+  double x[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) x[i] = 1.0 + 0.25 * i;
+  bool conv = false;
+  for (int it = 0; it < 16 && !conv; ++it) {
+    double z[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double v = x[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) v -= L[li(i, k)] * z[k];
+      z[i] = v * Li[i];
+    }
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+      double v = z[i];
+#pragma unroll
+      for (int k = i + 1; k < K; ++k) v -= L[li(k, i)] * z[k];
+      z[i] = v * Li[i];
+    }
+    double nz = 0.0, dot = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) nz += z[i] * z[i];
+    nz = rsqrt_fast(nz);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      z[i] *= nz;
+      dot += z[i] * x[i];
+    }
+    double diff = 0.0;
+    const double sg = dot >= 0.0 ? 1.0 : -1.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) diff = fmax(diff, fabs(z[i] - sg * x[i]));
+    if (it > 0 && diff <= 1e-14) conv = true;
+#pragma unroll
+    for (int i = 0; i < K; ++i) x[i] = z[i];
+  }
+  if (!conv) return false;
+  // one exact renormalisation (rsqrt_fast is a Newton approximation)
+  double nx = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) nx += x[i] * x[i];
+  nx = 1.0 / sqrt(nx);
+#pragma unroll
+  for (int i = 0; i < K; ++i) x[i] *= nx;
+  const double sgn = x[K - 1] >= 0.0 ? 1.0 : -1.0;
+  double v[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = x[i];
+  v[K - 1] += sgn;
+  double vv = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) vv += v[i] * v[i];
+  const double beta = 2.0 / vv;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+#pragma unroll
+    for (int j = 0; j < K - 1; ++j) Q[i * ldq + j] = (i == j ? 1.0 : 0.0) - beta * v[i] * v[j];
+    Q[i * ldq + K - 1] = x[i];
   }
   return true;
 }
