@@ -207,10 +207,83 @@ __device__ __noinline__ void cta_gather_cols(const double* __restrict__ Y, int64
   }
 }
 
+// Column branch gather with the l x l Gram accumulated on the way (the r = l - 1
+// path needs nothing else from the vectors: see perp_basis_small), nothing
+// stored. Same walk as cta_gather_cols; the per-thread partials are reduced as
+// in cta_gram_1pass (fixed order). Ends with the Gram published in `gram`
+// (the caller synchronises).
+template <int K>
+__device__ __noinline__ void cta_gather_cols_gram(const double* __restrict__ Y, int64_t n, int64_t mwp,
+                                                  const int* idx, const uint32_t* rw, double* gram,
+                                                  double* gred) {
+  constexpr int B = 4;
+  constexpr int P = K * (K + 1) / 2;
+  constexpr int NV = P <= 4 ? 4 : (P <= 8 ? 8 : (P <= 16 ? 16 : (P <= 32 ? 32 : 64)));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  int col[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) col[j] = idx[j];
+  double g[NV];
+#pragma unroll
+  for (int p = 0; p < NV; ++p) g[p] = 0.0;
+  for (int64_t w = tid; w < mwp; w += blockDim.x) {
+    uint32_t word = rw[w];
+    while (word) {
+      int64_t rows[B];
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        rows[q] = -1;
+        if (word) {
+          rows[q] = w * 32 + (__ffs(word) - 1);
+          word &= word - 1;
+        }
+      }
+      double x[B][K];
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[q][j] = rows[q] >= 0 ? __ldg(Y + rows[q] * n + col[j]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        int p = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int j = i; j < K; ++j) {
+            g[p] = fma(x[q][i], x[q][j], g[p]);
+            ++p;
+          }
+      }
+    }
+  }
+  warp_reduce_halving<NV>(g, lane);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const double t = warp_total<NV>(g, p);
+    if (lane == 0) gred[warp * P + p] = t;
+  }
+  __syncthreads();
+  if (tid < P) {
+    double t = 0.0;
+    for (int w = 0; w < nwarps; ++w) t += gred[w * P + tid];
+    int i = 0, rem = tid;
+    while (rem >= K - i) {
+      rem -= K - i;
+      ++i;
+    }
+    const int j = i + rem;
+    gram[i * KMAX + j] = t;
+    gram[j * KMAX + i] = t;
+  }
+}
+
 // threads per CTA: the column branch spreads a trial's ~q = m rho^l rows over
 // 16 warps (one trial per SM: the K x q vectors fill shared memory)
+#ifndef RSM_SVD_COL_THREADS
+#define RSM_SVD_COL_THREADS 128
+#endif
 template <bool M2>
-constexpr int svd_cta_threads() { return M2 ? 128 : 512; }
+constexpr int svd_cta_threads() { return M2 ? 128 : RSM_SVD_COL_THREADS; }
 
 template <int K>
 __device__ __noinline__ bool topr_basis_small(const double* Gsm, double* C);
@@ -249,7 +322,7 @@ __device__ __noinline__ bool perp_basis_rt(int K, const double* Gsm, double* Q, 
 }
 
 template <bool M2>
-__global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdArgs a) {
+__global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : (512 / RSM_SVD_COL_THREADS)) k_svd(SvdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nth = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
@@ -285,6 +358,7 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
   const int64_t t_end = a.sel_acc ? min(a.t_hi, (int64_t)*a.sel_acc) : a.t_hi;
   for (int64_t t = a.t_lo + blockIdx.x; t < t_end; t += gridDim.x) {
     const int64_t tl = t - a.t_lo;  // local index for outputs
+    bool colfast = false;            // column branch: basis taken straight from the gathered Gram
     if (tid < K) idx[tid] = a.t_idx[t * K + tid];
     __syncthreads();
     int64_t L;  // vector length
@@ -347,6 +421,38 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
       __syncthreads();
       L = flags[0];
       if (L > a.Lcap) continue;  // speculative launch only (uniform: L is in shared memory)
+      // r = l - 1: the right singular vectors of the q x l submatrix are the
+      // eigenvectors of its l x l Gram, and stage 3 consumes only the
+      // projector on the top r of them = I - u u^T, u the smallest
+      // eigenvector. Any orthonormal basis of u-perp serves
+      // (perp_basis_small: inverse iteration + Householder complement by one
+      // lane), so the Gram is accumulated while gathering and the vectors are
+      // never stored; without a clear gap the trial is gathered again for
+      // the one-sided Jacobi below.
+      if (a.fast_basis && a.rex == K - 1 && K >= 2 && K <= 8) {
+        switch (K) {
+          case 2: cta_gather_cols_gram<2>(a.Y, a.n, a.mwp, idx, rw, gram, gred); break;
+          case 3: cta_gather_cols_gram<3>(a.Y, a.n, a.mwp, idx, rw, gram, gred); break;
+          case 4: cta_gather_cols_gram<4>(a.Y, a.n, a.mwp, idx, rw, gram, gred); break;
+          case 5: cta_gather_cols_gram<5>(a.Y, a.n, a.mwp, idx, rw, gram, gred); break;
+          case 6: cta_gather_cols_gram<6>(a.Y, a.n, a.mwp, idx, rw, gram, gred); break;
+          case 7: cta_gather_cols_gram<7>(a.Y, a.n, a.mwp, idx, rw, gram, gred); break;
+          default: cta_gather_cols_gram<8>(a.Y, a.n, a.mwp, idx, rw, gram, gred); break;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int p = 0;
+          for (int i = 0; i < K; ++i)
+            for (int j = i; j < K; ++j) Tmp[p++] = gram[i * KMAX + j];
+          flags[3] = perp_basis_rt(K, Tmp, Vacc, KMAX) ? 1 : 0;
+          if (flags[3])
+            for (int i = 0; i < K; ++i) ord[i] = i;
+        }
+        __syncthreads();
+        colfast = flags[3] != 0;
+      }
+      if (colfast) {
+      } else
       // gather S^T (K x L): vector j = column idx[j] over surviving rows
       if (K >= 2 && K <= 8) {
         switch (K) {
@@ -370,7 +476,7 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
           ++c;
         }
       }
-      if (tid < K * K) Vacc[(tid / K) * KMAX + (tid % K)] = (tid / K == tid % K) ? 1.0 : 0.0;
+      if (!colfast && tid < K * K) Vacc[(tid / K) * KMAX + (tid % K)] = (tid / K == tid % K) ? 1.0 : 0.0;
     }
     __syncthreads();
 
@@ -379,6 +485,7 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
     // off-diagonals relative to the larger norm: this bounds the rotation of
     // the top-rex subspace (what stage 3 consumes) by ~tol * g_ii / (g_ii - g_jj)
     const double tol_ortho = 1e-14;
+    if (!colfast)
     for (int it = 0;; ++it) {
       if (K >= 2 && K <= (M2 ? 9 : 8)) {
         // one pass over the vectors: every thread accumulates all K(K+1)/2
@@ -422,23 +529,6 @@ __global__ void __launch_bounds__(svd_cta_threads<M2>(), M2 ? 3 : 1) k_svd(SvdAr
           for (int i = 0; i < K; ++i)
             for (int j = i; j < K; ++j) Tmp[p++] = gram[i * KMAX + j];
           flags[3] = topr_basis_rt(K, Tmp, W) ? 1 : 0;
-        }
-        __syncthreads();
-        if (flags[3]) break;
-      } else if (!M2 && it == 0 && a.fast_basis && a.rex == K - 1 && K >= 2 && K <= 8) {
-        // column branch, r = l - 1: the right singular vectors of the q x l
-        // submatrix are the eigenvectors of this l x l Gram, and stage 3
-        // consumes only the projector on the top r of them = I - u u^T with u
-        // the smallest eigenvector. Any orthonormal basis of u-perp serves
-        // (perp_basis_small: inverse iteration + Householder complement, one
-        // lane, no Jacobi sweeps and no rotation passes over the vectors)
-        if (tid == 0) {
-          int p = 0;
-          for (int i = 0; i < K; ++i)
-            for (int j = i; j < K; ++j) Tmp[p++] = gram[i * KMAX + j];
-          flags[3] = perp_basis_rt(K, Tmp, Vacc, KMAX) ? 1 : 0;
-          if (flags[3])
-            for (int i = 0; i < K; ++i) ord[i] = i;
         }
         __syncthreads();
         if (flags[3]) break;

@@ -697,7 +697,11 @@ HarvestOut harvest_impl(rsm_ctx* c, const View& v, const rsm_trial_params* p, ui
     c->spec_Lcap = Lpad;
     const size_t fixed = rsmk::svd_smem_fixed(cmw, m2);
     const size_t vecb = sizeof(double) * (size_t)K * Lpad;
-    const bool use_smem = fixed + vecb <= 200 * 1024;
+    static const int col_smem = [] {
+      const char* e = getenv("RSM_SVD_COL_SMEM");
+      return e ? atoi(e) : 0;
+    }();
+    const bool use_smem = fixed + vecb <= 200 * 1024 && (m2 || col_smem);
     const size_t smem = fixed + (use_smem ? vecb : 0);
     int occ = rsmk::svd_occupancy(m2, smem);
     if (occ < 1) occ = 1;

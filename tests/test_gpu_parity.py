@@ -431,3 +431,23 @@ def test_harvest_gram_pure_noise_small_gaps(k):
     vals, mask = random_masked(400, 60, 0.9, 40 + k)
     M = rsm.MaskedMatrix(400, 60, vals, mask)
     _gram_check(M, 1, k - 1, 300, k, block=k)
+
+
+@pytest.mark.parametrize("l", [3, 4, 6])
+def test_harvest_gram_column_branch_pure_noise_small_gaps(l):
+    # column branch, r = l - 1, no low-rank structure: the l x l Grams have no
+    # clear gap above their smallest eigenvalue, so the basis-from-the-Gram path
+    # (perp_basis_small) refuses most trials and they are gathered again for the
+    # one-sided Jacobi; both kinds of trial land in the same accumulator
+    vals, mask = random_masked(600, 40, 0.9, 70 + l)
+    M = rsm.MaskedMatrix(600, 40, vals, mask)
+    _gram_check(M, 0, l - 1, 200, l, block=l)
+
+
+@pytest.mark.parametrize("l,r", [(3, 2), (5, 4), (8, 7)])
+def test_harvest_gram_column_branch_gram_basis(l, r):
+    # column branch, r = l - 1 on planted low-rank data (noiseless and noisy):
+    # every trial takes the basis straight from the Gram accumulated while gathering
+    for sigma, seed in ((0.0, 5), (1e-2, 6)):
+        M = gen(3000, 64, r, 0.8, sigma, seed)
+        _gram_check(M, 0, r, 256, seed, block=l)
