@@ -277,8 +277,12 @@ __device__ __noinline__ void cta_gather_cols_gram(const double* __restrict__ Y, 
   }
 }
 
-// threads per CTA: the column branch spreads a trial's ~q = m rho^l rows over
-// 16 warps (one trial per SM: the K x q vectors fill shared memory)
+// threads per CTA: the column branch keeps a trial's vectors out of shared
+// memory (Gram accumulated while gathering; the Jacobi fallback's vectors go
+// to global scratch unless RSM_SVD_COL_SMEM=1), so four 128-thread trials
+// share an SM and one trial's serial parts hide under the others' gathers
+// (config 2: 512 threads 1.01 ms, 256 0.84, 128 0.80, 64 0.85 before the
+// Gram moved into the gather)
 #ifndef RSM_SVD_COL_THREADS
 #define RSM_SVD_COL_THREADS 128
 #endif

@@ -51,7 +51,7 @@ struct SvdArgs {
   int64_t Lpad;
   int use_smem;
   int max_outer;         // one-sided Jacobi rotations per trial (at most)
-  int fast_basis;        // row branch, r = k - 1: top-r basis from the Gram (no Jacobi)
+  int fast_basis;        // r = block - 1 (either branch): top-r basis from the Gram (no Jacobi)
   // speculative launch (decompose enqueues stages 2-5 before the selection's
   // outcome is on the host): trials at or past *sel_acc and trials whose
   // support exceeds Lcap are skipped; the host checks the selection state
